@@ -1,0 +1,333 @@
+"""bench.py — Lloyd iterations/s and distance evaluations/s of the B200 mixed-precision k-means
+hot path (BASELINE.json metric), on the synthetic workload of BASELINE.json configs[4]
+(n = 10M, d = 128, k = 1024, z-scored blobs, fp16 distance, fp32 work) unless --config says
+otherwise.
+
+A step = one kmeans_fit(X, C0, max_iter=ITERS, tol<0) through the C ABI, i.e. one pass of the
+whole hot path (normalise, prep, ITERS x {centroid prep, distance +
+argmin, update, [allreduce], finalize}, final working-precision pass) with X resident in HBM.
+value = distance evaluations per second over all ranks = n_total * k * ITERS * K / T, where T is
+the max over ranks of the CUDA-event time of K steps (barrier + synchronize on both sides).
+
+Launch: python bench.py [--gpus N --steps K --warmup W]; for N > 1 under torchrun (one rank per
+GPU, NCCL). `--impl reference` times the CPU oracle (the paper's method as a plain fp64 CPU
+program) on a bounded sample of the same workload on this box's host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Lloyd iters/s & distance evals/s at 1/2/4/8 B200; SSE/ARI vs fp64 oracle"
+UNIT = "distance evals/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c5_vq_10m")
+    ap.add_argument("--dist", default=None, help="distance precision (default: config's first)")
+    ap.add_argument("--iters", type=int, default=20, help="Lloyd iterations per step (tol < 0)")
+    ap.add_argument("--n", type=int, default=None, help="override total n (debug)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-simt", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.idx),
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def cpu_baseline(cfg, dist, norm, guard, target_s=12.0):
+    """The oracle as it stands, on this host's cores, on a bounded sample of the workload: the
+    first n_s rows, ITERS_S Lloyd iterations (tol < 0) + final pass. Returns the same metric."""
+    import oracle
+    import synth
+    work = cfg.work
+    iters = 2
+    n_s = min(cfg.n, 4096)
+    X, _, C0 = synth.make(cfg, n=max(n_s, min(cfg.n, 65536)), seed=0)
+    C0 = C0[:cfg.k]
+    t0 = time.perf_counter()
+    oracle.fit(X[:n_s], C0, work=work, dist=dist, norm=norm, guard=guard, max_iter=iters, tol=-1)
+    dt = time.perf_counter() - t0
+    # scale the sample so the timed run takes ~target_s
+    n_s2 = int(min(len(X), max(n_s, n_s * target_s / max(dt, 1e-3))))
+    t0 = time.perf_counter()
+    oracle.fit(X[:n_s2], C0, work=work, dist=dist, norm=norm, guard=guard, max_iter=iters, tol=-1)
+    dt = time.perf_counter() - t0
+    value = n_s2 * cfg.k * iters / dt
+    return {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"first {n_s2} of {cfg.n} rows, k={cfg.k}, d={cfg.d}, {iters} Lloyd "
+                      f"iterations + final pass ({dist} distance, {work} work, {norm}), "
+                      f"{dt:.2f} s", "seconds": dt}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed on host cores (rank 0 only under torchrun)."""
+    import synth
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = synth.CONFIGS[args.config]
+    dist = args.dist or cfg.dists[0]
+    norm = cfg.norms[0].replace("+guard", "")
+    guard = "+guard" in cfg.norms[0]
+    for _ in range(args.warmup):
+        cpu_baseline(cfg, dist, norm, guard, target_s=2.0)
+    vals = []
+    cb = None
+    for _ in range(args.steps):
+        cb = cpu_baseline(cfg, dist, norm, guard, target_s=8.0)
+        vals.append(cb["value"])
+    value = statistics.median(vals)
+    cb["value"] = value
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": args.config, "dist": dist, "norm": norm,
+                                            "n": cfg.n, "d": cfg.d, "k": cfg.k},
+            "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def traffic_from_profiles(workload, dist):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        d = json.load(open(p))
+        return d.get(f"{workload}:{dist}")
+    except Exception:
+        return None
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2407_12208_b200 as mpk
+    import synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = synth.CONFIGS[args.config]
+    dist = args.dist or cfg.dists[0]
+    norm = cfg.norms[0].replace("+guard", "")
+    guard = "+guard" in cfg.norms[0]
+    n_total = args.n or cfg.n
+    per = (n_total + world - 1) // world
+    r0, r1 = rank * per, min(n_total, (rank + 1) * per)
+    X, _, C0 = synth.make(cfg, n=n_total, seed=0, row_range=(r0, r1))
+    n_local, d, k = X.shape[0], cfg.d, cfg.k
+    tdt = torch.float32 if cfg.work == "fp32" else torch.float64
+    Xd = torch.from_numpy(X).cuda()
+    Cd = torch.from_numpy(C0).cuda()
+    labels = torch.empty(n_local, dtype=torch.int32, device="cuda")
+    cent = torch.empty((k, d), dtype=tdt, device="cuda")
+    flags = mpk.NORM[norm] | (mpk.KMEANS_GUARD_SCALE if guard else 0) | \
+        (mpk.KMEANS_FORCE_SIMT if args.force_simt else 0)
+    if world > 1:
+        nid = bytearray(mpk.kmeans_nccl_unique_id() if rank == 0 else bytes(128))
+        t = torch.tensor(list(nid), dtype=torch.uint8, device="cuda")
+        tdist.broadcast(t, 0)
+        h = mpk.kmeans_create_dist(n_local, d, k, cfg.work, dist, flags, bytes(t.cpu().tolist()),
+                                   world, rank)
+    else:
+        h = mpk.kmeans_create(n_local, d, k, cfg.work, dist, flags)
+    stream = torch.cuda.Stream()
+    mpk.kmeans_set_stream(h, stream.cuda_stream)
+
+    def step():
+        return mpk.kmeans_fit(h, Xd, Cd, args.iters, -1.0, labels, cent)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    mpk.kmeans_set_timing(h, True)
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    launches = 0
+    t_dist = 0.0
+    sse = None
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            rc, sse, iters = step()
+            st = mpk.kmeans_get_stats(h)
+            launches += st.n_kernel_launches
+            t_dist += st.t_dist_ms
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            tdist.barrier()
+    ms = e0.elapsed_time(e1)
+    st = mpk.stats_dict(mpk.kmeans_get_stats(h))
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tdist.all_reduce(ms_t, op=tdist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    evals = n_total * k * args.iters * args.steps
+    value = evals / (ms / 1e3)
+    iters_per_s = args.iters * args.steps / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (distance + argmin) ------------------------------
+    peaks, peak_src = load_peaks()
+    kern = st["dist_kernel"]
+    t_launch_ms = t_dist / (args.steps * args.iters)
+    flops = 2.0 * n_local * k * d
+    if kern == "tcgen05":
+        ratio = 2.0 if dist == "e5m2" else 1.0
+        peak = peaks["bf16_tflops"] * ratio
+        bound = "tensor"
+        peak_note = f"{peak_src} bf16 burst x {ratio} ({dist})"
+    else:
+        # CUDA-core FP32 FMA: 148 SMs x 128 lanes x 2 flop x max clock
+        peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        bound = "alu"
+        peak_note = "derived: 148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz"
+    achieved = flops / (t_launch_ms / 1e3) / 1e12 if t_launch_ms > 0 else None
+    roof = {"kernel": f"assign_{kern}", "bound": bound, "achieved": achieved, "peak": peak,
+            "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
+            "traffic": traffic_from_profiles(args.config, dist), "peak_source": peak_note,
+            "algorithmic_per_launch": f"2*n*k*d = {flops:.4e} flop",
+            "avg_launch_ms": t_launch_ms,
+            "share_of_step": (t_dist / ms) if ms > 0 else None}
+
+    # ---- end-to-end through the C ABI with host buffers -----------------------------------
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.from_numpy(X).pin_memory()
+        Ch = torch.from_numpy(C0).pin_memory()
+        lab_h = torch.empty(n_local, dtype=torch.int32).pin_memory()
+        cent_h = torch.empty((k, d), dtype=tdt).pin_memory()
+        mpk.kmeans_set_timing(h, False)
+        mpk.kmeans_fit(h, Xh, Ch, args.iters, -1.0, lab_h, cent_h)
+        e_steps = max(1, min(args.steps, 3))
+        if world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(e_steps):
+            mpk.kmeans_fit(h, Xh, Ch, args.iters, -1.0, lab_h, cent_h)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ems = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            tdist.all_reduce(ems, op=tdist.ReduceOp.MAX)
+        ems = float(ems.item())
+        e2e = {"value": n_total * k * args.iters * e_steps / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(X.nbytes + C0.nbytes),
+               "d2h_bytes_per_step": int(lab_h.numel() * 4 + cent_h.numel() * cent_h.element_size()
+                                         + 8), "steps": e_steps}
+
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline(cfg, dist, norm, guard)
+
+    mpk.kmeans_destroy(h)
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": dist if dist != "e5m2" else "e5m2",
+                "data": "synthetic (seeded Gaussian blobs, synth.make)",
+                "config": {"workload": args.config, "n": n_total, "d": d, "k": k,
+                           "work": cfg.work, "dist": dist, "norm": norm, "guard": guard,
+                           "lloyd_iters_per_step": args.iters,
+                           "parallelism": f"point-sharded dp{world}",
+                           "l2": "inputs larger than L2 (X fp32 %.2f GB)" % (X.nbytes * world / 1e9)
+                           if X.nbytes * world > 126e6 else "inputs smaller than L2"},
+                "lloyd_iters_per_s": iters_per_s,
+                "breakdown_ms_per_step": {
+                    "prep": st["t_prep_ms"], "loop": st["t_loop_ms"], "final": st["t_final_ms"],
+                    "dist": st["t_dist_ms"], "update": st["t_update_ms"],
+                    "allreduce": st["t_allreduce_ms"], "finalize": st["t_finalize_ms"]},
+                "dist_kernel": kern, "last_sse": sse,
+                "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

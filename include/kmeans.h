@@ -1,0 +1,195 @@
+/*
+ * kmeans.h — C ABI of the B200-native mixed-precision Lloyd k-means hot path.
+ *
+ * Method: Carson, Chen & Liu, "Computing k-means in mixed precision" (arXiv 2407.12208),
+ * /root/reference/PAPER.md. The library implements Algorithm 3 (mixed-precision k-means
+ * framework) steps 2-7 with the initial centroids C0 supplied by the caller:
+ *   step 3  assignment with the expanded distance  ||x||^2 - 2 x.c + ||c||^2  (eq:dist-eval,
+ *           PAPER.md:193-196) whose dot products run in the low precision u_l (fp16, bf16 or
+ *           q52 = OCP FP8 E5M2) with fp32 accumulation, fused with the argmin;
+ *   step 4  centroid update mu_j = (1/|S_j|) sum_{x in S_j} x (eq:center) in
+ *           the working precision u (fp32 or fp64);
+ *   step 6  stop at max_iter or when the cluster sets converge;
+ *   step 7  final assignment "computed in precision u".
+ * Optional: z-score (eq:z-norm) or min-max (image /255)
+ * normalisation first, and Algorithm 4's infinity-norm operand scaling as the
+ * low-precision overflow guard.
+ *
+ * Layout: every matrix is row-major and contiguous: X is n x d (one point per row; the paper's
+ * P = X^T), centroids are k x d. Elements of X, C0 and centroids have the WORKING
+ * precision's type (double for KMEANS_FP64, float for KMEANS_FP32). Labels are int32.
+ *
+ * Memory: pointers may be host or device (CUDA) pointers; the library detects which with
+ * cudaPointerGetAttributes and copies as needed. The caller owns every buffer it passes; the
+ * library owns everything it allocates (sized at create time from n, d, k) until destroy.
+ * Calls are blocking: outputs are valid when the call returns. A handle is not thread-safe;
+ * distinct handles are independent. No call ever falls back to a CPU implementation.
+ *
+ * Errors: 0 = OK; < 0 = error, nothing written to outputs, message via kmeans_last_error;
+ * > 0 = bitmask of KMEANS_WARN_* (results valid).
+ */
+#ifndef MPKMEANS_KMEANS_H
+#define MPKMEANS_KMEANS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct kmeans_ctx* kmeans_handle;
+
+/* Precisions (Table 1; bf16 added by the build). */
+enum kmeans_precision {
+    KMEANS_FP64 = 0, /* u = 2^-53 */
+    KMEANS_FP32 = 1, /* u = 2^-24 */
+    KMEANS_FP16 = 2, /* u = 2^-11 */
+    KMEANS_BF16 = 3, /* u = 2^-8  */
+    KMEANS_E5M2 = 4  /* u = 2^-3; the paper's quarter precision q52 */
+};
+
+/* Normalisation modes and flags (OR-able). */
+enum kmeans_flags {
+    KMEANS_NORM_NONE = 0,
+    KMEANS_NORM_MINMAX = 1,   /* (x - min) / (max - min) per feature; range 0 -> 1          */
+    KMEANS_NORM_ZSCORE = 2,   /* (x - mean) / std per feature (population std); std 0 -> 1 */
+    KMEANS_GUARD_SCALE = 0x100,
+    /* Alg 4 lines 1-5: every point and centroid is divided by its own
+       infinity norm (zero vector -> 1) in precision u before rounding to u_l, and the dot
+       product is rescaled by s_i * s_j (Alg 4 line 6). Applied to all pairs (delta = 1). */
+    KMEANS_FORCE_SIMT = 0x200
+    /* Debug/parity: use the CUDA-core distance kernel even where the tcgen05 kernel applies. */
+};
+
+enum kmeans_status {
+    KMEANS_OK = 0,
+    KMEANS_EINVAL = -1,
+    KMEANS_ENOMEM = -2,
+    KMEANS_ECUDA = -3,
+    KMEANS_ENCCL = -4,
+    KMEANS_ENODEV = -5,              /* no sm_100 device: the library never falls back to CPU */
+    KMEANS_WARN_NONFINITE = 1,       /* a low-precision cast produced +-inf / NaN (overflow)  */
+    KMEANS_WARN_EMPTY = 2,           /* some cluster was empty in some iteration (kept)       */
+    KMEANS_WARN_MAXITER = 4,         /* tol >= 0 and max_iter reached without convergence     */
+    KMEANS_WARN_UNDERFLOW = 8        /* a nonzero value rounded to zero or a subnormal in u_l  */
+};
+
+/* Per-fit observability (filled by kmeans_get_stats after kmeans_fit). */
+#define KMEANS_MAX_TRACE 1024
+typedef struct kmeans_stats {
+    int32_t iters;                       /* iterations run (assign + update pairs)          */
+    int32_t converged;                   /* 1 if stopped by a convergence test              */
+    int32_t warnings;                    /* KMEANS_WARN_* bitmask of the last fit           */
+    int32_t dist_kernel;                 /* 0 = SIMT fp64/fp32, 1 = SIMT low, 2 = tcgen05,
+                                            3 = small-d fused                               */
+    int64_t n_nonfinite;                 /* low-precision operands that became +-inf/NaN    */
+    int64_t n_underflow;                 /* nonzero operands rounded to zero/subnormal      */
+    double t_prep_ms, t_loop_ms, t_final_ms;        /* CUDA-event times of the last fit     */
+    double t_dist_ms, t_update_ms, t_finalize_ms, t_allreduce_ms; /* summed over iterations */
+    int32_t n_dist_launches;             /* distance-kernel launches in the loop            */
+    int32_t trace_len;                   /* min(iters, KMEANS_MAX_TRACE)                    */
+    double sse_t[KMEANS_MAX_TRACE];      /* per-iteration SSE_t = sum_i max(0, min_j D_ij)   */
+    double shift2_t[KMEANS_MAX_TRACE];   /* ||C_{t+1} - C_t||_F^2                            */
+    int64_t changed_t[KMEANS_MAX_TRACE]; /* labels that changed in iteration t              */
+    int32_t empty_t[KMEANS_MAX_TRACE];   /* empty clusters in iteration t                   */
+    int64_t n_kernel_launches;           /* kernels this library launched during the fit    */
+} kmeans_stats;
+
+/*
+ * kmeans_create — allocate a handle for n points of dimension d and k clusters.
+ *   work_prec in {FP64, FP32}; dist_prec in {FP64, FP32, FP16, BF16, E5M2} with
+ *   0 < u <= u_l: FP64 work allows every dist; FP32 work allows all but FP64.
+ *   dist_prec == work_prec is the working-precision k-means (Alg 2 with C0 given);
+ *   lower dist_prec is mp_k-means++_low (Alg 3).
+ *   flags = one KMEANS_NORM_* | optional KMEANS_GUARD_SCALE | optional KMEANS_FORCE_SIMT.
+ * Errors: EINVAL if n < 1, d < 1, k < 1, k > n, an unknown enum, or a NULL out; ENODEV without
+ * an sm_100 GPU; ENOMEM if device allocations fail. The current CUDA device at call time is the
+ * device the handle uses for its lifetime.
+ */
+int kmeans_create(int64_t n, int32_t d, int32_t k, int work_prec, int dist_prec, int flags,
+                  kmeans_handle* out);
+
+/*
+ * kmeans_fit — Alg 3 steps 2-7 from C0.
+ *   X: n x d working-precision points (host or device). C0: k x d initial centroids.
+ *   max_iter >= 1. tol >= 0: stop when no label changed or ||C_{t+1} - C_t||_F <= tol;
+ *   tol < 0: run exactly max_iter iterations (bench mode).
+ *   Outputs (any may be NULL except sse's target when non-NULL is wanted): labels[n] of the final
+ *   working-precision assignment (Alg 3 step 7), centroids k x d (working type), *sse = the
+ *   final SSE (eq:sse via the direct formula eq:dist-eval-alternative, PAPER.md:189-192,
+ *   accumulated in fp64), *iters = iterations run.
+ *   With normalisation on, X and C0 are in original coordinates and the centroids and SSE are
+ *   returned in the normalised space (as the paper's "(normalized)" columns);
+ *   kmeans_get_transform gives the map.
+ * Returns 0, a KMEANS_WARN_* mask, or an error.
+ */
+int kmeans_fit(kmeans_handle h, const void* X, const void* C0, int32_t max_iter, double tol,
+               int32_t* labels, void* centroids, double* sse, int32_t* iters);
+
+/*
+ * kmeans_assign — the standalone distance + argmin kernel in dist_prec with the handle's current
+ * centroids (after a fit or kmeans_set_centroids; EINVAL before either). X: m x d working
+ * precision points in ORIGINAL coordinates (the handle's stored transform is applied), any m >= 1
+ * (processed in chunks of at most n rows). labels[m] receives argmin_j of the expanded distance
+ * (lowest j on ties, NaN never selected). If sse != NULL, *sse = sum_i max(0, min_j D_ij).
+ */
+int kmeans_assign(kmeans_handle h, const void* X, int64_t m, int32_t* labels, double* sse);
+
+/* kmeans_set_centroids — overwrite the handle's centroids (k x d, working type, normalised
+ * space). kmeans_get_centroids — read them back. */
+int kmeans_set_centroids(kmeans_handle h, const void* C);
+int kmeans_get_centroids(kmeans_handle h, void* C);
+
+/* kmeans_get_transform — shift[d], scale[d] (working type) of the last fit's normalisation:
+ * x_normalised = round_u((x - shift) / scale). Identity (0, 1) without normalisation. */
+int kmeans_get_transform(kmeans_handle h, void* shift, void* scale);
+
+/* kmeans_get_stats — copy the last fit's statistics (see kmeans_stats). */
+int kmeans_get_stats(kmeans_handle h, kmeans_stats* out);
+
+/* kmeans_set_stream — run all of the handle's work on this cudaStream_t (NULL = the handle's
+ * own stream). The caller keeps ownership of the stream. */
+int kmeans_set_stream(kmeans_handle h, void* cuda_stream);
+
+/* kmeans_set_timing — 1 = record CUDA events around every kernel of the loop (per-kernel times
+ * in kmeans_stats), 0 = only the prep / loop / final events (default). */
+int kmeans_set_timing(kmeans_handle h, int enable);
+
+/* kmeans_destroy — free the handle (NULL is a no-op returning 0). */
+int kmeans_destroy(kmeans_handle h);
+
+/* kmeans_last_error — handle-local message for the last nonzero return (NULL handle: the
+ * message of the last failed kmeans_create on this thread). Never NULL. */
+const char* kmeans_last_error(kmeans_handle h);
+
+/*
+ * kmeans_cast — the operand-rounding kernel on its own (Table 1 formats):
+ * dst[i] = round_{dst_prec}(src[i]) with one round-to-nearest-even step from the source value,
+ * gradual underflow, and IEEE overflow to +-inf (never saturation). src_prec in {FP64, FP32},
+ * dst_prec in {FP32, FP16, BF16, E5M2} (element sizes 4, 2, 2, 1 bytes). src and dst must be
+ * DEVICE pointers to count elements. Returns 0 or an error.
+ */
+int kmeans_cast(int src_prec, int dst_prec, const void* src, int64_t count, void* dst);
+
+/*
+ * kmeans_create_dist — like kmeans_create for one rank of a point-sharded run: this rank holds
+ * n_local rows; all ranks hold the same C0. nccl_unique_id points to the 128-byte ncclUniqueId
+ * created by rank 0 and broadcast by the caller. Each iteration the packed partial sums,
+ * counts, SSE and changed-label count are combined with ONE ncclAllReduce over NVLink, so every
+ * rank computes identical centroids. kmeans_fit must be called collectively; X/labels are the
+ * local shard; centroids, sse and iters are identical on every rank (sse is global).
+ */
+int kmeans_create_dist(int64_t n_local, int32_t d, int32_t k, int work_prec, int dist_prec,
+                       int flags, const void* nccl_unique_id, int nranks, int rank,
+                       kmeans_handle* out);
+
+/* kmeans_nccl_unique_id — write a fresh 128-byte ncclUniqueId (call on rank 0 only). */
+int kmeans_nccl_unique_id(void* out128);
+
+/* kmeans_version — library version string. */
+const char* kmeans_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPKMEANS_KMEANS_H */

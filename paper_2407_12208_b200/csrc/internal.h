@@ -1,0 +1,118 @@
+// internal.h — handle state and kernel launchers (C++; never crosses the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/kmeans.h"
+
+namespace mpk {
+
+// Number of kernels this library launched (process-wide); reported per fit in kmeans_stats.
+long long launches_read();
+void launches_add(int n);
+
+// Packed per-iteration accumulator (fp64): [sums k*d][counts k][sse][changed][nonfinite][pad]
+// One ncclAllReduce over this buffer is the only per-iteration cross-GPU exchange.
+#ifdef __CUDACC__
+#define MPK_HD __host__ __device__ __forceinline__
+#else
+#define MPK_HD inline
+#endif
+struct AccLayout {
+    int64_t k, d;
+    MPK_HD int64_t sums() const { return 0; }
+    MPK_HD int64_t counts() const { return k * d; }
+    MPK_HD int64_t sse() const { return k * d + k; }
+    MPK_HD int64_t changed() const { return k * d + k + 1; }
+    MPK_HD int64_t nonfinite() const { return k * d + k + 2; }
+    MPK_HD int64_t total() const { return k * d + k + 4; }
+};
+
+// Per-iteration trace record (device), one per iteration: sse, shift2, changed, empty.
+struct IterRec {
+    double sse;
+    double shift2;
+    double changed;
+    double empty;
+};
+
+// Device-side problem description passed to kernels by value.
+struct Problem {
+    int64_t n;      // rows in this launch
+    int d;          // features
+    int k;          // clusters
+    int d_pad;      // row stride (elements) of the low-precision operand arrays
+    int guard;      // Alg 4 scaling on
+};
+
+enum DistKernel { DK_SIMT_WORK = 0, DK_SIMT_LOW = 1, DK_TCGEN05 = 2, DK_SMALLD = 3 };
+
+// ------------------------------------------------------------------------------------------
+// Launchers (each returns cudaError_t of the launch).
+// ------------------------------------------------------------------------------------------
+
+// K2: per-feature statistics of X (fp64, compensated partials combined in block order).
+//   ZSCORE: a = sum_i x_ic; then launch_norm_ssq: ssq = sum_i (x_ic - mean_c)^2.
+//   MINMAX: a = min, b = max. Multi-GPU: the aggregates are allreduced before launch_norm_post.
+//   launch_norm_post mode 0: shift = a / n; 1: scale = sqrt(ssq / n) (0 -> 1);
+//   2: scale = max - min (0 -> 1). launch_norm_apply: x = round_u((x - shift) / scale).
+cudaError_t launch_norm_stats(int work, int norm, const void* X, int64_t n, int d,
+                              double* partials, int nblocks, double* a, double* b,
+                              cudaStream_t s);
+cudaError_t launch_norm_ssq(int work, const void* X, int64_t n, int d, double* partials,
+                            int nblocks, const double* mean, double* ssq, cudaStream_t s);
+cudaError_t launch_norm_post(int mode, int d, double n_total, double* shift, double* scale,
+                             cudaStream_t s);
+cudaError_t launch_norm_apply(int work, void* X, int64_t rows, int d, const double* shift,
+                              const double* scale, cudaStream_t s);
+int norm_stats_blocks(int64_t n, int d);
+
+// K1 / K3: norms (fp64 -> work), guard scales, low-precision operands with padding, census.
+cudaError_t launch_prep(int work, int dist, const void* Xw, int64_t rows, int d, int d_pad,
+                        int guard, void* norms, void* scales, void* Xl,
+                        unsigned long long* census /* [nonfinite, underflow] */, cudaStream_t s);
+
+// kmeans_cast kernel.
+cudaError_t launch_cast(int src, int dst, const void* in, int64_t count, void* out,
+                        cudaStream_t s);
+
+// K6: SIMT distance + argmin (any precision). Writes labels; if labels_prev path: counts
+// changed labels into acc[changed], adds sum_i max(0, xn_i + min_j v_ij) into acc[sse].
+// final_mode: operands are the working-precision X/C (Alg 3 step 7) and sse_direct gets the
+// direct-formula SSE sum_i ||x_i - c_{l_i}||^2 (eq:dist-eval-alternative).
+cudaError_t launch_assign_simt(int work, int dist, const Problem& p, const void* Xl,
+                               const void* xn, const void* sx, const void* Cl, const void* cn,
+                               const void* sc, int32_t* labels, double* acc_sse,
+                               double* acc_changed, cudaStream_t s);
+cudaError_t launch_final_sse(int work, const void* Xw, int64_t n, int d, const void* Cw,
+                             const int32_t* labels, double* sse_out, cudaStream_t s);
+
+// K5: small-d fused assign + update (d <= 4, k <= 8).
+bool smalld_supported(int d, int k);
+cudaError_t launch_smalld_fused(int work, int dist, const Problem& p, const void* Xw,
+                                const void* Cl, const void* cn, const void* sc, int32_t* labels,
+                                double* acc, AccLayout L, cudaStream_t s);
+
+// K4: tcgen05 distance + argmin (fp16 / bf16 / e5m2 operands).
+bool tc_supported(int dist, int d_pad, int k);
+int tc_dpad(int dist, int d);   // padded row length (elements) the tcgen05 kernel needs
+struct TcPlan;                  // opaque (TMA descriptors etc.)
+TcPlan* tc_plan_create(int dist, int64_t n, int d, int d_pad, int k, const void* Xl,
+                       const void* Cl, std::string* err);
+void tc_plan_destroy(TcPlan*);
+cudaError_t launch_assign_tc(TcPlan* plan, const Problem& p, const float* xn, const float* sx,
+                             const float* cn, const float* sc, int32_t* labels, double* acc_sse,
+                             double* acc_changed, cudaStream_t s);
+
+// K7: update = bucket by label (count, scan, scatter) + segmented fp64 sums.
+cudaError_t launch_update(int work, const void* Xw, int64_t n, int d, int k,
+                          const int32_t* labels, int* cnt, int* offs, int* cursor, int* perm,
+                          double* acc, AccLayout L, cudaStream_t s);
+
+// K8: finalize: C = round_u(sum / count) (empty -> keep), shift^2, empty count, trace record.
+cudaError_t launch_finalize(int work, int64_t k, int d, const double* acc, AccLayout L,
+                            void* Cw, IterRec* rec, cudaStream_t s);
+
+}  // namespace mpk

@@ -1,0 +1,407 @@
+// k_assign_simt.cu — CUDA-core distance + argmin kernels.
+//
+// K6  assign_simt: generic register-tiled kernel for every precision pair. The operands are the
+//     stored low-precision values widened exactly to the accumulation type; the dot product
+//     x~_i . c~_j accumulates in fp32 FMA for fp32/fp16/bf16/E5M2 operands (the tensor-core
+//     model of reading Z2/Z3) and in fp64 for fp64 operands. Epilogue (working precision):
+//         v_ij = fma(-2 s_i s_j, dot_ij, ||c_j||^2)        (eq:dist-eval, PAPER.md:193-196;
+//                                                           Alg 4 line 6)
+//     ||x_i||^2 is row-constant and is added only to the minimum (SSE_t). Running argmin over
+//     j with (value, index) ordering: lowest j on ties, NaN never wins (readings Z12, Z13).
+//     Also the final working-precision assignment (Alg 3 step 7).
+// K5  smalld_fused: d <= 4, k <= 8 (image segmentation): one pass over X
+//     in working precision per iteration computes x~ on the fly, assigns, and accumulates the
+//     per-cluster sums in fp64 registers -> warp shuffles -> block smem -> one global fp64
+//     atomic per (block, value): the update of eq:center fused in.
+// K10 final_sse: sum_i ||x_i - c_{l_i}||^2 by the direct formula (eq:dist-eval-alternative,
+//     PAPER.md:189-192) in fp64.
+#include "common.cuh"
+#include "internal.h"
+
+namespace mpk {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 32, NT = 256;
+
+template <typename LT, typename AT, typename W>
+__global__ void __launch_bounds__(NT)
+assign_simt_kernel(Problem p, const LT* __restrict__ Xl, const W* __restrict__ xn,
+                   const W* __restrict__ sx, const LT* __restrict__ Cl,
+                   const W* __restrict__ cn, const W* __restrict__ sc,
+                   int32_t* __restrict__ labels, double* acc_sse, double* acc_changed) {
+    __shared__ AT Xs[BK][BM];
+    __shared__ AT Cs[BK][BN];
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;
+    const int64_t row0 = (int64_t)blockIdx.x * BM;
+
+    W bestv[4];
+    int bestj[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) { bestv[r] = (W)INFINITY; bestj[r] = 0; }
+    W srow[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        int64_t row = row0 + ty * 4 + r;
+        srow[r] = (p.guard && sx && row < p.n) ? sx[row] : (W)1;
+    }
+
+    for (int n0 = 0; n0 < p.k; n0 += BN) {
+        AT acc[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[r][c] = (AT)0;
+        for (int k0 = 0; k0 < p.d; k0 += BK) {
+#pragma unroll
+            for (int e = 0; e < (BM * BK) / NT; ++e) {
+                int idx = tid + e * NT;
+                int r = idx / BK, kk = idx % BK;
+                int64_t row = row0 + r;
+                int col = k0 + kk;
+                AT v = (AT)0;
+                if (row < p.n && col < p.d) v = (AT)widen(Xl[row * p.d_pad + col]);
+                Xs[kk][r] = v;
+                int cj = n0 + r;
+                AT w = (AT)0;
+                if (cj < p.k && col < p.d) w = (AT)widen(Cl[(int64_t)cj * p.d_pad + col]);
+                Cs[kk][r] = w;
+            }
+            __syncthreads();
+#pragma unroll 8
+            for (int kk = 0; kk < BK; ++kk) {
+                AT a[4], b[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) a[r] = Xs[kk][ty * 4 + r];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) b[c] = Cs[kk][tx * 4 + c];
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[r][c] = fma(a[r], b[c], acc[r][c]);
+            }
+            __syncthreads();
+        }
+        // epilogue for this centroid tile: ascending j per thread
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            int j = n0 + tx * 4 + c;
+            if (j < p.k) {
+                W cnj = cn[j];
+                W scj = (p.guard && sc) ? sc[j] : (W)1;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    W m2 = (W)-2 * (srow[r] * scj);
+                    W v = fma(m2, (W)acc[r][c], cnj);
+                    if (v < bestv[r]) { bestv[r] = v; bestj[r] = j; }
+                }
+            }
+        }
+    }
+    // reduce across the 16 threads (tx) that share rows: lanes ty*16 .. ty*16+15
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+            W v2 = __shfl_xor_sync(0xffffffffu, bestv[r], o);
+            int j2 = __shfl_xor_sync(0xffffffffu, bestj[r], o);
+            argmin_merge(bestv[r], bestj[r], v2, j2);
+        }
+    }
+    double my_sse = 0.0, my_changed = 0.0;
+    if (tx == 0) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            int64_t row = row0 + ty * 4 + r;
+            if (row < p.n) {
+                if (acc_changed && labels[row] != bestj[r]) my_changed += 1.0;
+                labels[row] = bestj[r];
+                if (acc_sse) {
+                    double md = (double)xn[row] + (double)bestv[r];
+                    my_sse += md > 0.0 ? md : 0.0;
+                }
+            }
+        }
+    }
+    if (acc_sse || acc_changed) {
+        my_sse = warp_sum(my_sse);
+        my_changed = warp_sum(my_changed);
+        __shared__ double red[2][NT / 32];
+        if ((tid & 31) == 0) { red[0][tid >> 5] = my_sse; red[1][tid >> 5] = my_changed; }
+        __syncthreads();
+        if (tid == 0) {
+            double a = 0, b = 0;
+            for (int w = 0; w < NT / 32; ++w) { a += red[0][w]; b += red[1][w]; }
+            if (acc_sse) atomicAdd(acc_sse, a);
+            if (acc_changed && b != 0.0) atomicAdd(acc_changed, b);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K5 small-d fused assign + update.
+// ------------------------------------------------------------------------------------------
+constexpr int SD_D = 4, SD_K = 8, SD_T = 256;
+
+template <typename W, int DIST>
+__global__ void __launch_bounds__(SD_T)
+smalld_kernel(Problem p, const W* __restrict__ X, const typename low_type<DIST>::T* __restrict__ Cl,
+              const W* __restrict__ cn, const W* __restrict__ sc, int32_t* __restrict__ labels,
+              double* __restrict__ acc, AccLayout L) {
+    using AT = typename std::conditional<DIST == KMEANS_FP64, double, float>::type;
+    constexpr int WORK = sizeof(W) == 8 ? KMEANS_FP64 : KMEANS_FP32;
+    constexpr bool same = (DIST == WORK);
+    __shared__ AT cl_s[SD_K][SD_D];
+    __shared__ W cn_s[SD_K], sc_s[SD_K];
+    const int tid = threadIdx.x;
+    if (tid < SD_K * SD_D) {
+        int j = tid / SD_D, t = tid % SD_D;
+        cl_s[j][t] = (j < p.k && t < p.d) ? (AT)widen(Cl[(int64_t)j * p.d_pad + t]) : (AT)0;
+    }
+    if (tid < SD_K) {
+        cn_s[tid] = tid < p.k ? cn[tid] : (W)0;
+        sc_s[tid] = (tid < p.k && p.guard && sc) ? sc[tid] : (W)1;
+    }
+    __syncthreads();
+
+    double sums[SD_K][SD_D];
+    double cnts[SD_K];
+#pragma unroll
+    for (int j = 0; j < SD_K; ++j) {
+        cnts[j] = 0.0;
+#pragma unroll
+        for (int t = 0; t < SD_D; ++t) sums[j][t] = 0.0;
+    }
+    double my_sse = 0.0, my_changed = 0.0;
+
+    for (int64_t i = (int64_t)blockIdx.x * SD_T + tid; i < p.n; i += (int64_t)gridDim.x * SD_T) {
+        W x[SD_D];
+        double nrm = 0.0, amax = 0.0;
+#pragma unroll
+        for (int t = 0; t < SD_D; ++t) {
+            x[t] = t < p.d ? X[i * p.d + t] : (W)0;
+            double v = (double)x[t];
+            nrm = __dadd_rn(nrm, __dmul_rn(v, v));
+            amax = fmax(amax, fabs(v));
+        }
+        W xn = rounder<WORK>::from(nrm);
+        W s = (W)1;
+        if (p.guard && !same) s = (amax == 0.0 || isnan(amax)) ? (W)1 : (W)amax;
+        AT xl[SD_D];
+#pragma unroll
+        for (int t = 0; t < SD_D; ++t) {
+            W q = (s == (W)1) ? x[t] : x[t] / s;
+            xl[t] = (AT)widen(rounder<DIST>::from(q));
+        }
+        W best = (W)INFINITY;
+        int bj = 0;
+#pragma unroll
+        for (int j = 0; j < SD_K; ++j) {
+            if (j < p.k) {
+                AT dot = (AT)0;
+#pragma unroll
+                for (int t = 0; t < SD_D; ++t) dot = fma(xl[t], cl_s[j][t], dot);
+                W v = fma((W)-2 * (s * sc_s[j]), (W)dot, cn_s[j]);
+                if (v < best) { best = v; bj = j; }
+            }
+        }
+        if (labels[i] != bj) my_changed += 1.0;
+        labels[i] = bj;
+        double md = (double)xn + (double)best;
+        my_sse += md > 0.0 ? md : 0.0;
+#pragma unroll
+        for (int j = 0; j < SD_K; ++j) {
+            const bool hit = (bj == j);
+            cnts[j] += hit ? 1.0 : 0.0;
+#pragma unroll
+            for (int t = 0; t < SD_D; ++t) sums[j][t] += hit ? (double)x[t] : 0.0;
+        }
+    }
+    // warp -> block -> global
+    constexpr int NV = SD_K * SD_D + SD_K + 2;
+    __shared__ double red[SD_T / 32][NV];
+    const int lane = tid & 31, w = tid >> 5;
+#pragma unroll
+    for (int j = 0; j < SD_K; ++j) {
+#pragma unroll
+        for (int t = 0; t < SD_D; ++t) {
+            double v = warp_sum(sums[j][t]);
+            if (lane == 0) red[w][j * SD_D + t] = v;
+        }
+        double c = warp_sum(cnts[j]);
+        if (lane == 0) red[w][SD_K * SD_D + j] = c;
+    }
+    my_sse = warp_sum(my_sse);
+    my_changed = warp_sum(my_changed);
+    if (lane == 0) { red[w][NV - 2] = my_sse; red[w][NV - 1] = my_changed; }
+    __syncthreads();
+    if (tid < NV) {
+        double a = 0.0;
+        for (int q = 0; q < SD_T / 32; ++q) a += red[q][tid];
+        double* dst = nullptr;
+        if (tid < SD_K * SD_D) {
+            int j = tid / SD_D, t = tid % SD_D;
+            if (j < p.k && t < p.d) dst = acc + L.sums() + (int64_t)j * p.d + t;
+        } else if (tid < SD_K * SD_D + SD_K) {
+            int j = tid - SD_K * SD_D;
+            if (j < p.k) dst = acc + L.counts() + j;
+        } else if (tid == NV - 2) {
+            dst = acc + L.sse();
+        } else {
+            dst = acc + L.changed();
+        }
+        if (dst && a != 0.0) atomicAdd(dst, a);
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K10 final SSE, direct formula in fp64: one warp per row.
+// ------------------------------------------------------------------------------------------
+template <typename W>
+__global__ void final_sse_kernel(const W* __restrict__ X, int64_t n, int d,
+                                 const W* __restrict__ C, const int32_t* __restrict__ labels,
+                                 double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double acc = 0.0;
+    for (int64_t i = warp; i < n; i += nwarps) {
+        const W* x = X + i * d;
+        const W* c = C + (int64_t)labels[i] * d;
+        double a = 0.0;
+        for (int t = lane; t < d; t += 32) {
+            double df = (double)x[t] - (double)c[t];
+            a = fma(df, df, a);
+        }
+        acc += a;
+    }
+    acc = warp_sum(acc);
+    __shared__ double red[8];
+    if (lane == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += red[w];
+        atomicAdd(out, a);
+    }
+}
+
+template <typename LT, typename W>
+cudaError_t simt_dispatch_acc(int dist, const Problem& p, const void* Xl, const void* xn,
+                              const void* sx, const void* Cl, const void* cn, const void* sc,
+                              int32_t* labels, double* acc_sse, double* acc_changed,
+                              cudaStream_t s) {
+    int64_t blocks = (p.n + BM - 1) / BM;
+    if (blocks == 0) return cudaSuccess;
+    if (dist == KMEANS_FP64)
+        assign_simt_kernel<LT, double, W><<<(unsigned)blocks, NT, 0, s>>>(
+            p, (const LT*)Xl, (const W*)xn, (const W*)sx, (const LT*)Cl, (const W*)cn,
+            (const W*)sc, labels, acc_sse, acc_changed);
+    else
+        assign_simt_kernel<LT, float, W><<<(unsigned)blocks, NT, 0, s>>>(
+            p, (const LT*)Xl, (const W*)xn, (const W*)sx, (const LT*)Cl, (const W*)cn,
+            (const W*)sc, labels, acc_sse, acc_changed);
+    return cudaGetLastError();
+}
+
+template <typename W>
+cudaError_t simt_dispatch(int dist, const Problem& p, const void* Xl, const void* xn,
+                          const void* sx, const void* Cl, const void* cn, const void* sc,
+                          int32_t* labels, double* acc_sse, double* acc_changed,
+                          cudaStream_t s) {
+    switch (dist) {
+        case KMEANS_FP64:
+            return simt_dispatch_acc<double, W>(dist, p, Xl, xn, sx, Cl, cn, sc, labels, acc_sse,
+                                                acc_changed, s);
+        case KMEANS_FP32:
+            return simt_dispatch_acc<float, W>(dist, p, Xl, xn, sx, Cl, cn, sc, labels, acc_sse,
+                                               acc_changed, s);
+        case KMEANS_FP16:
+            return simt_dispatch_acc<__half, W>(dist, p, Xl, xn, sx, Cl, cn, sc, labels, acc_sse,
+                                                acc_changed, s);
+        case KMEANS_BF16:
+            return simt_dispatch_acc<__nv_bfloat16, W>(dist, p, Xl, xn, sx, Cl, cn, sc, labels,
+                                                       acc_sse, acc_changed, s);
+        case KMEANS_E5M2:
+            return simt_dispatch_acc<e5m2_t, W>(dist, p, Xl, xn, sx, Cl, cn, sc, labels, acc_sse,
+                                                acc_changed, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <typename W>
+cudaError_t smalld_dispatch(int dist, const Problem& p, const W* X, const void* Cl,
+                            const W* cn, const W* sc, int32_t* labels, double* acc, AccLayout L,
+                            cudaStream_t s) {
+    int64_t want = (p.n + SD_T * 4 - 1) / (SD_T * 4);
+    int grid = (int)(want < 1 ? 1 : (want > kNumSMs * 4 ? kNumSMs * 4 : want));
+    switch (dist) {
+        case KMEANS_FP64:
+            smalld_kernel<W, KMEANS_FP64><<<grid, SD_T, 0, s>>>(p, X, (const double*)Cl, cn, sc,
+                                                                labels, acc, L);
+            break;
+        case KMEANS_FP32:
+            smalld_kernel<W, KMEANS_FP32><<<grid, SD_T, 0, s>>>(p, X, (const float*)Cl, cn, sc,
+                                                                labels, acc, L);
+            break;
+        case KMEANS_FP16:
+            smalld_kernel<W, KMEANS_FP16><<<grid, SD_T, 0, s>>>(p, X, (const __half*)Cl, cn, sc,
+                                                                labels, acc, L);
+            break;
+        case KMEANS_BF16:
+            smalld_kernel<W, KMEANS_BF16><<<grid, SD_T, 0, s>>>(
+                p, X, (const __nv_bfloat16*)Cl, cn, sc, labels, acc, L);
+            break;
+        case KMEANS_E5M2:
+            smalld_kernel<W, KMEANS_E5M2><<<grid, SD_T, 0, s>>>(p, X, (const e5m2_t*)Cl, cn, sc,
+                                                                labels, acc, L);
+            break;
+        default:
+            return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_assign_simt(int work, int dist, const Problem& p, const void* Xl,
+                               const void* xn, const void* sx, const void* Cl, const void* cn,
+                               const void* sc, int32_t* labels, double* acc_sse,
+                               double* acc_changed, cudaStream_t s) {
+    launches_add(1);
+    if (work == KMEANS_FP64)
+        return simt_dispatch<double>(dist, p, Xl, xn, sx, Cl, cn, sc, labels, acc_sse,
+                                     acc_changed, s);
+    return simt_dispatch<float>(dist, p, Xl, xn, sx, Cl, cn, sc, labels, acc_sse, acc_changed,
+                                s);
+}
+
+bool smalld_supported(int d, int k) { return d <= SD_D && k <= SD_K; }
+
+cudaError_t launch_smalld_fused(int work, int dist, const Problem& p, const void* Xw,
+                                const void* Cl, const void* cn, const void* sc, int32_t* labels,
+                                double* acc, AccLayout L, cudaStream_t s) {
+    launches_add(1);
+    if (work == KMEANS_FP64)
+        return smalld_dispatch<double>(dist, p, (const double*)Xw, Cl, (const double*)cn,
+                                       (const double*)sc, labels, acc, L, s);
+    return smalld_dispatch<float>(dist, p, (const float*)Xw, Cl, (const float*)cn,
+                                  (const float*)sc, labels, acc, L, s);
+}
+
+cudaError_t launch_final_sse(int work, const void* Xw, int64_t n, int d, const void* Cw,
+                             const int32_t* labels, double* sse_out, cudaStream_t s) {
+    launches_add(1);
+    int64_t want = (n * 32 + 255) / 256;
+    int grid = (int)(want < 1 ? 1 : (want > kNumSMs * 8 ? kNumSMs * 8 : want));
+    if (work == KMEANS_FP64)
+        final_sse_kernel<double><<<grid, 256, 0, s>>>((const double*)Xw, n, d, (const double*)Cw,
+                                                     labels, sse_out);
+    else
+        final_sse_kernel<float><<<grid, 256, 0, s>>>((const float*)Xw, n, d, (const float*)Cw,
+                                                    labels, sse_out);
+    return cudaGetLastError();
+}
+
+}  // namespace mpk

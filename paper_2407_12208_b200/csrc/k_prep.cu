@@ -1,0 +1,381 @@
+// k_prep.cu — K2 normalisation, K1/K3 operand preparation, and the standalone cast kernel.
+//
+// K2 (one-time): per-feature statistics in fp64 with compensated (Neumaier) partial sums, then
+//   x <- round_u((x - shift) / scale) in place. ZSCORE: eq:z-norm, population
+//   sigma, sigma = 0 -> 1. MINMAX: (x - min) / (max - min), range 0 -> 1; on 0..255-spanning
+//   images this is the paper's "divided by 255".
+// K1/K3: per row, ||x||^2 summed in fp64 and stored in precision u; with the
+//   guard, s = ||x||_inf and x~ = round_l(round_u(x / s)) (Alg 4 lines 1-5);
+//   without, x~ = round_l(x). Rows are padded with zeros to the kernel's row stride (exact:
+//   zero columns add nothing to a dot product). Overflowed (+-inf/NaN) and underflowed
+//   (nonzero -> zero/subnormal) operands are counted (readings Z7, Z8).
+// HBM-bound: one warp per row, lanes over columns (coalesced), grid = a multiple of 148 SMs.
+#include "common.cuh"
+#include "internal.h"
+
+namespace mpk {
+
+namespace {
+
+constexpr int kStatThreads = 256;
+
+template <typename W>
+__global__ void norm_stats_kernel(int norm, const W* __restrict__ X, int64_t n, int d,
+                                  double* __restrict__ partials /* [nblocks][d][2] */) {
+    // Thread layout: column c = tid % d, row lane r = tid / d (d <= 256), else column loop.
+    const int tid = threadIdx.x;
+    const int lanes = d <= kStatThreads ? kStatThreads / d : 1;
+    const int64_t rows_per_block = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
+    const int64_t r1 = min(n, r0 + rows_per_block);
+    __shared__ double sh_s[kStatThreads], sh_c[kStatThreads];
+    for (int cbase = 0; cbase < d; cbase += (d <= kStatThreads ? d : kStatThreads)) {
+        int c, lane;
+        bool active;
+        if (d <= kStatThreads) {
+            c = tid % d; lane = tid / d; active = lane < lanes;
+        } else {
+            c = cbase + tid; lane = 0; active = c < d;
+        }
+        double s = 0.0, comp = 0.0;   // ZSCORE: Neumaier sum; MINMAX: s = min, comp = max
+        if (norm == KMEANS_NORM_MINMAX) { s = INFINITY; comp = -INFINITY; }
+        if (active) {
+            for (int64_t i = r0 + lane; i < r1; i += lanes) {
+                double x = (double)X[i * d + c];
+                if (norm == KMEANS_NORM_MINMAX) {
+                    s = fmin(s, x);
+                    comp = fmax(comp, x);
+                } else {
+                    double t = s + x;
+                    comp += (fabs(s) >= fabs(x)) ? ((s - t) + x) : ((x - t) + s);
+                    s = t;
+                }
+            }
+        }
+        sh_s[tid] = s;
+        sh_c[tid] = comp;
+        __syncthreads();
+        // combine row lanes of the same column in fixed order (lane 0..lanes-1)
+        if (active && lane == 0) {
+            double S = s, Cc = comp;
+            for (int l = 1; l < lanes; ++l) {
+                double s2 = sh_s[l * d + c], c2 = sh_c[l * d + c];
+                if (norm == KMEANS_NORM_MINMAX) {
+                    S = fmin(S, s2);
+                    Cc = fmax(Cc, c2);
+                } else {
+                    double t = S + s2;
+                    Cc += ((fabs(S) >= fabs(s2)) ? ((S - t) + s2) : ((s2 - t) + S)) + c2;
+                    S = t;
+                }
+            }
+            partials[((int64_t)blockIdx.x * d + c) * 2 + 0] = S;
+            partials[((int64_t)blockIdx.x * d + c) * 2 + 1] = Cc;
+        }
+        __syncthreads();
+        if (d <= kStatThreads) break;
+    }
+}
+
+// Sum of squared deviations from the (final) mean, compensated.
+template <typename W>
+__global__ void norm_var_kernel(const W* __restrict__ X, int64_t n, int d,
+                                const double* __restrict__ mu, double* __restrict__ partials) {
+    const int tid = threadIdx.x;
+    const int lanes = d <= kStatThreads ? kStatThreads / d : 1;
+    const int64_t rows_per_block = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
+    const int64_t r1 = min(n, r0 + rows_per_block);
+    __shared__ double sh_s[kStatThreads], sh_c[kStatThreads];
+    for (int cbase = 0; cbase < d; cbase += (d <= kStatThreads ? d : kStatThreads)) {
+        int c, lane;
+        bool active;
+        if (d <= kStatThreads) {
+            c = tid % d; lane = tid / d; active = lane < lanes;
+        } else {
+            c = cbase + tid; lane = 0; active = c < d;
+        }
+        double s = 0.0, comp = 0.0;
+        if (active) {
+            const double m = mu[c];
+            for (int64_t i = r0 + lane; i < r1; i += lanes) {
+                double z = (double)X[i * d + c] - m;
+                double x = z * z;
+                double t = s + x;
+                comp += (fabs(s) >= fabs(x)) ? ((s - t) + x) : ((x - t) + s);
+                s = t;
+            }
+        }
+        sh_s[tid] = s;
+        sh_c[tid] = comp;
+        __syncthreads();
+        if (active && lane == 0) {
+            double S = s, Cc = comp;
+            for (int l = 1; l < lanes; ++l) {
+                double s2 = sh_s[l * d + c], c2 = sh_c[l * d + c];
+                double t = S + s2;
+                Cc += ((fabs(S) >= fabs(s2)) ? ((S - t) + s2) : ((s2 - t) + S)) + c2;
+                S = t;
+            }
+            partials[((int64_t)blockIdx.x * d + c) * 2 + 0] = S;
+            partials[((int64_t)blockIdx.x * d + c) * 2 + 1] = Cc;
+        }
+        __syncthreads();
+        if (d <= kStatThreads) break;
+    }
+}
+
+// Combine the per-block partials of one column in block order.
+// mode 0: compensated sum (-> a), mode 2: min (-> a) and max (-> b).
+__global__ void norm_combine_kernel(int mode, const double* __restrict__ partials, int nblocks,
+                                    int d, double* a, double* b) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= d) return;
+    if (mode == 2) {
+        double mn = INFINITY, mx = -INFINITY;
+        for (int q = 0; q < nblocks; ++q) {
+            mn = fmin(mn, partials[((int64_t)q * d + c) * 2 + 0]);
+            mx = fmax(mx, partials[((int64_t)q * d + c) * 2 + 1]);
+        }
+        a[c] = mn;
+        b[c] = mx;
+        return;
+    }
+    double S = 0.0, Cc = 0.0;
+    for (int q = 0; q < nblocks; ++q) {
+        double s2 = partials[((int64_t)q * d + c) * 2 + 0];
+        double c2 = partials[((int64_t)q * d + c) * 2 + 1];
+        double t = S + s2;
+        Cc += ((fabs(S) >= fabs(s2)) ? ((S - t) + s2) : ((s2 - t) + S)) + c2;
+        S = t;
+    }
+    a[c] = S + Cc;
+}
+
+// Turn (global) aggregates into the map: 0: shift = sum / n; 1: scale = sqrt(ssq / n), 0 -> 1;
+// 2: scale = max - min, 0 -> 1 (shift already holds min).
+__global__ void norm_post_kernel(int mode, int d, double n_total, double* shift, double* scale) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= d) return;
+    if (mode == 0) {
+        shift[c] = shift[c] / n_total;
+    } else if (mode == 1) {
+        double sigma = sqrt(scale[c] / n_total);
+        scale[c] = (sigma == 0.0) ? 1.0 : sigma;
+    } else {
+        double r = scale[c] - shift[c];
+        scale[c] = (r == 0.0) ? 1.0 : r;
+    }
+}
+
+template <typename W>
+__global__ void norm_apply_kernel(W* __restrict__ X, int64_t total, int d,
+                                  const double* __restrict__ shift,
+                                  const double* __restrict__ scale) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int c = (int)(i % d);
+        double z = ((double)X[i] - shift[c]) / scale[c];
+        X[i] = rounder<sizeof(W) == 8 ? KMEANS_FP64 : KMEANS_FP32>::from(z);
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K1 / K3 prep: one warp per row.
+// ------------------------------------------------------------------------------------------
+template <typename W, int DIST>
+__global__ void prep_kernel(const W* __restrict__ X, int64_t rows, int d, int d_pad, int guard,
+                            W* __restrict__ norms, W* __restrict__ scales,
+                            typename low_type<DIST>::T* __restrict__ Xl,
+                            unsigned long long* __restrict__ census) {
+    using L = typename low_type<DIST>::T;
+    constexpr int WORK = sizeof(W) == 8 ? KMEANS_FP64 : KMEANS_FP32;
+    constexpr bool same = (DIST == WORK);
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long n_nonfinite = 0, n_under = 0;
+    for (int64_t i = warp; i < rows; i += nwarps) {
+        const W* x = X + i * d;
+        double acc = 0.0;
+        double amax = 0.0;
+        for (int c = lane; c < d; c += 32) {
+            double v = (double)x[c];
+            acc = __dadd_rn(acc, __dmul_rn(v, v));
+            amax = fmax(amax, fabs(v));
+        }
+        acc = warp_sum(acc);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        double s = 1.0;
+        if (guard && !same) s = (amax == 0.0 || isnan(amax)) ? 1.0 : amax;
+        if (lane == 0) {
+            norms[i] = rounder<WORK>::from(acc);
+            if (scales) scales[i] = (W)s;
+        }
+        const W sw = (W)s;
+        for (int c = lane; c < d_pad; c += 32) {
+            L o;
+            if (c < d) {
+                W v = x[c];
+                W q = (s == 1.0) ? v : v / sw;     // precision-u division (IEEE, RN)
+                o = rounder<DIST>::from(q);
+                if (!same) {
+                    if (is_nonfinite_low(o)) n_nonfinite++;
+                    else if (q != (W)0 && is_zero_or_subnormal_low(o)) n_under++;
+                }
+            } else {
+                o = rounder<DIST>::from((W)0);
+            }
+            Xl[i * d_pad + c] = o;
+        }
+    }
+    if (census) {
+        n_nonfinite = warp_sum(n_nonfinite);
+        n_under = warp_sum(n_under);
+        if (lane == 0 && (n_nonfinite | n_under)) {
+            atomicAdd(&census[0], n_nonfinite);
+            atomicAdd(&census[1], n_under);
+        }
+    }
+}
+
+template <typename S, int DST>
+__global__ void cast_kernel(const S* __restrict__ in, int64_t count,
+                            typename low_type<DST>::T* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = rounder<DST>::from(in[i]);
+}
+
+inline int grid_for(int64_t work_items, int threads, int per_sm = 8) {
+    int64_t b = (work_items + threads - 1) / threads;
+    int64_t cap = (int64_t)kNumSMs * per_sm;
+    return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+}  // namespace
+
+int norm_stats_blocks(int64_t n, int d) {
+    int64_t b = (n * d + 8191) / 8192;
+    if (b < 1) b = 1;
+    if (b > kNumSMs * 4) b = kNumSMs * 4;
+    return (int)b;
+}
+
+cudaError_t launch_norm_stats(int work, int norm, const void* X, int64_t n, int d,
+                              double* partials, int nblocks, double* a, double* b,
+                              cudaStream_t s) {
+    launches_add(2);
+    if (work == KMEANS_FP64)
+        norm_stats_kernel<double><<<nblocks, kStatThreads, 0, s>>>(norm, (const double*)X, n, d,
+                                                                   partials);
+    else
+        norm_stats_kernel<float><<<nblocks, kStatThreads, 0, s>>>(norm, (const float*)X, n, d,
+                                                                  partials);
+    norm_combine_kernel<<<(d + 127) / 128, 128, 0, s>>>(norm == KMEANS_NORM_MINMAX ? 2 : 0,
+                                                         partials, nblocks, d, a, b);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_norm_ssq(int work, const void* X, int64_t n, int d, double* partials,
+                            int nblocks, const double* mean, double* ssq, cudaStream_t s) {
+    launches_add(2);
+    if (work == KMEANS_FP64)
+        norm_var_kernel<double><<<nblocks, kStatThreads, 0, s>>>((const double*)X, n, d, mean,
+                                                                 partials);
+    else
+        norm_var_kernel<float><<<nblocks, kStatThreads, 0, s>>>((const float*)X, n, d, mean,
+                                                                partials);
+    norm_combine_kernel<<<(d + 127) / 128, 128, 0, s>>>(0, partials, nblocks, d, ssq, nullptr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_norm_post(int mode, int d, double n_total, double* shift, double* scale,
+                             cudaStream_t s) {
+    launches_add(1);
+    norm_post_kernel<<<(d + 127) / 128, 128, 0, s>>>(mode, d, n_total, shift, scale);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_norm_apply(int work, void* X, int64_t rows, int d, const double* shift,
+                              const double* scale, cudaStream_t s) {
+    launches_add(1);
+    int64_t total = rows * d;
+    int g = grid_for(total, 256, 16);
+    if (work == KMEANS_FP64)
+        norm_apply_kernel<double><<<g, 256, 0, s>>>((double*)X, total, d, shift, scale);
+    else
+        norm_apply_kernel<float><<<g, 256, 0, s>>>((float*)X, total, d, shift, scale);
+    return cudaGetLastError();
+}
+
+template <typename W>
+static cudaError_t prep_dispatch(int dist, const W* X, int64_t rows, int d, int d_pad, int guard,
+                                 W* norms, W* scales, void* Xl, unsigned long long* census,
+                                 cudaStream_t s) {
+    int g = grid_for(rows * 32, 256, 16);
+    switch (dist) {
+        case KMEANS_FP64:
+            prep_kernel<W, KMEANS_FP64><<<g, 256, 0, s>>>(X, rows, d, d_pad, guard, norms, scales,
+                                                         (double*)Xl, census);
+            break;
+        case KMEANS_FP32:
+            prep_kernel<W, KMEANS_FP32><<<g, 256, 0, s>>>(X, rows, d, d_pad, guard, norms, scales,
+                                                         (float*)Xl, census);
+            break;
+        case KMEANS_FP16:
+            prep_kernel<W, KMEANS_FP16><<<g, 256, 0, s>>>(X, rows, d, d_pad, guard, norms, scales,
+                                                         (__half*)Xl, census);
+            break;
+        case KMEANS_BF16:
+            prep_kernel<W, KMEANS_BF16><<<g, 256, 0, s>>>(X, rows, d, d_pad, guard, norms, scales,
+                                                         (__nv_bfloat16*)Xl, census);
+            break;
+        case KMEANS_E5M2:
+            prep_kernel<W, KMEANS_E5M2><<<g, 256, 0, s>>>(X, rows, d, d_pad, guard, norms, scales,
+                                                         (e5m2_t*)Xl, census);
+            break;
+        default:
+            return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prep(int work, int dist, const void* Xw, int64_t rows, int d, int d_pad,
+                        int guard, void* norms, void* scales, void* Xl,
+                        unsigned long long* census, cudaStream_t s) {
+    launches_add(1);
+    if (rows <= 0) return cudaSuccess;
+    if (work == KMEANS_FP64)
+        return prep_dispatch<double>(dist, (const double*)Xw, rows, d, d_pad, guard,
+                                     (double*)norms, (double*)scales, Xl, census, s);
+    return prep_dispatch<float>(dist, (const float*)Xw, rows, d, d_pad, guard, (float*)norms,
+                                (float*)scales, Xl, census, s);
+}
+
+template <typename S>
+static cudaError_t cast_dispatch(int dst, const S* in, int64_t count, void* out, cudaStream_t s) {
+    int g = grid_for(count, 256, 16);
+    switch (dst) {
+        case KMEANS_FP32: cast_kernel<S, KMEANS_FP32><<<g, 256, 0, s>>>(in, count, (float*)out); break;
+        case KMEANS_FP16: cast_kernel<S, KMEANS_FP16><<<g, 256, 0, s>>>(in, count, (__half*)out); break;
+        case KMEANS_BF16:
+            cast_kernel<S, KMEANS_BF16><<<g, 256, 0, s>>>(in, count, (__nv_bfloat16*)out);
+            break;
+        case KMEANS_E5M2: cast_kernel<S, KMEANS_E5M2><<<g, 256, 0, s>>>(in, count, (e5m2_t*)out); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cast(int src, int dst, const void* in, int64_t count, void* out,
+                        cudaStream_t s) {
+    launches_add(1);
+    if (count <= 0) return cudaSuccess;
+    if (src == KMEANS_FP64) return cast_dispatch<double>(dst, (const double*)in, count, out, s);
+    if (src == KMEANS_FP32) return cast_dispatch<float>(dst, (const float*)in, count, out, s);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace mpk

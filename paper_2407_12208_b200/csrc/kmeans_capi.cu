@@ -1,0 +1,647 @@
+// kmeans_capi.cu — the C ABI (include/kmeans.h): handle lifetime, input staging, the Lloyd
+// loop of Alg 3 with C0 given, the final working-precision pass, and the
+// optional point-sharded NCCL path. All arithmetic runs in the kernels of k_*.cu.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace mpk;
+
+struct kmeans_ctx {
+    int64_t n = 0;
+    int d = 0, k = 0, work = 0, dist = 0, flags = 0, norm = 0, guard = 0, force_simt = 0;
+    int d_pad = 0;                 // row stride of the low operands
+    int wsize = 0, lsize = 0;      // element sizes of work / low types
+    int device = 0;
+    cudaStream_t own_stream = nullptr, stream = nullptr;
+    int timing = 0;
+    std::string err;
+
+    // device buffers
+    void* Xw = nullptr;            // normalised points (work), n x d
+    void* Xl = nullptr;            // low operands, n x d_pad (alias Xw when dist == work)
+    void* xn = nullptr;            // ||x||^2 (work), n
+    void* sx = nullptr;            // guard scales (work), n
+    void* Cw = nullptr;            // centroids (work), k x d
+    void* Cl = nullptr;            // low centroid operands, k x d_pad
+    void* cn = nullptr;            // ||c||^2 (work), k
+    void* sc = nullptr;            // guard scales (work), k
+    int32_t* labels = nullptr;     // n
+    double* acc = nullptr;         // packed accumulator (AccLayout)
+    int *cnt = nullptr, *offs = nullptr, *cursor = nullptr, *perm = nullptr;
+    IterRec* trace = nullptr;      // KMEANS_MAX_TRACE records
+    double* shift = nullptr;       // d (fp64)
+    double* scale = nullptr;       // d (fp64)
+    double* partials = nullptr;    // normalisation partials
+    int npartials = 0;
+    unsigned long long* census = nullptr;   // [nonfinite, underflow] prep + per-iteration
+    double* sse_dev = nullptr;     // final SSE accumulator
+    bool have_centroids = false;
+    bool xl_alias = false;
+
+    TcPlan* tc = nullptr;
+    int dist_kernel = 0;
+    AccLayout L{0, 0};
+
+    // distributed
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+
+    kmeans_stats stats{};
+};
+
+namespace mpk {
+static std::atomic<long long> g_launches{0};
+long long launches_read() { return g_launches.load(); }
+void launches_add(int n) { g_launches += n; }
+}  // namespace mpk
+
+namespace {
+
+thread_local std::string g_create_err;
+
+int fail(kmeans_ctx* h, int code, const std::string& msg) {
+    if (h) h->err = msg; else g_create_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t _e = (call);                                                          \
+        if (_e != cudaSuccess)                                                            \
+            return fail(h, KMEANS_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+#define CKN(call)                                                                         \
+    do {                                                                                  \
+        ncclResult_t _r = (call);                                                         \
+        if (_r != ncclSuccess)                                                            \
+            return fail(h, KMEANS_ENCCL, std::string(#call) + ": " + ncclGetErrorString(_r)); \
+    } while (0)
+
+int elem_size(int prec) {
+    switch (prec) {
+        case KMEANS_FP64: return 8;
+        case KMEANS_FP32: return 4;
+        case KMEANS_FP16: return 2;
+        case KMEANS_BF16: return 2;
+        case KMEANS_E5M2: return 1;
+    }
+    return 0;
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int check_device(kmeans_ctx* h) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(h, KMEANS_ENODEV, "no CUDA device");
+    }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess)
+        return fail(h, KMEANS_ENODEV, "cudaGetDeviceProperties failed");
+    if (prop.major != 10)
+        return fail(h, KMEANS_ENODEV,
+                    "this library is built for sm_100a (B200); device is sm_" +
+                        std::to_string(prop.major) + std::to_string(prop.minor));
+    return dev;
+}
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    return cudaMalloc((void**)p, bytes);
+}
+
+void free_all(kmeans_ctx* h) {
+    if (h->tc) tc_plan_destroy(h->tc);
+    void* bufs[] = {h->Xw, h->xl_alias ? nullptr : h->Xl, h->xn, h->sx, h->Cw, h->Cl, h->cn,
+                    h->sc, h->labels, h->acc, h->cnt, h->offs, h->cursor, h->perm, h->trace,
+                    h->shift, h->scale, h->partials, h->census, h->sse_dev};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    if (h->own_stream) cudaStreamDestroy(h->own_stream);
+    if (h->comm) ncclCommDestroy(h->comm);
+}
+
+int create_impl(int64_t n, int32_t d, int32_t k, int work, int dist, int flags,
+                kmeans_handle* out, const void* nccl_id, int nranks, int rank) {
+    kmeans_ctx* h = nullptr;
+    if (!out) return fail(nullptr, KMEANS_EINVAL, "out is NULL");
+    *out = nullptr;
+    int norm = flags & 0xff;
+    if (n < 1 || d < 1 || k < 1 || (nranks == 1 && k > n))
+        return fail(nullptr, KMEANS_EINVAL, "need n >= 1, d >= 1, 1 <= k <= n");
+    if (work != KMEANS_FP64 && work != KMEANS_FP32)
+        return fail(nullptr, KMEANS_EINVAL, "work_prec must be KMEANS_FP64 or KMEANS_FP32");
+    if (dist < KMEANS_FP64 || dist > KMEANS_E5M2)
+        return fail(nullptr, KMEANS_EINVAL, "unknown dist_prec");
+    if (work == KMEANS_FP32 && dist == KMEANS_FP64)
+        return fail(nullptr, KMEANS_EINVAL, "dist_prec must not be more precise than work_prec");
+    if (norm > KMEANS_NORM_ZSCORE || (flags & ~(0xff | KMEANS_GUARD_SCALE | KMEANS_FORCE_SIMT)))
+        return fail(nullptr, KMEANS_EINVAL, "unknown flags");
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+        return fail(nullptr, KMEANS_EINVAL, "bad rank / nranks");
+    int dev = check_device(nullptr);
+    if (dev < 0) return dev;
+
+    h = new kmeans_ctx();
+    h->n = n; h->d = d; h->k = k; h->work = work; h->dist = dist; h->flags = flags;
+    h->norm = norm; h->guard = (flags & KMEANS_GUARD_SCALE) ? 1 : 0;
+    h->force_simt = (flags & KMEANS_FORCE_SIMT) ? 1 : 0;
+    h->device = dev;
+    h->wsize = elem_size(work);
+    h->lsize = elem_size(dist);
+    h->nranks = nranks; h->rank = rank;
+    h->L = AccLayout{k, d};
+
+    // choose the distance kernel (host-side dispatch by (d, k, precision))
+    bool low = dist >= KMEANS_FP16;
+    h->d_pad = d;
+    if (!h->force_simt && smalld_supported(d, k)) {
+        h->dist_kernel = DK_SMALLD;
+    } else if (!h->force_simt && low && work == KMEANS_FP32 &&
+               tc_supported(dist, tc_dpad(dist, d), k)) {
+        h->dist_kernel = DK_TCGEN05;
+        h->d_pad = tc_dpad(dist, d);
+    } else {
+        h->dist_kernel = (dist == work) ? DK_SIMT_WORK : DK_SIMT_LOW;
+    }
+
+    auto bail = [&](int code, const std::string& m) {
+        g_create_err = m;
+        free_all(h);
+        delete h;
+        return code;
+    };
+#define CA(call)                                                                           \
+    do {                                                                                   \
+        cudaError_t _e = (call);                                                           \
+        if (_e != cudaSuccess) {                                                           \
+            cudaGetLastError();                                                            \
+            return bail(_e == cudaErrorMemoryAllocation ? KMEANS_ENOMEM : KMEANS_ECUDA,    \
+                        std::string(#call) + ": " + cudaGetErrorString(_e));               \
+        }                                                                                  \
+    } while (0)
+
+    CA(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+    h->stream = h->own_stream;
+    size_t W = h->wsize;
+    CA(dalloc(&h->Xw, (size_t)n * d * W));
+    if (dist == work) {
+        h->Xl = h->Xw;
+        h->xl_alias = true;
+    } else {
+        CA(dalloc(&h->Xl, (size_t)n * h->d_pad * h->lsize));
+    }
+    CA(dalloc(&h->xn, (size_t)n * W));
+    CA(dalloc(&h->sx, (size_t)n * W));
+    CA(dalloc(&h->Cw, (size_t)k * d * W));
+    CA(dalloc(&h->Cl, (size_t)k * std::max(h->d_pad, d) * std::max(h->lsize, h->wsize)));
+    CA(dalloc(&h->cn, (size_t)k * W));
+    CA(dalloc(&h->sc, (size_t)k * W));
+    CA(dalloc(&h->labels, (size_t)n * sizeof(int32_t)));
+    CA(dalloc(&h->acc, (size_t)h->L.total() * sizeof(double)));
+    CA(dalloc(&h->cnt, (size_t)k * sizeof(int)));
+    CA(dalloc(&h->offs, (size_t)(k + 1) * sizeof(int)));
+    CA(dalloc(&h->cursor, (size_t)k * sizeof(int)));
+    CA(dalloc(&h->perm, (size_t)n * sizeof(int)));
+    CA(dalloc(&h->trace, (size_t)KMEANS_MAX_TRACE * sizeof(IterRec)));
+    CA(dalloc(&h->shift, (size_t)d * sizeof(double)));
+    CA(dalloc(&h->scale, (size_t)d * sizeof(double)));
+    h->npartials = norm_stats_blocks(n, d);
+    CA(dalloc(&h->partials, (size_t)h->npartials * d * 2 * sizeof(double)));
+    CA(dalloc(&h->census, 4 * sizeof(unsigned long long)));
+    CA(dalloc(&h->sse_dev, 4 * sizeof(double)));
+    if (h->dist_kernel == DK_TCGEN05) {
+        std::string e;
+        h->tc = tc_plan_create(dist, n, d, h->d_pad, k, h->Xl, h->Cl, &e);
+        if (!h->tc) {
+            // the tcgen05 path must exist for these shapes on sm_100a: report, do not fall back
+            return bail(KMEANS_ECUDA, "tcgen05 plan: " + e);
+        }
+    }
+    if (nranks > 1) {
+        ncclUniqueId id;
+        memcpy(&id, nccl_id, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&h->comm, nranks, id, rank);
+        if (r != ncclSuccess) return bail(KMEANS_ENCCL, std::string("ncclCommInitRank: ") +
+                                                            ncclGetErrorString(r));
+    }
+    // identity transform until a normalising fit
+    std::vector<double> zero(d, 0.0), one(d, 1.0);
+    CA(cudaMemcpy(h->shift, zero.data(), d * sizeof(double), cudaMemcpyHostToDevice));
+    CA(cudaMemcpy(h->scale, one.data(), d * sizeof(double), cudaMemcpyHostToDevice));
+#undef CA
+    *out = h;
+    return KMEANS_OK;
+}
+
+// Copy rows (host or device source) of the work type into a device buffer.
+int stage_rows(kmeans_ctx* h, const void* src, int64_t rows, void* dst) {
+    size_t bytes = (size_t)rows * h->d * h->wsize;
+    cudaMemcpyKind kind = is_device_ptr(src) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CK(cudaMemcpyAsync(dst, src, bytes, kind, h->stream));
+    return 0;
+}
+
+// Normalise X (already staged in h->Xw) in place; computes shift/scale from it (globally
+// across ranks when sharded: the per-feature aggregates are allreduced).
+int normalise_points(kmeans_ctx* h, int64_t rows) {
+    if (h->norm == KMEANS_NORM_NONE) return 0;
+    cudaStream_t s = h->stream;
+    int nb = norm_stats_blocks(rows, h->d);
+    if (nb > h->npartials) nb = h->npartials;
+    double n_total = (double)rows;
+    if (h->comm) {
+        double* tmp = h->sse_dev + 2;
+        CK(cudaMemcpyAsync(tmp, &n_total, sizeof(double), cudaMemcpyHostToDevice, s));
+        CKN(ncclAllReduce(tmp, tmp, 1, ncclDouble, ncclSum, h->comm, s));
+        CK(cudaMemcpyAsync(&n_total, tmp, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    CK(launch_norm_stats(h->work, h->norm, h->Xw, rows, h->d, h->partials, nb, h->shift,
+                         h->scale, s));
+    if (h->norm == KMEANS_NORM_ZSCORE) {
+        if (h->comm) CKN(ncclAllReduce(h->shift, h->shift, h->d, ncclDouble, ncclSum, h->comm, s));
+        CK(launch_norm_post(0, h->d, n_total, h->shift, h->scale, s));
+        CK(launch_norm_ssq(h->work, h->Xw, rows, h->d, h->partials, nb, h->shift, h->scale, s));
+        if (h->comm) CKN(ncclAllReduce(h->scale, h->scale, h->d, ncclDouble, ncclSum, h->comm, s));
+        CK(launch_norm_post(1, h->d, n_total, h->shift, h->scale, s));
+    } else {
+        if (h->comm) {
+            CKN(ncclAllReduce(h->shift, h->shift, h->d, ncclDouble, ncclMin, h->comm, s));
+            CKN(ncclAllReduce(h->scale, h->scale, h->d, ncclDouble, ncclMax, h->comm, s));
+        }
+        CK(launch_norm_post(2, h->d, n_total, h->shift, h->scale, s));
+    }
+    CK(launch_norm_apply(h->work, h->Xw, rows, h->d, h->shift, h->scale, s));
+    return 0;
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+}
+
+struct EventPool {
+    std::vector<cudaEvent_t> ev;
+    ~EventPool() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+    cudaEvent_t get() {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        ev.push_back(e);
+        return e;
+    }
+};
+
+// Distance + argmin for the current centroids on h->n rows (loop iteration or assign).
+int run_assign(kmeans_ctx* h, int64_t rows, double* acc_sse, double* acc_changed) {
+    Problem p{rows, h->d, h->k, h->d_pad, h->guard};
+    if (h->dist_kernel == DK_TCGEN05) {
+        CK(launch_assign_tc(h->tc, p, (const float*)h->xn, h->guard ? (const float*)h->sx : nullptr,
+                            (const float*)h->cn, h->guard ? (const float*)h->sc : nullptr,
+                            h->labels, acc_sse, acc_changed, h->stream));
+    } else {
+        CK(launch_assign_simt(h->work, h->dist, p, h->Xl, h->xn, h->guard ? h->sx : nullptr,
+                              h->Cl, h->cn, h->guard ? h->sc : nullptr, h->labels, acc_sse,
+                              acc_changed, h->stream));
+    }
+    return 0;
+}
+
+int prep_centroids(kmeans_ctx* h) {
+    CK(launch_prep(h->work, h->dist, h->Cw, h->k, h->d, h->d_pad, h->guard, h->cn, h->sc, h->Cl,
+                   h->census + 2, h->stream));
+    return 0;
+}
+
+int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, double tol,
+             int32_t* labels_out, void* cent_out, double* sse_out, int32_t* iters_out) {
+    if (!X || !C0) return fail(h, KMEANS_EINVAL, "X and C0 are required");
+    if (max_iter < 1) return fail(h, KMEANS_EINVAL, "max_iter must be >= 1");
+    CK(cudaSetDevice(h->device));
+    cudaStream_t s = h->stream;
+    EventPool evp;
+    const long long launches0 = launches_read();
+    cudaEvent_t e0 = evp.get(), e1 = evp.get(), e2 = evp.get(), e3 = evp.get();
+    const int64_t n = h->n;
+    const int d = h->d, k = h->k;
+
+    CK(cudaEventRecord(e0, s));
+    // ---- A1: stage + normalise X and C0 -------------------------------------------------
+    if (int rc = stage_rows(h, X, n, h->Xw)) return rc;
+    if (int rc = stage_rows(h, C0, k, h->Cw)) return rc;
+    if (h->norm != KMEANS_NORM_NONE) {
+        if (int rc = normalise_points(h, n)) return rc;
+        CK(launch_norm_apply(h->work, h->Cw, k, d, h->shift, h->scale, s));
+    }
+    // ---- A2: point prep (norms, guard scales, low operands) -----------------------------
+    CK(cudaMemsetAsync(h->census, 0, 4 * sizeof(unsigned long long), s));
+    CK(launch_prep(h->work, h->dist, h->Xw, n, d, h->d_pad, h->guard, h->xn, h->sx, h->Xl,
+                   h->census, s));
+    CK(cudaMemsetAsync(h->labels, 0xff, (size_t)n * sizeof(int32_t), s));   // labels_prev = -1
+    CK(cudaMemsetAsync(h->trace, 0, sizeof(IterRec) * KMEANS_MAX_TRACE, s));
+    CK(cudaEventRecord(e1, s));
+
+    // ---- A3..A7: Lloyd iterations ---------------------------------------------------------
+    std::vector<cudaEvent_t> kev;
+    const bool timing = h->timing != 0;
+    int it = 0;
+    bool converged = false;
+    IterRec rec_h{};
+    IterRec* rec_scratch = h->trace + (KMEANS_MAX_TRACE - 1);
+    for (it = 1; it <= max_iter; ++it) {
+        IterRec* rec = (it <= KMEANS_MAX_TRACE - 1) ? h->trace + (it - 1) : rec_scratch;
+        if (rec == rec_scratch) CK(cudaMemsetAsync(rec_scratch, 0, sizeof(IterRec), s));
+        cudaEvent_t t0 = nullptr, t1 = nullptr, t2 = nullptr, t3 = nullptr, t4 = nullptr;
+        if (timing) { t0 = evp.get(); t1 = evp.get(); t2 = evp.get(); t3 = evp.get(); t4 = evp.get(); }
+        CK(cudaMemsetAsync(h->acc, 0, sizeof(double) * h->L.total(), s));
+        if (int rc = prep_centroids(h)) return rc;                         // A3
+        if (timing) CK(cudaEventRecord(t0, s));
+        if (h->dist_kernel == DK_SMALLD) {                                  // A4 + A5 fused
+            Problem p{n, d, k, h->d_pad, h->guard};
+            CK(launch_smalld_fused(h->work, h->dist, p, h->Xw, h->Cl, h->cn,
+                                   h->guard ? h->sc : nullptr, h->labels, h->acc, h->L, s));
+            if (timing) { CK(cudaEventRecord(t1, s)); CK(cudaEventRecord(t2, s)); }
+        } else {
+            if (int rc = run_assign(h, n, h->acc + h->L.sse(), h->acc + h->L.changed()))
+                return rc;                                                   // A4
+            if (timing) CK(cudaEventRecord(t1, s));
+            CK(launch_update(h->work, h->Xw, n, d, k, h->labels, h->cnt, h->offs, h->cursor,
+                             h->perm, h->acc, h->L, s));                     // A5
+            if (timing) CK(cudaEventRecord(t2, s));
+        }
+        if (h->comm)                                                         // A6
+            CKN(ncclAllReduce(h->acc, h->acc, h->L.total(), ncclDouble, ncclSum, h->comm, s));
+        if (timing) CK(cudaEventRecord(t3, s));
+        CK(launch_finalize(h->work, k, d, h->acc, h->L, h->Cw, rec, s));    // A7
+        if (timing) { CK(cudaEventRecord(t4, s)); kev.insert(kev.end(), {t0, t1, t2, t3, t4}); }
+        if (tol >= 0.0) {
+            CK(cudaMemcpyAsync(&rec_h, rec, sizeof(IterRec), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (rec_h.changed == 0.0 || std::sqrt(rec_h.shift2) <= tol) {
+                converged = true;
+                break;
+            }
+        }
+    }
+    if (it > max_iter) it = max_iter;
+    CK(cudaEventRecord(e2, s));
+
+    // ---- A8: final assignment in working precision + direct-formula SSE -------------------
+    {
+        // cn recomputed from the final centroids; operands are the work-precision X and C
+        // (Cl holds a work-precision copy of C here).
+        CK(launch_prep(h->work, h->work, h->Cw, k, d, d, 0, h->cn, nullptr, h->Cl, nullptr, s));
+        Problem p{n, d, k, d, 0};
+        CK(launch_assign_simt(h->work, h->work, p, h->Xw, h->xn, nullptr, h->Cl, h->cn, nullptr,
+                              h->labels, nullptr, nullptr, s));
+        CK(cudaMemsetAsync(h->sse_dev, 0, sizeof(double), s));
+        CK(launch_final_sse(h->work, h->Xw, n, d, h->Cw, h->labels, h->sse_dev, s));
+        if (h->comm)
+            CKN(ncclAllReduce(h->sse_dev, h->sse_dev, 1, ncclDouble, ncclSum, h->comm, s));
+    }
+    CK(cudaEventRecord(e3, s));
+
+    // ---- outputs ---------------------------------------------------------------------------
+    double sse_h = 0.0;
+    CK(cudaMemcpyAsync(&sse_h, h->sse_dev, sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (labels_out) {
+        cudaMemcpyKind kind = is_device_ptr(labels_out) ? cudaMemcpyDeviceToDevice
+                                                        : cudaMemcpyDeviceToHost;
+        CK(cudaMemcpyAsync(labels_out, h->labels, (size_t)n * sizeof(int32_t), kind, s));
+    }
+    if (cent_out) {
+        cudaMemcpyKind kind = is_device_ptr(cent_out) ? cudaMemcpyDeviceToDevice
+                                                      : cudaMemcpyDeviceToHost;
+        CK(cudaMemcpyAsync(cent_out, h->Cw, (size_t)k * d * h->wsize, kind, s));
+    }
+    unsigned long long census_h[4];
+    CK(cudaMemcpyAsync(census_h, h->census, sizeof(census_h), cudaMemcpyDeviceToHost, s));
+    int tl = std::min(it, KMEANS_MAX_TRACE - 1);
+    std::vector<IterRec> tr(tl);
+    if (tl > 0) CK(cudaMemcpyAsync(tr.data(), h->trace, sizeof(IterRec) * tl,
+                                   cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+
+    kmeans_stats& st = h->stats;
+    memset(&st, 0, sizeof(st));
+    st.iters = it;
+    st.converged = converged ? 1 : 0;
+    st.dist_kernel = h->dist_kernel;
+    st.n_nonfinite = (int64_t)(census_h[0] + census_h[2]);
+    st.n_underflow = (int64_t)(census_h[1] + census_h[3]);
+    st.t_prep_ms = elapsed(e0, e1);
+    st.t_loop_ms = elapsed(e1, e2);
+    st.t_final_ms = elapsed(e2, e3);
+    st.trace_len = tl;
+    int any_empty = 0;
+    for (int t = 0; t < tl; ++t) {
+        st.sse_t[t] = tr[t].sse;
+        st.shift2_t[t] = tr[t].shift2;
+        st.changed_t[t] = (int64_t)tr[t].changed;
+        st.empty_t[t] = (int32_t)tr[t].empty;
+        if (tr[t].empty > 0) any_empty = 1;
+    }
+    if (timing) {
+        for (size_t q = 0; q + 4 < kev.size() + 0; q += 5) {
+            st.t_dist_ms += elapsed(kev[q], kev[q + 1]);
+            st.t_update_ms += elapsed(kev[q + 1], kev[q + 2]);
+            st.t_allreduce_ms += elapsed(kev[q + 2], kev[q + 3]);
+            st.t_finalize_ms += elapsed(kev[q + 3], kev[q + 4]);
+        }
+    }
+    st.n_dist_launches = it;
+    st.n_kernel_launches = launches_read() - launches0;
+    int warn = 0;
+    if (st.n_nonfinite > 0) warn |= KMEANS_WARN_NONFINITE;
+    if (any_empty) warn |= KMEANS_WARN_EMPTY;
+    if (tol >= 0.0 && !converged) warn |= KMEANS_WARN_MAXITER;
+    if (st.n_underflow > 0) warn |= KMEANS_WARN_UNDERFLOW;
+    st.warnings = warn;
+    if (sse_out) *sse_out = sse_h;
+    if (iters_out) *iters_out = it;
+    h->have_centroids = true;
+    return warn;
+}
+
+}  // namespace
+
+extern "C" {
+
+int kmeans_create(int64_t n, int32_t d, int32_t k, int work_prec, int dist_prec, int flags,
+                  kmeans_handle* out) {
+    return create_impl(n, d, k, work_prec, dist_prec, flags, out, nullptr, 1, 0);
+}
+
+int kmeans_create_dist(int64_t n_local, int32_t d, int32_t k, int work_prec, int dist_prec,
+                       int flags, const void* nccl_unique_id, int nranks, int rank,
+                       kmeans_handle* out) {
+    if (!nccl_unique_id && nranks > 1) return fail(nullptr, KMEANS_EINVAL, "nccl id is NULL");
+    return create_impl(n_local, d, k, work_prec, dist_prec, flags, out, nccl_unique_id, nranks,
+                       rank);
+}
+
+int kmeans_nccl_unique_id(void* out128) {
+    if (!out128) return KMEANS_EINVAL;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return KMEANS_ENCCL;
+    memcpy(out128, &id, sizeof(id));
+    return KMEANS_OK;
+}
+
+int kmeans_fit(kmeans_handle h, const void* X, const void* C0, int32_t max_iter, double tol,
+               int32_t* labels, void* centroids, double* sse, int32_t* iters) {
+    if (!h) return KMEANS_EINVAL;
+    return fit_impl(h, X, C0, max_iter, tol, labels, centroids, sse, iters);
+}
+
+int kmeans_assign(kmeans_handle h, const void* X, int64_t m, int32_t* labels, double* sse) {
+    if (!h) return KMEANS_EINVAL;
+    if (!X || !labels || m < 1) return fail(h, KMEANS_EINVAL, "X, labels and m >= 1 required");
+    if (!h->have_centroids) return fail(h, KMEANS_EINVAL, "no centroids: fit or set them first");
+    CK(cudaSetDevice(h->device));
+    cudaStream_t s = h->stream;
+    double total = 0.0;
+    const bool lab_dev = is_device_ptr(labels);
+    if (int rc = prep_centroids(h)) return rc;
+    for (int64_t r0 = 0; r0 < m; r0 += h->n) {
+        int64_t rows = std::min<int64_t>(h->n, m - r0);
+        const char* src = (const char*)X + (size_t)r0 * h->d * h->wsize;
+        if (int rc = stage_rows(h, src, rows, h->Xw)) return rc;
+        if (h->norm != KMEANS_NORM_NONE)
+            CK(launch_norm_apply(h->work, h->Xw, rows, h->d, h->shift, h->scale, s));
+        CK(launch_prep(h->work, h->dist, h->Xw, rows, h->d, h->d_pad, h->guard, h->xn, h->sx,
+                       h->Xl, nullptr, s));
+        CK(cudaMemsetAsync(h->sse_dev, 0, sizeof(double), s));
+        if (h->dist_kernel == DK_SMALLD) {
+            Problem p{rows, h->d, h->k, h->d_pad, h->guard};
+            CK(launch_assign_simt(h->work, h->dist, p, h->Xl, h->xn, h->guard ? h->sx : nullptr,
+                                  h->Cl, h->cn, h->guard ? h->sc : nullptr, h->labels,
+                                  h->sse_dev, nullptr, s));
+        } else {
+            if (int rc = run_assign(h, rows, h->sse_dev, nullptr)) return rc;
+        }
+        double part = 0.0;
+        CK(cudaMemcpyAsync(&part, h->sse_dev, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(labels + r0, h->labels, (size_t)rows * sizeof(int32_t),
+                           lab_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        total += part;
+    }
+    if (sse) *sse = total;
+    return KMEANS_OK;
+}
+
+int kmeans_set_centroids(kmeans_handle h, const void* C) {
+    if (!h) return KMEANS_EINVAL;
+    if (!C) return fail(h, KMEANS_EINVAL, "C is NULL");
+    CK(cudaSetDevice(h->device));
+    if (int rc = stage_rows(h, C, h->k, h->Cw)) return rc;
+    CK(cudaStreamSynchronize(h->stream));
+    h->have_centroids = true;
+    return KMEANS_OK;
+}
+
+int kmeans_get_centroids(kmeans_handle h, void* C) {
+    if (!h) return KMEANS_EINVAL;
+    if (!C) return fail(h, KMEANS_EINVAL, "C is NULL");
+    CK(cudaMemcpyAsync(C, h->Cw, (size_t)h->k * h->d * h->wsize,
+                       is_device_ptr(C) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return KMEANS_OK;
+}
+
+int kmeans_get_transform(kmeans_handle h, void* shift, void* scale) {
+    if (!h) return KMEANS_EINVAL;
+    std::vector<double> a(h->d), b(h->d);
+    CK(cudaMemcpyAsync(a.data(), h->shift, sizeof(double) * h->d, cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaMemcpyAsync(b.data(), h->scale, sizeof(double) * h->d, cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    for (int t = 0; t < h->d; ++t) {
+        if (h->work == KMEANS_FP64) {
+            if (shift) ((double*)shift)[t] = a[t];
+            if (scale) ((double*)scale)[t] = b[t];
+        } else {
+            if (shift) ((float*)shift)[t] = (float)a[t];
+            if (scale) ((float*)scale)[t] = (float)b[t];
+        }
+    }
+    return KMEANS_OK;
+}
+
+int kmeans_get_stats(kmeans_handle h, kmeans_stats* out) {
+    if (!h || !out) return KMEANS_EINVAL;
+    *out = h->stats;
+    return KMEANS_OK;
+}
+
+int kmeans_set_stream(kmeans_handle h, void* stream) {
+    if (!h) return KMEANS_EINVAL;
+    h->stream = stream ? (cudaStream_t)stream : h->own_stream;
+    return KMEANS_OK;
+}
+
+int kmeans_set_timing(kmeans_handle h, int enable) {
+    if (!h) return KMEANS_EINVAL;
+    h->timing = enable;
+    return KMEANS_OK;
+}
+
+int kmeans_destroy(kmeans_handle h) {
+    if (!h) return KMEANS_OK;
+    cudaSetDevice(h->device);
+    cudaDeviceSynchronize();
+    free_all(h);
+    delete h;
+    return KMEANS_OK;
+}
+
+const char* kmeans_last_error(kmeans_handle h) {
+    if (!h) return g_create_err.c_str();
+    return h->err.c_str();
+}
+
+int kmeans_cast(int src_prec, int dst_prec, const void* src, int64_t count, void* dst) {
+    kmeans_ctx* h = nullptr;
+    if ((src_prec != KMEANS_FP64 && src_prec != KMEANS_FP32) || dst_prec < KMEANS_FP32 ||
+        dst_prec > KMEANS_E5M2 || count < 0 || (count > 0 && (!src || !dst)))
+        return fail(nullptr, KMEANS_EINVAL, "kmeans_cast: bad arguments");
+    if (count > 0 && (!is_device_ptr(src) || !is_device_ptr(dst)))
+        return fail(nullptr, KMEANS_EINVAL, "kmeans_cast: src and dst must be device pointers");
+    CK(launch_cast(src_prec, dst_prec, src, count, dst, 0));
+    CK(cudaStreamSynchronize(0));
+    return KMEANS_OK;
+}
+
+const char* kmeans_version(void) { return "mpkmeans-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"
