@@ -93,6 +93,7 @@ typedef struct kmeans_stats {
     int64_t changed_t[KMEANS_MAX_TRACE]; /* labels that changed in iteration t              */
     int32_t empty_t[KMEANS_MAX_TRACE];   /* empty clusters in iteration t                   */
     int64_t n_kernel_launches;           /* kernels this library launched during the fit    */
+    int64_t n_final_fallback;            /* final-pass rows re-evaluated on CUDA cores (-1: all) */
 } kmeans_stats;
 
 /*

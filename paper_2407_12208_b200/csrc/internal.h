@@ -85,7 +85,8 @@ cudaError_t launch_cast(int src, int dst, const void* in, int64_t count, void* o
 cudaError_t launch_assign_simt(int work, int dist, const Problem& p, const void* Xl,
                                const void* xn, const void* sx, const void* Cl, const void* cn,
                                const void* sc, int32_t* labels, double* acc_sse,
-                               double* acc_changed, cudaStream_t s);
+                               double* acc_changed, cudaStream_t s,
+                               const int* row_list = nullptr);
 cudaError_t launch_final_sse(int work, const void* Xw, int64_t n, int d, const void* Cw,
                              const int32_t* labels, double* sse_out, cudaStream_t s);
 
@@ -105,6 +106,12 @@ void tc_plan_destroy(TcPlan*);
 cudaError_t launch_assign_tc(TcPlan* plan, const Problem& p, const float* xn, const float* sx,
                              const float* cn, const float* sc, int32_t* labels, double* acc_sse,
                              double* acc_changed, cudaStream_t s);
+// Final pass (Alg 3 step 7) as a certified tensor-core filter: rows whose top-2 gap exceeds the
+// error bound get the filter's argmin (= the working-precision argmin); the others are appended
+// to fb_rows (count in *fb_count) for launch_assign_simt(row_list = fb_rows).
+cudaError_t launch_final_tc(TcPlan* plan, const Problem& p, const float* xn, const float* sx,
+                            const float* cn, const float* sc, int32_t* labels, int* fb_count,
+                            int* fb_rows, cudaStream_t s);
 
 // K7: update = bucket by label (count, scan, scatter) + segmented fp64 sums.
 cudaError_t launch_update(int work, const void* Xw, int64_t n, int d, int k,

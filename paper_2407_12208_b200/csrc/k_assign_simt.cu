@@ -29,7 +29,8 @@ __global__ void __launch_bounds__(NT)
 assign_simt_kernel(Problem p, const LT* __restrict__ Xl, const W* __restrict__ xn,
                    const W* __restrict__ sx, const LT* __restrict__ Cl,
                    const W* __restrict__ cn, const W* __restrict__ sc,
-                   int32_t* __restrict__ labels, double* acc_sse, double* acc_changed) {
+                   int32_t* __restrict__ labels, double* acc_sse, double* acc_changed,
+                   const int* __restrict__ rows) {
     __shared__ AT Xs[BK][BM];
     __shared__ AT Cs[BK][BN];
     const int tid = threadIdx.x;
@@ -43,8 +44,9 @@ assign_simt_kernel(Problem p, const LT* __restrict__ Xl, const W* __restrict__ x
     W srow[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-        int64_t row = row0 + ty * 4 + r;
-        srow[r] = (p.guard && sx && row < p.n) ? sx[row] : (W)1;
+        const int64_t li = row0 + ty * 4 + r;   // list index; the row is rows[li] if listed
+        const int64_t row = (rows && li < p.n) ? (int64_t)rows[li] : li;
+        srow[r] = (p.guard && sx && li < p.n) ? sx[row] : (W)1;
     }
 
     for (int n0 = 0; n0 < p.k; n0 += BN) {
@@ -58,10 +60,13 @@ assign_simt_kernel(Problem p, const LT* __restrict__ Xl, const W* __restrict__ x
             for (int e = 0; e < (BM * BK) / NT; ++e) {
                 int idx = tid + e * NT;
                 int r = idx / BK, kk = idx % BK;
-                int64_t row = row0 + r;
+                const int64_t li = row0 + r;
                 int col = k0 + kk;
                 AT v = (AT)0;
-                if (row < p.n && col < p.d) v = (AT)widen(Xl[row * p.d_pad + col]);
+                if (li < p.n && col < p.d) {
+                    const int64_t row = rows ? (int64_t)rows[li] : li;
+                    v = (AT)widen(Xl[row * p.d_pad + col]);
+                }
                 Xs[kk][r] = v;
                 int cj = n0 + r;
                 AT w = (AT)0;
@@ -113,8 +118,9 @@ assign_simt_kernel(Problem p, const LT* __restrict__ Xl, const W* __restrict__ x
     if (tx == 0) {
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-            int64_t row = row0 + ty * 4 + r;
-            if (row < p.n) {
+            const int64_t li = row0 + ty * 4 + r;
+            if (li < p.n) {
+                const int64_t row = rows ? (int64_t)rows[li] : li;
                 if (acc_changed && labels[row] != bestj[r]) my_changed += 1.0;
                 labels[row] = bestj[r];
                 if (acc_sse) {
@@ -291,17 +297,14 @@ template <typename LT, typename W>
 cudaError_t simt_dispatch_acc(int dist, const Problem& p, const void* Xl, const void* xn,
                               const void* sx, const void* Cl, const void* cn, const void* sc,
                               int32_t* labels, double* acc_sse, double* acc_changed,
-                              cudaStream_t s) {
+                              cudaStream_t s, const int* rows) {
     int64_t blocks = (p.n + BM - 1) / BM;
     if (blocks == 0) return cudaSuccess;
-    if (dist == KMEANS_FP64)
-        assign_simt_kernel<LT, double, W><<<(unsigned)blocks, NT, 0, s>>>(
-            p, (const LT*)Xl, (const W*)xn, (const W*)sx, (const LT*)Cl, (const W*)cn,
-            (const W*)sc, labels, acc_sse, acc_changed);
-    else
-        assign_simt_kernel<LT, float, W><<<(unsigned)blocks, NT, 0, s>>>(
-            p, (const LT*)Xl, (const W*)xn, (const W*)sx, (const LT*)Cl, (const W*)cn,
-            (const W*)sc, labels, acc_sse, acc_changed);
+    // fp64 operands accumulate in fp64; every other operand type in fp32 (reading Z2/Z3)
+    using AT = typename std::conditional<std::is_same<LT, double>::value, double, float>::type;
+    assign_simt_kernel<LT, AT, W><<<(unsigned)blocks, NT, 0, s>>>(
+        p, (const LT*)Xl, (const W*)xn, (const W*)sx, (const LT*)Cl, (const W*)cn, (const W*)sc,
+        labels, acc_sse, acc_changed, rows);
     return cudaGetLastError();
 }
 
@@ -309,24 +312,17 @@ template <typename W>
 cudaError_t simt_dispatch(int dist, const Problem& p, const void* Xl, const void* xn,
                           const void* sx, const void* Cl, const void* cn, const void* sc,
                           int32_t* labels, double* acc_sse, double* acc_changed,
-                          cudaStream_t s) {
+                          cudaStream_t s, const int* rows) {
+#define MPK_SIMT(LT) \
+    simt_dispatch_acc<LT, W>(dist, p, Xl, xn, sx, Cl, cn, sc, labels, acc_sse, acc_changed, s, rows)
     switch (dist) {
-        case KMEANS_FP64:
-            return simt_dispatch_acc<double, W>(dist, p, Xl, xn, sx, Cl, cn, sc, labels, acc_sse,
-                                                acc_changed, s);
-        case KMEANS_FP32:
-            return simt_dispatch_acc<float, W>(dist, p, Xl, xn, sx, Cl, cn, sc, labels, acc_sse,
-                                               acc_changed, s);
-        case KMEANS_FP16:
-            return simt_dispatch_acc<__half, W>(dist, p, Xl, xn, sx, Cl, cn, sc, labels, acc_sse,
-                                                acc_changed, s);
-        case KMEANS_BF16:
-            return simt_dispatch_acc<__nv_bfloat16, W>(dist, p, Xl, xn, sx, Cl, cn, sc, labels,
-                                                       acc_sse, acc_changed, s);
-        case KMEANS_E5M2:
-            return simt_dispatch_acc<e5m2_t, W>(dist, p, Xl, xn, sx, Cl, cn, sc, labels, acc_sse,
-                                                acc_changed, s);
+        case KMEANS_FP64: return MPK_SIMT(double);
+        case KMEANS_FP32: return MPK_SIMT(float);
+        case KMEANS_FP16: return MPK_SIMT(__half);
+        case KMEANS_BF16: return MPK_SIMT(__nv_bfloat16);
+        case KMEANS_E5M2: return MPK_SIMT(e5m2_t);
     }
+#undef MPK_SIMT
     return cudaErrorInvalidValue;
 }
 
@@ -368,13 +364,13 @@ cudaError_t smalld_dispatch(int dist, const Problem& p, const W* X, const void* 
 cudaError_t launch_assign_simt(int work, int dist, const Problem& p, const void* Xl,
                                const void* xn, const void* sx, const void* Cl, const void* cn,
                                const void* sc, int32_t* labels, double* acc_sse,
-                               double* acc_changed, cudaStream_t s) {
+                               double* acc_changed, cudaStream_t s, const int* row_list) {
     launches_add(1);
     if (work == KMEANS_FP64)
         return simt_dispatch<double>(dist, p, Xl, xn, sx, Cl, cn, sc, labels, acc_sse,
-                                     acc_changed, s);
-    return simt_dispatch<float>(dist, p, Xl, xn, sx, Cl, cn, sc, labels, acc_sse, acc_changed,
-                                s);
+                                     acc_changed, s, row_list);
+    return simt_dispatch<float>(dist, p, Xl, xn, sx, Cl, cn, sc, labels, acc_sse, acc_changed, s,
+                                row_list);
 }
 
 bool smalld_supported(int d, int k) { return d <= SD_D && k <= SD_K; }

@@ -7,18 +7,26 @@
 // (fp32 accumulation: reading Z2/Z3). The epilogue warps read the accumulator with tcgen05.ld
 // (one thread = one TMEM lane = one point) and fold
 //     v_ij = fma(-2 s_i s_j, acc_ij, ||c_j||^2)          (Alg 4 line 6)
-// into a running per-point (min, argmin) in registers, lowest j on ties (reading Z12): the
-// n x k distance matrix never leaves the SM. Only labels, the changed-label count and the SSE_t
-// partial (sum_i max(0, ||x_i||^2 + min_j v_ij)) are written.
+// into per-point (min, argmin) chains in registers, merged with lowest-j-on-ties (reading
+// Z12): the n x k distance matrix never leaves the SM. Only labels, the changed-label count and
+// the SSE_t partial (sum_i max(0, ||x_i||^2 + min_j v_ij)) are written.
 //
-// Structure (persistent, one CTA per SM, 192 threads):
-//   warp 0      TMA producer: A = R row-blocks of X~ per group (ring of 2R slots, so the next
-//               group prefetches while this one computes), B = centroid tiles (ring of S_B).
-//   warp 1      MMA issuer (one elected thread): for each centroid tile, R MMAs (one per
-//               row-block) into 4 rotating TMEM accumulators of 128 columns; tcgen05.commit
-//               signals "accumulator full" and "smem slot free".
-//   warps 2..5  epilogue: TMEM -> registers -> fma + argmin; arrive "accumulator empty".
-// B tiles are re-streamed from L2 once per group of R*128 points (C~ is at most 256 KB).
+// FINAL mode (Alg 3 step 7, "computed in precision u") runs the same contraction
+// as a certified filter: the epilogue also keeps the second-smallest v, and a row whose gap
+// v_(2) - v_(1) exceeds twice a rigorous bound on |v^ - v| (operand rounding, fp32
+// accumulation, and the working-precision evaluation's own error) gets the
+// low-precision argmin, which then provably equals the working-precision argmin. Other rows are
+// appended to a list that the CUDA-core working-precision kernel re-evaluates.
+//
+// Structure (persistent, one CTA per SM, 384 threads):
+//   warp 0      A producer (TMA): R row-blocks of X~ per group, ring of 2R slots (the next group
+//               prefetches while the current one computes).
+//   warp 2      B producer (TMA): centroid tiles, ring of SB stages (runs ahead independently).
+//   warp 1      MMA issuer (one elected thread): per centroid tile, R MMAs (one per row-block)
+//               into rotating TMEM accumulators; tcgen05.commit frees smem and signals TMEM.
+//   warps 4-11  epilogue, two warpgroups: warpgroup w handles the row-blocks r = w (mod 2),
+//               so one warpgroup computes while the other waits on TMEM.
+// C~ is at most 256 KB (L2-resident) and is re-streamed once per group of R*128 points.
 #include <cuda.h>
 
 #include <string>
@@ -31,13 +39,15 @@ namespace mpk {
 namespace tcdev {
 
 constexpr int BM = 128;
-constexpr int NUM_ACC = 4;
-constexpr int ACC_COLS = 128;
-constexpr int kThreads = 192;
+constexpr int kNonEpiWarps = 4;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = (kNonEpiWarps + kEpiWarps) * 32;
+constexpr int MAX_ACC = 8;
+constexpr int NCH = 8;   // independent argmin chains per point
 
 struct Params {
     int64_t n;
-    int k, k_pad, BN, NT, KB, SWZ, R, SB;
+    int k, k_pad, d, d_pad, BN, NT, KB, SWZ, R, SB, nacc, acc_cols, tmem_cols;
     uint32_t a_tile_bytes, b_tile_bytes, kb_a_bytes, kb_b_bytes;
     uint32_t idesc;
     int guard, is_f8;
@@ -48,6 +58,11 @@ struct Params {
     int32_t* labels;
     double* acc_sse;
     double* acc_changed;
+    // FINAL mode: uncertified rows are appended here
+    int* fb_count;
+    int* fb_rows;
+    double u_low;     // unit roundoff of the filter operands
+    double eta_low;   // half the smallest subnormal of the filter format (absolute underflow)
 };
 
 MPK_DEV uint32_t smem_u32(const void* p) {
@@ -137,38 +152,73 @@ MPK_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[32]) {
 }
 MPK_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-template <int R>
+
+// Fold 32 accumulator columns j0..j0+31 into the chains: v = fma(acc, -2 s_i s_j, ||c_j||^2).
+// TOP2 also tracks the second-smallest value of each chain.
+template <bool GUARD, bool TOP2>
+MPK_DEV void fold32(const uint32_t (&v)[32], const float* cn_s, const float* sc_s, float m2,
+                    int j0, float (&cv)[NCH], int (&cj)[NCH], float (&c2)[NCH]) {
+    const float4* cn4 = reinterpret_cast<const float4*>(cn_s + j0);
+    const float4* sc4 = reinterpret_cast<const float4*>(sc_s + j0);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const float4 cc = cn4[e];
+        float s[4] = {-2.0f, -2.0f, -2.0f, -2.0f};
+        if (GUARD) {
+            const float4 ss = sc4[e];
+            s[0] = m2 * ss.x; s[1] = m2 * ss.y; s[2] = m2 * ss.z; s[3] = m2 * ss.w;
+        }
+        const float cnv[4] = {cc.x, cc.y, cc.z, cc.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float x = fmaf(__uint_as_float(v[4 * e + u]), s[u], cnv[u]);
+            const int c = (e & 1) * 4 + u;
+            if (TOP2) {
+                const bool p = x < cv[c];
+                const float t2 = fminf(c2[c], x);
+                c2[c] = p ? cv[c] : t2;
+                cv[c] = p ? x : cv[c];
+                cj[c] = p ? (j0 + 4 * e + u) : cj[c];
+            } else {
+                if (x < cv[c]) { cv[c] = x; cj[c] = j0 + 4 * e + u; }
+            }
+        }
+    }
+}
+
+template <int R, bool FINAL>
 __global__ void __launch_bounds__(kThreads, 1)
 assign_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                  const __grid_constant__ CUtensorMap tmap_c, Params p) {
+    static_assert(R % 2 == 0, "two epilogue warpgroups split the row-blocks by parity");
+    constexpr int RH = R / 2;   // row-blocks per warpgroup
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // 1024-align the dynamic smem base (SW128 atoms)
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const int NA = 2 * R;
     uint8_t* a_base = smem;
     uint8_t* b_base = a_base + (size_t)NA * p.a_tile_bytes;
     float* cn_s = (float*)(b_base + (size_t)p.SB * p.b_tile_bytes);
     float* sc_s = cn_s + p.k_pad;
-    uint64_t* bars = (uint64_t*)(sc_s + (p.guard ? p.k_pad : 0));
+    uint64_t* bars = (uint64_t*)(sc_s + p.k_pad);
     uint64_t* a_full = bars;
     uint64_t* a_empty = a_full + NA;
     uint64_t* b_full = a_empty + NA;
     uint64_t* b_empty = b_full + p.SB;
     uint64_t* t_full = b_empty + p.SB;
-    uint64_t* t_empty = t_full + NUM_ACC;
-    uint32_t* tmem_slot = (uint32_t*)(t_empty + NUM_ACC);
+    uint64_t* t_empty = t_full + MAX_ACC;
+    uint32_t* tmem_slot = (uint32_t*)(t_empty + MAX_ACC);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
     for (int j = threadIdx.x; j < p.k_pad; j += blockDim.x) {
         cn_s[j] = j < p.k ? p.cn[j] : INFINITY;       // padded centroids never win
-        if (p.guard) sc_s[j] = j < p.k ? p.sc[j] : 1.0f;
+        sc_s[j] = (p.guard && j < p.k) ? p.sc[j] : 1.0f;
     }
     if (threadIdx.x == 0) {
         for (int i = 0; i < NA; ++i) { mbar_init(smem_u32(&a_full[i]), 1); mbar_init(smem_u32(&a_empty[i]), 1); }
         for (int i = 0; i < p.SB; ++i) { mbar_init(smem_u32(&b_full[i]), 1); mbar_init(smem_u32(&b_empty[i]), 1); }
-        for (int i = 0; i < NUM_ACC; ++i) { mbar_init(smem_u32(&t_full[i]), 1); mbar_init(smem_u32(&t_empty[i]), 4); }
+        for (int i = 0; i < p.nacc; ++i) { mbar_init(smem_u32(&t_full[i]), 1); mbar_init(smem_u32(&t_empty[i]), 4); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_c)) : "memory");
@@ -176,7 +226,7 @@ assign_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
-                     "r"(NUM_ACC * ACC_COLS)
+                     "r"(p.tmem_cols)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -187,33 +237,39 @@ assign_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
 
     const int64_t rows_per_group = (int64_t)R * BM;
     const int64_t num_groups = (p.n + rows_per_group - 1) / rows_per_group;
+    const int elem_per_swz = p.SWZ / (p.is_f8 ? 1 : 2);
 
     if (warp == 0) {
-        // ------------------------------------------------ TMA producer
+        // ------------------------------------------------ A producer
         if (lane == 0) {
-            uint32_t gi = 0, bi = 0;
-            for (int64_t g = blockIdx.x; g < num_groups; g += gridDim.x, ++gi) {
-                for (int r = 0; r < R; ++r) {
-                    uint32_t u = gi * R + r;
-                    int slot = u % NA;
+            uint32_t u = 0;
+            for (int64_t g = blockIdx.x; g < num_groups; g += gridDim.x) {
+                for (int r = 0; r < R; ++r, ++u) {
+                    const int slot = u % NA;
                     mbar_wait(smem_u32(&a_empty[slot]), ((u / NA) & 1) ^ 1);
-                    uint32_t fb = smem_u32(&a_full[slot]);
+                    const uint32_t fb = smem_u32(&a_full[slot]);
                     mbar_expect_tx(fb, p.a_tile_bytes);
-                    uint32_t dst = smem_u32(a_base + (size_t)slot * p.a_tile_bytes);
-                    int row0 = (int)(g * rows_per_group + r * BM);
+                    const uint32_t dst = smem_u32(a_base + (size_t)slot * p.a_tile_bytes);
+                    const int row0 = (int)(g * rows_per_group + r * BM);
                     for (int kb = 0; kb < p.KB; ++kb)
-                        tma_load_2d(dst + kb * p.kb_a_bytes, &tmap_x, kb * p.SWZ / (p.is_f8 ? 1 : 2),
-                                    row0, fb);
+                        tma_load_2d(dst + kb * p.kb_a_bytes, &tmap_x, kb * elem_per_swz, row0, fb);
                 }
+            }
+        }
+    } else if (warp == 2) {
+        // ------------------------------------------------ B producer
+        if (lane == 0) {
+            uint32_t bi = 0;
+            for (int64_t g = blockIdx.x; g < num_groups; g += gridDim.x) {
                 for (int t = 0; t < p.NT; ++t, ++bi) {
-                    int st = bi % p.SB;
+                    const int st = bi % p.SB;
                     mbar_wait(smem_u32(&b_empty[st]), ((bi / p.SB) & 1) ^ 1);
-                    uint32_t fb = smem_u32(&b_full[st]);
+                    const uint32_t fb = smem_u32(&b_full[st]);
                     mbar_expect_tx(fb, p.b_tile_bytes);
-                    uint32_t dst = smem_u32(b_base + (size_t)st * p.b_tile_bytes);
+                    const uint32_t dst = smem_u32(b_base + (size_t)st * p.b_tile_bytes);
                     for (int kb = 0; kb < p.KB; ++kb)
-                        tma_load_2d(dst + kb * p.kb_b_bytes, &tmap_c, kb * p.SWZ / (p.is_f8 ? 1 : 2),
-                                    t * p.BN, fb);
+                        tma_load_2d(dst + kb * p.kb_b_bytes, &tmap_c, kb * elem_per_swz, t * p.BN,
+                                    fb);
                 }
             }
         }
@@ -224,23 +280,25 @@ assign_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
             const int ksteps = p.SWZ / 32;   // 32-byte K per MMA: 16 fp16/bf16 or 32 e5m2
             for (int64_t g = blockIdx.x; g < num_groups; g += gridDim.x, ++gi) {
                 for (int t = 0; t < p.NT; ++t, ++bi) {
-                    int st = bi % p.SB;
+                    const int st = bi % p.SB;
                     mbar_wait(smem_u32(&b_full[st]), (bi / p.SB) & 1);
                     const uint32_t b_addr = smem_u32(b_base + (size_t)st * p.b_tile_bytes);
                     for (int r = 0; r < R; ++r, ++ai) {
-                        uint32_t u = gi * R + r;
-                        int slot = u % NA;
+                        const uint32_t u = gi * R + r;
+                        const int slot = u % NA;
                         if (t == 0) mbar_wait(smem_u32(&a_full[slot]), (u / NA) & 1);
-                        int buf = ai % NUM_ACC;
-                        mbar_wait(smem_u32(&t_empty[buf]), ((ai / NUM_ACC) & 1) ^ 1);
+                        const int buf = ai % p.nacc;
+                        mbar_wait(smem_u32(&t_empty[buf]), ((ai / p.nacc) & 1) ^ 1);
                         tc_fence_after();
                         const uint32_t a_addr = smem_u32(a_base + (size_t)slot * p.a_tile_bytes);
-                        const uint32_t d_tmem = tmem_base + buf * ACC_COLS;
+                        const uint32_t d_tmem = tmem_base + buf * p.acc_cols;
                         for (int kb = 0; kb < p.KB; ++kb) {
                             for (int ks = 0; ks < ksteps; ++ks) {
-                                uint64_t ad = umma_desc(a_addr + kb * p.kb_a_bytes + ks * 32, p.SWZ);
-                                uint64_t bd = umma_desc(b_addr + kb * p.kb_b_bytes + ks * 32, p.SWZ);
-                                uint32_t accum = (kb | ks) ? 1u : 0u;
+                                const uint64_t ad =
+                                    umma_desc(a_addr + kb * p.kb_a_bytes + ks * 32, p.SWZ);
+                                const uint64_t bd =
+                                    umma_desc(b_addr + kb * p.kb_b_bytes + ks * 32, p.SWZ);
+                                const uint32_t accum = (kb | ks) ? 1u : 0u;
                                 if (p.is_f8) mma_f8(d_tmem, ad, bd, p.idesc, accum);
                                 else mma_f16(d_tmem, ad, bd, p.idesc, accum);
                             }
@@ -252,108 +310,143 @@ assign_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 }
             }
         }
-    } else {
-        // ------------------------------------------------ epilogue (warps 2..5)
-        const int quarter = warp & 3;                 // TMEM lanes 32*quarter .. +31
-        const int q = quarter * 32 + lane;            // row within the row-block
+    } else if (warp >= kNonEpiWarps) {
+        // ------------------------------------------------ epilogue (2 warpgroups)
+        const int wg = (warp - kNonEpiWarps) >> 2;      // row-blocks r = wg (mod 2)
+        const int quarter = warp & 3;                   // TMEM lanes 32*quarter .. +31
+        const int q = quarter * 32 + lane;              // row within the row-block
         const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
+        float cn_max = 0.0f, s_max = 1.0f;
+        if (FINAL) {
+            for (int j = 0; j < p.k; ++j) {
+                cn_max = fmaxf(cn_max, cn_s[j]);
+                s_max = fmaxf(s_max, sc_s[j]);
+            }
+        }
         double my_sse = 0.0, my_changed = 0.0;
-        uint32_t ai = 0;
-        for (int64_t g = blockIdx.x; g < num_groups; g += gridDim.x) {
-            float best[R];
-            int bidx[R];
-            float m2[R];
+        uint32_t gi = 0;
+        for (int64_t g = blockIdx.x; g < num_groups; g += gridDim.x, ++gi) {
+            float cv[RH][NCH], c2[RH][NCH];
+            int cj[RH][NCH];
+            float m2[RH];
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                best[r] = INFINITY;
-                bidx[r] = 0;
-                int64_t row = g * rows_per_group + r * BM + q;
-                m2[r] = (p.guard && row < p.n) ? -2.0f * p.sx[row] : -2.0f;
+            for (int h = 0; h < RH; ++h) {
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) { cv[h][c] = INFINITY; c2[h][c] = INFINITY; cj[h][c] = 0; }
+                const int64_t row = g * rows_per_group + (2 * h + wg) * BM + q;
+                m2[h] = (p.guard && row < p.n) ? -2.0f * p.sx[row] : -2.0f;
             }
             for (int t = 0; t < p.NT; ++t) {
 #pragma unroll
-                for (int r = 0; r < R; ++r, ++ai) {
-                    int buf = ai % NUM_ACC;
-                    mbar_wait(smem_u32(&t_full[buf]), (ai / NUM_ACC) & 1);
+                for (int h = 0; h < RH; ++h) {
+                    const int r = 2 * h + wg;
+                    const uint32_t ai = (gi * p.NT + t) * R + r;
+                    const int buf = ai % p.nacc;
+                    mbar_wait(smem_u32(&t_full[buf]), (ai / p.nacc) & 1);
                     tc_fence_after();
-                    const uint32_t col0 = tmem_base + lane_addr + buf * ACC_COLS;
-                    float bv = best[r];
-                    int bj = bidx[r];
-                    if ((p.BN & 31) == 0) {
-                        for (int c = 0; c < p.BN; c += 32) {
-                            uint32_t v[32];
-                            tmem_ld32(col0 + c, v);
+                    const uint32_t col0 = tmem_base + lane_addr + buf * p.acc_cols;
+                    if ((p.BN & 63) == 0) {
+                        for (int c = 0; c < p.BN; c += 64) {
+                            uint32_t v0[32], v1[32];
+                            tmem_ld32(col0 + c, v0);
+                            tmem_ld32(col0 + c + 32, v1);
                             tmem_wait_ld();
                             const int j0 = t * p.BN + c;
-                            const float4* cn4 = reinterpret_cast<const float4*>(cn_s + j0);
-                            if (!p.guard) {
-#pragma unroll
-                                for (int e = 0; e < 8; ++e) {
-                                    float4 cc = cn4[e];
-                                    float x0 = fmaf(__uint_as_float(v[4 * e + 0]), -2.0f, cc.x);
-                                    float x1 = fmaf(__uint_as_float(v[4 * e + 1]), -2.0f, cc.y);
-                                    float x2 = fmaf(__uint_as_float(v[4 * e + 2]), -2.0f, cc.z);
-                                    float x3 = fmaf(__uint_as_float(v[4 * e + 3]), -2.0f, cc.w);
-                                    if (x0 < bv) { bv = x0; bj = j0 + 4 * e + 0; }
-                                    if (x1 < bv) { bv = x1; bj = j0 + 4 * e + 1; }
-                                    if (x2 < bv) { bv = x2; bj = j0 + 4 * e + 2; }
-                                    if (x3 < bv) { bv = x3; bj = j0 + 4 * e + 3; }
-                                }
+                            if (p.guard) {
+                                fold32<true, FINAL>(v0, cn_s, sc_s, m2[h], j0, cv[h], cj[h], c2[h]);
+                                fold32<true, FINAL>(v1, cn_s, sc_s, m2[h], j0 + 32, cv[h], cj[h], c2[h]);
                             } else {
-                                const float4* sc4 = reinterpret_cast<const float4*>(sc_s + j0);
-#pragma unroll
-                                for (int e = 0; e < 8; ++e) {
-                                    float4 cc = cn4[e];
-                                    float4 ss = sc4[e];
-                                    float x0 = fmaf(__uint_as_float(v[4 * e + 0]), m2[r] * ss.x, cc.x);
-                                    float x1 = fmaf(__uint_as_float(v[4 * e + 1]), m2[r] * ss.y, cc.y);
-                                    float x2 = fmaf(__uint_as_float(v[4 * e + 2]), m2[r] * ss.z, cc.z);
-                                    float x3 = fmaf(__uint_as_float(v[4 * e + 3]), m2[r] * ss.w, cc.w);
-                                    if (x0 < bv) { bv = x0; bj = j0 + 4 * e + 0; }
-                                    if (x1 < bv) { bv = x1; bj = j0 + 4 * e + 1; }
-                                    if (x2 < bv) { bv = x2; bj = j0 + 4 * e + 2; }
-                                    if (x3 < bv) { bv = x3; bj = j0 + 4 * e + 3; }
-                                }
+                                fold32<false, FINAL>(v0, cn_s, sc_s, m2[h], j0, cv[h], cj[h], c2[h]);
+                                fold32<false, FINAL>(v1, cn_s, sc_s, m2[h], j0 + 32, cv[h], cj[h], c2[h]);
                             }
                         }
-                    } else {
-                        for (int c = 0; c < p.BN; c += 16) {
-                            uint32_t v[32];
-                            tmem_ld16(col0 + c, v);
-                            tmem_wait_ld();
-                            const int j0 = t * p.BN + c;
+                    } else if ((p.BN & 31) == 0) {
+                        uint32_t v0[32];
+                        tmem_ld32(col0, v0);
+                        tmem_wait_ld();
+                        const int j0 = t * p.BN;
+                        if (p.guard) fold32<true, FINAL>(v0, cn_s, sc_s, m2[h], j0, cv[h], cj[h], c2[h]);
+                        else fold32<false, FINAL>(v0, cn_s, sc_s, m2[h], j0, cv[h], cj[h], c2[h]);
+                    } else {   // BN == 16
+                        uint32_t v[32];
+                        tmem_ld16(col0, v);
+                        tmem_wait_ld();
+                        const int j0 = t * p.BN;
 #pragma unroll
-                            for (int e = 0; e < 16; ++e) {
-                                float s = p.guard ? m2[r] * sc_s[j0 + e] : -2.0f;
-                                float x = fmaf(__uint_as_float(v[e]), s, cn_s[j0 + e]);
-                                if (x < bv) { bv = x; bj = j0 + e; }
+                        for (int e = 0; e < 16; ++e) {
+                            const float s = p.guard ? m2[h] * sc_s[j0 + e] : -2.0f;
+                            const float x = fmaf(__uint_as_float(v[e]), s, cn_s[j0 + e]);
+                            const int c = e & 7;
+                            if (FINAL) {
+                                const bool pr = x < cv[h][c];
+                                const float t2 = fminf(c2[h][c], x);
+                                c2[h][c] = pr ? cv[h][c] : t2;
+                                cv[h][c] = pr ? x : cv[h][c];
+                                cj[h][c] = pr ? (j0 + e) : cj[h][c];
+                            } else if (x < cv[h][c]) {
+                                cv[h][c] = x;
+                                cj[h][c] = j0 + e;
                             }
                         }
                     }
-                    best[r] = bv;
-                    bidx[r] = bj;
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(smem_u32(&t_empty[buf]));
                 }
             }
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                int64_t row = g * rows_per_group + r * BM + q;
-                if (row < p.n) {
-                    int old = p.labels[row];
-                    if (old != bidx[r]) my_changed += 1.0;
-                    p.labels[row] = bidx[r];
-                    double md = (double)p.xn[row] + (double)best[r];
+            for (int h = 0; h < RH; ++h) {
+                int w = 0;
+                float b1 = cv[h][0];
+                int j1 = cj[h][0];
+#pragma unroll
+                for (int c = 1; c < NCH; ++c) {
+                    if (cv[h][c] < b1 || (cv[h][c] == b1 && cj[h][c] < j1)) { b1 = cv[h][c]; j1 = cj[h][c]; w = c; }
+                }
+                const int64_t row = g * rows_per_group + (2 * h + wg) * BM + q;
+                if (row >= p.n) continue;
+                if (!FINAL) {
+                    const int old = p.labels[row];
+                    if (old != j1) my_changed += 1.0;
+                    p.labels[row] = j1;
+                    const double md = (double)p.xn[row] + (double)b1;
                     my_sse += md > 0.0 ? md : 0.0;
+                } else {
+                    float b2 = INFINITY;
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c) b2 = fminf(b2, c == w ? c2[h][c] : cv[h][c]);
+                    p.labels[row] = j1;
+                    // certification: |v^ - v| <= E, |fl32(v) - v| <= B32
+                    const double xn = (double)p.xn[row];
+                    const double si = p.guard ? (double)p.sx[row] : 1.0;
+                    const double cmax = (double)cn_max, smax = (double)s_max;
+                    const double S = sqrt(fmax(xn, 0.0) * fmax(cmax, 0.0)) * (1.0 + 1e-6);
+                    const double u32 = 5.9604644775390625e-08;
+                    const double ul = p.u_low;
+                    const double gacc = (double)(p.d_pad + 2) * 2.384185791015625e-07;
+                    const double gd = (double)p.d * u32 / (1.0 - (double)p.d * u32);
+                    const double E = 2.0 * (2.0 * ul + ul * ul + gacc + 2.0 * u32) * S +
+                                     2.0 * p.eta_low * sqrt((double)p.d) *
+                                         (si * sqrt(fmax(cmax, 0.0)) + smax * sqrt(fmax(xn, 0.0))) +
+                                     u32 * (cmax + 2.0 * S);
+                    const double B32 = gd * 2.0 * S + u32 * (cmax + 2.0 * S);
+                    const double thr = 2.0 * (E + B32) * 1.001;
+                    const bool ok = isfinite(b1) && isfinite(xn) && isfinite(cmax) &&
+                                    ((double)b2 - (double)b1 > thr);
+                    if (!ok) {
+                        const int slot = atomicAdd(p.fb_count, 1);
+                        p.fb_rows[slot] = (int)row;
+                    }
                 }
             }
         }
-        my_sse = warp_sum(my_sse);
-        my_changed = warp_sum(my_changed);
-        if (lane == 0) {
-            if (p.acc_sse) atomicAdd(p.acc_sse, my_sse);
-            if (p.acc_changed && my_changed != 0.0) atomicAdd(p.acc_changed, my_changed);
+        if (!FINAL) {
+            my_sse = warp_sum(my_sse);
+            my_changed = warp_sum(my_changed);
+            if (lane == 0) {
+                if (p.acc_sse) atomicAdd(p.acc_sse, my_sse);
+                if (p.acc_changed && my_changed != 0.0) atomicAdd(p.acc_changed, my_changed);
+            }
         }
     }
     tc_fence_before();
@@ -361,7 +454,7 @@ assign_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
     tc_fence_after();
     if (warp == 1) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                     "r"(NUM_ACC * ACC_COLS)
+                     "r"(p.tmem_cols)
                      : "memory");
     }
 }
@@ -391,8 +484,8 @@ int tc_dpad(int dist, int d) {
 bool tc_supported(int dist, int d_pad, int k) {
     if (dist != KMEANS_FP16 && dist != KMEANS_BF16 && dist != KMEANS_E5M2) return false;
     int rb = d_pad * esize_of(dist);
-    if (rb > 512) return false;    // d <= 256 (fp16/bf16) / 512 (e5m2): A tile <= 64 KB
-    if (k < 16) return false;      // tiny k: the SIMT kernels are the right tool
+    if (rb > 512) return false;    // A tile <= 64 KB
+    if (k < 16) return false;      // tiny k: the CUDA-core kernels are the right tool
     return true;
 }
 
@@ -439,6 +532,12 @@ static bool encode(CUtensorMap* m, int dist, const void* base, int64_t rows, int
     return true;
 }
 
+template <int R, bool FINAL>
+static cudaError_t set_smem(size_t bytes) {
+    return cudaFuncSetAttribute(tcdev::assign_tc_kernel<R, FINAL>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
 TcPlan* tc_plan_create(int dist, int64_t n, int d, int d_pad, int k, const void* Xl,
                        const void* Cl, std::string* err) {
     TcPlan* pl = new TcPlan();
@@ -448,52 +547,77 @@ TcPlan* tc_plan_create(int dist, int64_t n, int d, int d_pad, int k, const void*
     const int RB = d_pad * es;
     const int SWZ = RB >= 128 ? 128 : RB;   // 32, 64 or 128
     const int KB = RB / SWZ;
-    int BN = k >= 128 ? 128 : ((k + 15) / 16) * 16;
-    if (BN > 32 && (BN & 31)) BN = ((BN + 31) / 32) * 32;
+    const double rate = dist == KMEANS_E5M2 ? 8192.0 : 4096.0;   // dense MAC / clk / SM
+    const size_t budget = 227 * 1024;
+    // Choose (BN, R, SB): enough B stages in flight to cover the L2 -> smem latency
+    // (>= ~4096 MMA cycles), then the largest R*BN (less re-streaming), then more stages.
+    int bestBN = 0, bestR = 0, bestSB = 0;
+    double best_key[3] = {-1, -1, -1};
+    for (int bn_cap : {128, 64, 32}) {
+        int bn = k >= bn_cap ? bn_cap : ((k + 15) / 16) * 16;
+        if (bn > 32 && (bn & 31)) bn = ((bn + 31) / 32) * 32;
+        const int nt = (k + bn - 1) / bn;
+        const size_t fixed = 1024 + (size_t)nt * bn * 8 + 64 * 8 + 64;
+        for (int r : {4, 2}) {
+            const size_t a = (size_t)2 * r * tcdev::BM * RB;
+            const size_t b = (size_t)bn * RB;
+            if (fixed + a + 2 * b > budget) continue;
+            int sb = (int)std::min<size_t>(8, (budget - fixed - a) / b);
+            const double stage = (double)r * tcdev::BM * bn * d_pad / rate;
+            const double key[3] = {std::min(stage * sb, 4096.0), (double)r * bn, (double)sb};
+            bool better = false;
+            for (int q = 0; q < 3; ++q) {
+                if (key[q] != best_key[q]) { better = key[q] > best_key[q]; break; }
+            }
+            if (better) {
+                for (int q = 0; q < 3; ++q) best_key[q] = key[q];
+                bestBN = bn; bestR = r; bestSB = sb;
+            }
+        }
+    }
+    if (!bestR) { if (err) *err = "tile does not fit in shared memory"; delete pl; return nullptr; }
+    const int BN = bestBN, R = bestR, SB = bestSB;
     const int NT = (k + BN - 1) / BN;
     const int k_pad = NT * BN;
-    const uint32_t a_tile = (uint32_t)tcdev::BM * RB;
-    const uint32_t b_tile = (uint32_t)BN * RB;
-    const size_t budget = 227 * 1024;
-    int R = 0, SB = 0;
-    for (int r : {4, 2, 1}) {
-        for (int sb : {4, 3, 2}) {
-            size_t bytes = 1024 + (size_t)2 * r * a_tile + (size_t)sb * b_tile +
-                           (size_t)k_pad * 8 + 64 * 8 + 16;
-            if (bytes <= budget) { R = r; SB = sb; break; }
-        }
-        if (R) break;
-    }
-    if (!R) { if (err) *err = "tile does not fit in shared memory"; delete pl; return nullptr; }
     pl->R = R;
     tcdev::Params& p = pl->prm;
     p = tcdev::Params{};
-    p.k = k; p.k_pad = k_pad; p.BN = BN; p.NT = NT; p.KB = KB; p.SWZ = SWZ; p.R = R; p.SB = SB;
-    p.a_tile_bytes = a_tile; p.b_tile_bytes = b_tile;
+    p.k = k; p.k_pad = k_pad; p.d = d; p.d_pad = d_pad; p.BN = BN; p.NT = NT; p.KB = KB;
+    p.SWZ = SWZ; p.R = R; p.SB = SB;
+    p.acc_cols = BN < 32 ? 32 : BN;
+    p.nacc = std::min(tcdev::MAX_ACC, 512 / p.acc_cols);
+    int cols = p.nacc * p.acc_cols;
+    int pw = 32;
+    while (pw < cols) pw <<= 1;
+    p.tmem_cols = pw;
+    p.a_tile_bytes = (uint32_t)tcdev::BM * RB;
+    p.b_tile_bytes = (uint32_t)BN * RB;
     p.kb_a_bytes = (uint32_t)tcdev::BM * SWZ;
     p.kb_b_bytes = (uint32_t)BN * SWZ;
     p.is_f8 = dist == KMEANS_E5M2;
+    // filter constants for FINAL mode (unit roundoff, half smallest subnormal)
+    p.u_low = dist == KMEANS_FP16 ? 0x1p-11 : (dist == KMEANS_BF16 ? 0x1p-8 : 0x1p-3);
+    p.eta_low = dist == KMEANS_FP16 ? 0x1p-25 : (dist == KMEANS_BF16 ? 0x1p-134 : 0x1p-17);
     // instruction descriptor: fp32 accumulate, K-major A/B, M = 128, N = BN
-    uint32_t fmt = dist == KMEANS_BF16 ? 1u : (dist == KMEANS_E5M2 ? 1u : 0u);
+    const uint32_t fmt = dist == KMEANS_BF16 ? 1u : (dist == KMEANS_E5M2 ? 1u : 0u);
     p.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(BN >> 3) << 17) |
               ((uint32_t)(tcdev::BM >> 4) << 24);
-    pl->smem_bytes = 1024 + (size_t)2 * R * a_tile + (size_t)SB * b_tile + (size_t)k_pad * 8 +
-                     64 * 8 + 16;
+    pl->smem_bytes = 1024 + (size_t)2 * R * p.a_tile_bytes + (size_t)SB * p.b_tile_bytes +
+                     (size_t)k_pad * 8 + 2 * tcdev::MAX_ACC * 8 + (size_t)(4 * R + 2 * SB) * 8 +
+                     64;
+    if (pl->smem_bytes > budget + 1024) {
+        if (err) *err = "smem plan overflow";
+        delete pl;
+        return nullptr;
+    }
     if (!encode(&pl->tmap_x, dist, Xl, n, d_pad, SWZ, tcdev::BM, err) ||
         !encode(&pl->tmap_c, dist, Cl, k, d_pad, SWZ, BN, err)) {
         delete pl;
         return nullptr;
     }
-    cudaError_t e = cudaSuccess;
-    if (R == 4)
-        e = cudaFuncSetAttribute(tcdev::assign_tc_kernel<4>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->smem_bytes);
-    else if (R == 2)
-        e = cudaFuncSetAttribute(tcdev::assign_tc_kernel<2>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->smem_bytes);
-    else
-        e = cudaFuncSetAttribute(tcdev::assign_tc_kernel<1>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->smem_bytes);
+    cudaError_t e = R == 4 ? set_smem<4, false>(pl->smem_bytes) : set_smem<2, false>(pl->smem_bytes);
+    if (e == cudaSuccess)
+        e = R == 4 ? set_smem<4, true>(pl->smem_bytes) : set_smem<2, true>(pl->smem_bytes);
     if (e != cudaSuccess) {
         if (err) *err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
         delete pl;
@@ -504,10 +628,30 @@ TcPlan* tc_plan_create(int dist, int64_t n, int d, int d_pad, int k, const void*
 
 void tc_plan_destroy(TcPlan* p) { delete p; }
 
+static cudaError_t launch_impl(TcPlan* pl, const tcdev::Params& p, bool final_mode,
+                               cudaStream_t s) {
+    const int64_t groups = (p.n + (int64_t)pl->R * tcdev::BM - 1) / ((int64_t)pl->R * tcdev::BM);
+    const int grid = (int)(groups < kNumSMs ? groups : kNumSMs);
+    if (grid < 1) return cudaSuccess;
+    launches_add(1);
+    const size_t smem = pl->smem_bytes;
+    if (pl->R == 4) {
+        if (final_mode)
+            tcdev::assign_tc_kernel<4, true><<<grid, tcdev::kThreads, smem, s>>>(pl->tmap_x, pl->tmap_c, p);
+        else
+            tcdev::assign_tc_kernel<4, false><<<grid, tcdev::kThreads, smem, s>>>(pl->tmap_x, pl->tmap_c, p);
+    } else {
+        if (final_mode)
+            tcdev::assign_tc_kernel<2, true><<<grid, tcdev::kThreads, smem, s>>>(pl->tmap_x, pl->tmap_c, p);
+        else
+            tcdev::assign_tc_kernel<2, false><<<grid, tcdev::kThreads, smem, s>>>(pl->tmap_x, pl->tmap_c, p);
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_assign_tc(TcPlan* pl, const Problem& pb, const float* xn, const float* sx,
                              const float* cn, const float* sc, int32_t* labels, double* acc_sse,
                              double* acc_changed, cudaStream_t s) {
-    launches_add(1);
     tcdev::Params p = pl->prm;
     p.n = pb.n;
     p.guard = pb.guard;
@@ -515,17 +659,20 @@ cudaError_t launch_assign_tc(TcPlan* pl, const Problem& pb, const float* xn, con
     p.labels = labels;
     p.acc_sse = acc_sse;
     p.acc_changed = acc_changed;
-    size_t smem = pl->smem_bytes;
-    int64_t groups = (pb.n + (int64_t)pl->R * tcdev::BM - 1) / ((int64_t)pl->R * tcdev::BM);
-    int grid = (int)(groups < kNumSMs ? groups : kNumSMs);
-    if (grid < 1) return cudaSuccess;
-    if (pl->R == 4)
-        tcdev::assign_tc_kernel<4><<<grid, tcdev::kThreads, smem, s>>>(pl->tmap_x, pl->tmap_c, p);
-    else if (pl->R == 2)
-        tcdev::assign_tc_kernel<2><<<grid, tcdev::kThreads, smem, s>>>(pl->tmap_x, pl->tmap_c, p);
-    else
-        tcdev::assign_tc_kernel<1><<<grid, tcdev::kThreads, smem, s>>>(pl->tmap_x, pl->tmap_c, p);
-    return cudaGetLastError();
+    return launch_impl(pl, p, false, s);
+}
+
+cudaError_t launch_final_tc(TcPlan* pl, const Problem& pb, const float* xn, const float* sx,
+                            const float* cn, const float* sc, int32_t* labels, int* fb_count,
+                            int* fb_rows, cudaStream_t s) {
+    tcdev::Params p = pl->prm;
+    p.n = pb.n;
+    p.guard = pb.guard;
+    p.xn = xn; p.sx = sx; p.cn = cn; p.sc = sc;
+    p.labels = labels;
+    p.fb_count = fb_count;
+    p.fb_rows = fb_rows;
+    return launch_impl(pl, p, true, s);
 }
 
 }  // namespace mpk

@@ -51,6 +51,17 @@ struct kmeans_ctx {
     bool xl_alias = false;
 
     TcPlan* tc = nullptr;
+    // final-pass filter (Alg 3 step 7): an fp16 guarded copy when the loop operands cannot
+    // serve (E5M2, or overflowed unguarded operands); allocated on first use.
+    TcPlan* fin = nullptr;
+    void* fin_Xl = nullptr;
+    void* fin_Cl = nullptr;
+    void* fin_sx = nullptr;
+    void* fin_sc = nullptr;
+    int fin_dpad = 0;
+    bool fin_failed = false;
+    int* fbc = nullptr;            // fallback-row counter
+    int64_t last_fallback = 0;     // rows re-evaluated on CUDA cores in the last final pass
     int dist_kernel = 0;
     AccLayout L{0, 0};
 
@@ -135,6 +146,10 @@ cudaError_t dalloc(T** p, size_t bytes) {
 
 void free_all(kmeans_ctx* h) {
     if (h->tc) tc_plan_destroy(h->tc);
+    if (h->fin) tc_plan_destroy(h->fin);
+    void* fin_bufs[] = {h->fin_Xl, h->fin_Cl, h->fin_sx, h->fin_sc, h->fbc};
+    for (void* b : fin_bufs)
+        if (b) cudaFree(b);
     void* bufs[] = {h->Xw, h->xl_alias ? nullptr : h->Xl, h->xn, h->sx, h->Cw, h->Cl, h->cn,
                     h->sc, h->labels, h->acc, h->cnt, h->offs, h->cursor, h->perm, h->trace,
                     h->shift, h->scale, h->partials, h->census, h->sse_dev};
@@ -233,6 +248,7 @@ int create_impl(int64_t n, int32_t d, int32_t k, int work, int dist, int flags,
     CA(dalloc(&h->partials, (size_t)h->npartials * d * 2 * sizeof(double)));
     CA(dalloc(&h->census, 4 * sizeof(unsigned long long)));
     CA(dalloc(&h->sse_dev, 4 * sizeof(double)));
+    CA(dalloc(&h->fbc, 4 * sizeof(int)));
     if (h->dist_kernel == DK_TCGEN05) {
         std::string e;
         h->tc = tc_plan_create(dist, n, d, h->d_pad, k, h->Xl, h->Cl, &e);
@@ -339,6 +355,88 @@ int prep_centroids(kmeans_ctx* h) {
     return 0;
 }
 
+// Alg 3 step 7: labels = argmin_j of the working-precision expanded distance with
+// the final centroids. With tcgen05 available the contraction runs as a certified filter
+// (launch_final_tc): rows whose low-precision top-2 gap exceeds the rigorous error bound keep
+// the filter's argmin, which equals the working-precision argmin; the remaining rows are
+// re-evaluated by the CUDA-core kernel in working precision. Otherwise the CUDA-core kernel
+// evaluates every row.
+int final_assign(kmeans_ctx* h, const Problem& pf) {
+    cudaStream_t s = h->stream;
+    const int64_t n = h->n;
+    const int d = h->d, k = h->k;
+    h->last_fallback = -1;
+    // working-precision norms of the final centroids
+    CK(launch_prep(h->work, h->work, h->Cw, k, d, d, 0, h->cn, nullptr, h->Cl, nullptr, s));
+    TcPlan* plan = nullptr;
+    const void* fx_sx = nullptr;
+    const void* fx_sc = nullptr;
+    int fguard = 0, fdpad = 0;
+    if (h->dist_kernel == DK_TCGEN05 && h->work == KMEANS_FP32) {
+        unsigned long long cen[4];
+        CK(cudaMemcpyAsync(cen, h->census, sizeof(cen), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        bool reuse = (h->dist == KMEANS_FP16 || h->dist == KMEANS_BF16) && cen[0] == 0;
+        if (reuse) {
+            // loop operands: rebuild C~ from the final centroids, check it stayed finite
+            CK(cudaMemsetAsync(h->census + 2, 0, 2 * sizeof(unsigned long long), s));
+            CK(launch_prep(h->work, h->dist, h->Cw, k, d, h->d_pad, h->guard, h->cn, h->sc, h->Cl,
+                           h->census + 2, s));
+            CK(cudaMemcpyAsync(cen, h->census, sizeof(cen), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (cen[2] == 0) {
+                plan = h->tc;
+                fx_sx = h->sx; fx_sc = h->sc; fguard = h->guard; fdpad = h->d_pad;
+            }
+        }
+        if (!plan && !h->fin_failed) {
+            if (!h->fin) {
+                h->fin_dpad = tc_dpad(KMEANS_FP16, d);
+                cudaError_t e1 = cudaMalloc(&h->fin_Xl, (size_t)n * h->fin_dpad * 2);
+                cudaError_t e2 = cudaMalloc(&h->fin_Cl, (size_t)k * h->fin_dpad * 2);
+                cudaError_t e3 = cudaMalloc(&h->fin_sx, (size_t)n * 4);
+                cudaError_t e4 = cudaMalloc(&h->fin_sc, (size_t)k * 4);
+                std::string err;
+                if (e1 == cudaSuccess && e2 == cudaSuccess && e3 == cudaSuccess &&
+                    e4 == cudaSuccess && tc_supported(KMEANS_FP16, h->fin_dpad, k))
+                    h->fin = tc_plan_create(KMEANS_FP16, n, d, h->fin_dpad, k, h->fin_Xl,
+                                            h->fin_Cl, &err);
+                cudaGetLastError();
+                if (!h->fin) h->fin_failed = true;
+            }
+            if (h->fin) {
+                // guarded fp16 operands (Alg 4 scaling: never overflows)
+                CK(launch_prep(h->work, KMEANS_FP16, h->Xw, n, d, h->fin_dpad, 1, h->xn,
+                               h->fin_sx, h->fin_Xl, nullptr, s));
+                CK(launch_prep(h->work, KMEANS_FP16, h->Cw, k, d, h->fin_dpad, 1, h->cn,
+                               h->fin_sc, h->fin_Cl, nullptr, s));
+                plan = h->fin;
+                fx_sx = h->fin_sx; fx_sc = h->fin_sc; fguard = 1; fdpad = h->fin_dpad;
+            }
+        }
+    }
+    if (plan) {
+        Problem p{n, d, k, fdpad, fguard};
+        CK(cudaMemsetAsync(h->fbc, 0, sizeof(int), s));
+        CK(launch_final_tc(plan, p, (const float*)h->xn, (const float*)fx_sx,
+                           (const float*)h->cn, (const float*)fx_sc, h->labels, h->fbc, h->perm,
+                           s));
+        int nfb = 0;
+        CK(cudaMemcpyAsync(&nfb, h->fbc, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        h->last_fallback = nfb;
+        if (nfb > 0) {
+            Problem pl{nfb, d, k, d, 0};
+            CK(launch_assign_simt(h->work, h->work, pl, h->Xw, h->xn, nullptr, h->Cw, h->cn,
+                                  nullptr, h->labels, nullptr, nullptr, s, h->perm));
+        }
+        return 0;
+    }
+    CK(launch_assign_simt(h->work, h->work, pf, h->Xw, h->xn, nullptr, h->Cw, h->cn, nullptr,
+                          h->labels, nullptr, nullptr, s));
+    return 0;
+}
+
 int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, double tol,
              int32_t* labels_out, void* cent_out, double* sse_out, int32_t* iters_out) {
     if (!X || !C0) return fail(h, KMEANS_EINVAL, "X and C0 are required");
@@ -414,12 +512,8 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
 
     // ---- A8: final assignment in working precision + direct-formula SSE -------------------
     {
-        // cn recomputed from the final centroids; operands are the work-precision X and C
-        // (Cl holds a work-precision copy of C here).
-        CK(launch_prep(h->work, h->work, h->Cw, k, d, d, 0, h->cn, nullptr, h->Cl, nullptr, s));
-        Problem p{n, d, k, d, 0};
-        CK(launch_assign_simt(h->work, h->work, p, h->Xw, h->xn, nullptr, h->Cl, h->cn, nullptr,
-                              h->labels, nullptr, nullptr, s));
+        Problem pf{n, d, k, d, 0};
+        if (int rc = final_assign(h, pf)) return rc;
         CK(cudaMemsetAsync(h->sse_dev, 0, sizeof(double), s));
         CK(launch_final_sse(h->work, h->Xw, n, d, h->Cw, h->labels, h->sse_dev, s));
         if (h->comm)
@@ -478,6 +572,7 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
     }
     st.n_dist_launches = it;
     st.n_kernel_launches = launches_read() - launches0;
+    st.n_final_fallback = h->last_fallback;
     int warn = 0;
     if (st.n_nonfinite > 0) warn |= KMEANS_WARN_NONFINITE;
     if (any_empty) warn |= KMEANS_WARN_EMPTY;

@@ -72,3 +72,39 @@ def test_tc_vs_simt_same_fit(dist):
     assert res[0][2] == "tcgen05" and res[1][2] == "simt_low"
     assert abs(res[0][0] - res[1][0]) <= 1e-4 * res[1][0]
     assert np.mean(res[0][1] == res[1][1]) > 0.995
+
+
+@pytest.mark.parametrize("dist,guard", [("fp16", False), ("bf16", False), ("e5m2", False),
+                                        ("fp16", True), ("e5m2", True)])
+def test_final_pass_certified_filter(dist, guard):
+    """Alg 3 step 7 via the certified tensor-core filter: the final labels equal the
+    working-precision argmin for the returned centroids (checked against an fp64 evaluation,
+    mismatches allowed only within the fp32 evaluation error), with few CUDA-core fallbacks."""
+    X, _, C0 = synth.make("c3_blobs_1m_d64", n=25000, seed=3)
+    C0 = C0[:96].copy()
+    km = mpk.KMeans(len(X), 64, 96, "fp32", dist, norm="zscore", guard=guard)
+    lab = torch.empty(len(X), dtype=torch.int32, device="cuda")
+    cent = torch.empty((96, 64), dtype=torch.float32, device="cuda")
+    rc, sse, it = km.fit(dev(X), dev(C0), max_iter=6, tol=-1.0, labels=lab, centroids=cent)
+    st = km.stats()
+    shift = np.empty(64, np.float32)
+    scale = np.empty(64, np.float32)
+    mpk.kmeans_get_transform(km.h, shift, scale)
+    km.close()
+    assert st["dist_kernel"] == "tcgen05"
+    assert 0 <= st["n_final_fallback"] <= 0.01 * len(X)
+    ref = oracle.fit(X, C0, work="fp32", dist=dist, norm="zscore", guard=guard, max_iter=6,
+                     tol=-1.0)
+    Xn = oracle.apply_normalization(X, ref["shift"], ref["scale"], "fp32")
+    C = cent.cpu().numpy().astype(np.float64)
+    g = lab.cpu().numpy()
+    want, _ = oracle.final(Xn, C, work="fp32")
+    D = (Xn * Xn).sum(1)[:, None] - 2 * Xn @ C.T + (C * C).sum(1)[None, :]
+    bad = np.nonzero(g != want)[0]
+    if bad.size:
+        tol = 2 * (66 * 2.0 ** -24) * ((Xn * Xn).sum(1) + 2 * np.sqrt((Xn * Xn).sum(1) * (C * C).sum(1).max())
+                                       + (C * C).sum(1).max())
+        gap = D[bad, g[bad]] - D[bad, want[bad]]
+        assert np.all(gap <= tol[bad]), gap.max()
+    direct = float(np.sum((Xn - C[g]) ** 2))
+    assert abs(sse - direct) <= 1e-6 * direct
