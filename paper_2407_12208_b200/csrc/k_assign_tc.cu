@@ -33,6 +33,10 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "tc_common.cuh"
+#include "tc_pair.h"
+
+#include <stdlib.h>
 
 namespace mpk {
 
@@ -43,7 +47,6 @@ constexpr int kNonEpiWarps = 4;
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = (kNonEpiWarps + kEpiWarps) * 32;
 constexpr int MAX_ACC = 8;
-constexpr int NCH = 8;   // independent argmin chains per point
 
 struct Params {
     int64_t n;
@@ -64,127 +67,6 @@ struct Params {
     double u_low;     // unit roundoff of the filter operands
     double eta_low;   // half the smallest subnormal of the filter format (absolute underflow)
 };
-
-MPK_DEV uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-MPK_DEV void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-MPK_DEV void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-                 : "memory");
-}
-MPK_DEV void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-MPK_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n\t}" ::"r"(bar),
-        "r"(parity)
-        : "memory");
-}
-MPK_DEV void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
-        : "memory");
-}
-MPK_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-MPK_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-MPK_DEV void tc_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                     bar)
-                 : "memory");
-}
-MPK_DEV void mma_f16(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-        "l"(a), "l"(b), "r"(idesc), "r"(accum)
-        : "memory");
-}
-MPK_DEV void mma_f8(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-        "l"(a), "l"(b), "r"(idesc), "r"(accum)
-        : "memory");
-}
-// K-major operand, canonical swizzled layout: rows of SWZ bytes, 8-row atoms (SBO = 8*SWZ).
-MPK_DEV uint64_t umma_desc(uint32_t saddr, int swz) {
-    uint64_t layout = swz == 128 ? 2ull : (swz == 64 ? 4ull : 6ull);
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-    d |= (uint64_t)1u << 16;                              // LBO (unused for swizzled K-major)
-    d |= (uint64_t)(((8u * (uint32_t)swz) >> 4) & 0x3FFFu) << 32;   // SBO
-    d |= (uint64_t)1u << 46;                              // descriptor version (sm_100)
-    d |= layout << 61;
-    return d;
-}
-MPK_DEV void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-        "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
-        "%28, %29, %30, %31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
-          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-          "=r"(r[31])
-        : "r"(taddr));
-}
-MPK_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-        "%11, %12, %13, %14, %15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-}
-MPK_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-
-// Fold 32 accumulator columns j0..j0+31 into the chains: v = fma(acc, -2 s_i s_j, ||c_j||^2).
-// TOP2 also tracks the second-smallest value of each chain.
-template <bool GUARD, bool TOP2>
-MPK_DEV void fold32(const uint32_t (&v)[32], const float* cn_s, const float* sc_s, float m2,
-                    int j0, float (&cv)[NCH], int (&cj)[NCH], float (&c2)[NCH]) {
-    const float4* cn4 = reinterpret_cast<const float4*>(cn_s + j0);
-    const float4* sc4 = reinterpret_cast<const float4*>(sc_s + j0);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-        const float4 cc = cn4[e];
-        float s[4] = {-2.0f, -2.0f, -2.0f, -2.0f};
-        if (GUARD) {
-            const float4 ss = sc4[e];
-            s[0] = m2 * ss.x; s[1] = m2 * ss.y; s[2] = m2 * ss.z; s[3] = m2 * ss.w;
-        }
-        const float cnv[4] = {cc.x, cc.y, cc.z, cc.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const float x = fmaf(__uint_as_float(v[4 * e + u]), s[u], cnv[u]);
-            const int c = (e & 1) * 4 + u;
-            if (TOP2) {
-                const bool p = x < cv[c];
-                const float t2 = fminf(c2[c], x);
-                c2[c] = p ? cv[c] : t2;
-                cv[c] = p ? x : cv[c];
-                cj[c] = p ? (j0 + 4 * e + u) : cj[c];
-            } else {
-                if (x < cv[c]) { cv[c] = x; cj[c] = j0 + 4 * e + u; }
-            }
-        }
-    }
-}
 
 template <int R, bool FINAL>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -466,9 +348,11 @@ assign_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
 // ----------------------------------------------------------------------------------------------
 struct TcPlan {
     int dist, d, d_pad, k, R, esize;
+    int kind;                      // 2 = CTA-pair centroid-stationary, 1 = streaming
     int64_t n;
     CUtensorMap tmap_x, tmap_c;
-    tcdev::Params prm;
+    tcdev::Params prm;             // kind 1
+    tcdev::PairParams pp;          // kind 2
     size_t smem_bytes;
 };
 
@@ -544,6 +428,24 @@ TcPlan* tc_plan_create(int dist, int64_t n, int d, int d_pad, int k, const void*
     pl->dist = dist; pl->n = n; pl->d = d; pl->d_pad = d_pad; pl->k = k;
     const int es = esize_of(dist);
     pl->esize = es;
+    // Preferred: CTA pairs with the centroid tiles resident in shared memory (k_assign_tc2.cu).
+    const char* force = getenv("MPK_TC_KIND");
+    if (!(force && force[0] == '1')) {
+        size_t smem = 0;
+        if (tcdev::pair_plan(dist, d, d_pad, k, &pl->pp, &smem)) {
+            const int swz = pl->pp.SWZ;
+            if (encode(&pl->tmap_x, dist, Xl, n, d_pad, swz, 128, err) &&
+                encode(&pl->tmap_c, dist, Cl, k, d_pad, swz, tcdev::pair_box_rows(pl->pp), err) &&
+                tcdev::pair_set_smem(smem) == cudaSuccess) {
+                pl->kind = 2;
+                pl->smem_bytes = smem;
+                pl->R = 2;
+                return pl;
+            }
+            cudaGetLastError();
+        }
+    }
+    pl->kind = 1;
     const int RB = d_pad * es;
     const int SWZ = RB >= 128 ? 128 : RB;   // 32, 64 or 128
     const int KB = RB / SWZ;
@@ -659,6 +561,12 @@ cudaError_t launch_assign_tc(TcPlan* pl, const Problem& pb, const float* xn, con
     p.labels = labels;
     p.acc_sse = acc_sse;
     p.acc_changed = acc_changed;
+    if (pl->kind == 2) {
+        tcdev::PairParams q = pl->pp;
+        q.n = pb.n; q.guard = pb.guard; q.xn = xn; q.sx = sx; q.cn = cn; q.sc = sc;
+        q.labels = labels; q.acc_sse = acc_sse; q.acc_changed = acc_changed;
+        return tcdev::pair_launch(pl->tmap_x, pl->tmap_c, q, false, pl->smem_bytes, s);
+    }
     return launch_impl(pl, p, false, s);
 }
 
@@ -672,6 +580,12 @@ cudaError_t launch_final_tc(TcPlan* pl, const Problem& pb, const float* xn, cons
     p.labels = labels;
     p.fb_count = fb_count;
     p.fb_rows = fb_rows;
+    if (pl->kind == 2) {
+        tcdev::PairParams q = pl->pp;
+        q.n = pb.n; q.guard = pb.guard; q.xn = xn; q.sx = sx; q.cn = cn; q.sc = sc;
+        q.labels = labels; q.fb_count = fb_count; q.fb_rows = fb_rows;
+        return tcdev::pair_launch(pl->tmap_x, pl->tmap_c, q, true, pl->smem_bytes, s);
+    }
     return launch_impl(pl, p, true, s);
 }
 

@@ -1,0 +1,39 @@
+// tc_pair.h — the CTA-pair (cta_group::2), centroid-stationary distance + argmin kernel.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mpk {
+namespace tcdev {
+
+struct PairParams {
+    int64_t n;
+    int k, k_pad, d, d_pad, NB, NT, KB, SWZ, SA, nacc, tmem_cols;
+    uint32_t a_tile_bytes;   // 128 rows x row bytes (this CTA's half of M = 256)
+    uint32_t b_half_bytes;   // NB/2 rows x row bytes (this CTA's half of one centroid tile)
+    uint32_t kb_a_bytes, kb_b_bytes;
+    uint32_t idesc;          // M = 256, N = NB, fp32 accumulate
+    int guard, is_f8;
+    const float* xn;
+    const float* sx;
+    const float* cn;
+    const float* sc;
+    int32_t* labels;
+    double* acc_sse;
+    double* acc_changed;
+    int* fb_count;
+    int* fb_rows;
+    double u_low, eta_low;
+};
+
+// Fill the static part of PairParams and the dynamic smem size for (dist, d_pad, k); false if
+// the resident centroid halves plus two X~ slots do not fit in shared memory.
+bool pair_plan(int dist, int d, int d_pad, int k, PairParams* p, size_t* smem_bytes);
+int pair_box_rows(const PairParams& p);   // TMA box rows for the centroid map (NB / 2)
+cudaError_t pair_set_smem(size_t bytes);
+cudaError_t pair_launch(const CUtensorMap& tmap_x, const CUtensorMap& tmap_c, const PairParams& p,
+                        bool final_mode, size_t smem_bytes, cudaStream_t s);
+
+}  // namespace tcdev
+}  // namespace mpk
