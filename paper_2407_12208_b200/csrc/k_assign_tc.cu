@@ -259,15 +259,16 @@ assign_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                             const float s = p.guard ? m2[h] * sc_s[j0 + e] : -2.0f;
                             const float x = fmaf(__uint_as_float(v[e]), s, cn_s[j0 + e]);
                             const int c = e & 7;
+                            const int grp = (j0 + e) >> 3;   // chain c = (j0 + e) & 7
                             if (FINAL) {
                                 const bool pr = x < cv[h][c];
                                 const float t2 = fminf(c2[h][c], x);
                                 c2[h][c] = pr ? cv[h][c] : t2;
                                 cv[h][c] = pr ? x : cv[h][c];
-                                cj[h][c] = pr ? (j0 + e) : cj[h][c];
+                                cj[h][c] = pr ? grp : cj[h][c];
                             } else if (x < cv[h][c]) {
                                 cv[h][c] = x;
-                                cj[h][c] = j0 + e;
+                                cj[h][c] = grp;
                             }
                         }
                     }
@@ -279,12 +280,9 @@ assign_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
 #pragma unroll
             for (int h = 0; h < RH; ++h) {
                 int w = 0;
-                float b1 = cv[h][0];
-                int j1 = cj[h][0];
-#pragma unroll
-                for (int c = 1; c < NCH; ++c) {
-                    if (cv[h][c] < b1 || (cv[h][c] == b1 && cj[h][c] < j1)) { b1 = cv[h][c]; j1 = cj[h][c]; w = c; }
-                }
+                float b1;
+                int j1;
+                merge_chains(cv[h], cj[h], b1, j1, &w);
                 const int64_t row = g * rows_per_group + (2 * h + wg) * BM + q;
                 if (row >= p.n) continue;
                 if (!FINAL) {

@@ -214,11 +214,9 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             }
             // merge the 8 chains: lowest value, then lowest index (sequential-scan semantics)
             int w = 0;
-            float b1 = cv[0];
-            int j1 = cj[0];
-#pragma unroll
-            for (int c = 1; c < NCH; ++c)
-                if (cv[c] < b1 || (cv[c] == b1 && cj[c] < j1)) { b1 = cv[c]; j1 = cj[c]; w = c; }
+            float b1;
+            int j1;
+            merge_chains(cv, cj, b1, j1, &w);
             float b2 = INFINITY;
             if (FINAL) {
 #pragma unroll

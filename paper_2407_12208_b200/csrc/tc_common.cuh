@@ -101,11 +101,17 @@ MPK_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: 
 
 // Fold 32 accumulator columns j0..j0+31 into the chains: v = fma(acc, -2 s_i s_j, ||c_j||^2).
 // TOP2 also tracks the second-smallest value of each chain.
+// Fold 32 accumulator columns j0..j0+31 (j0 a multiple of 8) into the chains:
+//   v = fma(acc, -2 s_i s_j, ||c_j||^2).
+// Chain c takes the columns j = 8g + c; it records the GROUP g of its minimum (one add per 8
+// columns instead of per column); the column is recovered as 8 g + c when chains merge.
+// TOP2 also tracks the second-smallest value of each chain.
 template <bool GUARD, bool TOP2>
 MPK_DEV void fold32(const uint32_t (&v)[32], const float* cn_s, const float* sc_s, float m2,
-                    int j0, float (&cv)[NCH], int (&cj)[NCH], float (&c2)[NCH]) {
+                    int j0, float (&cv)[NCH], int (&cg)[NCH], float (&c2)[NCH]) {
     const float4* cn4 = reinterpret_cast<const float4*>(cn_s + j0);
     const float4* sc4 = reinterpret_cast<const float4*>(sc_s + j0);
+    const int g0 = j0 >> 3;
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
         const float4 cc = cn4[e];
@@ -115,6 +121,7 @@ MPK_DEV void fold32(const uint32_t (&v)[32], const float* cn_s, const float* sc_
             s[0] = m2 * ss.x; s[1] = m2 * ss.y; s[2] = m2 * ss.z; s[3] = m2 * ss.w;
         }
         const float cnv[4] = {cc.x, cc.y, cc.z, cc.w};
+        const int g = g0 + (e >> 1);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const float x = fmaf(__uint_as_float(v[4 * e + u]), s[u], cnv[u]);
@@ -124,14 +131,28 @@ MPK_DEV void fold32(const uint32_t (&v)[32], const float* cn_s, const float* sc_
                 const float t2 = fminf(c2[c], x);
                 c2[c] = p ? cv[c] : t2;
                 cv[c] = p ? x : cv[c];
-                cj[c] = p ? (j0 + 4 * e + u) : cj[c];
+                cg[c] = p ? g : cg[c];
             } else {
-                if (x < cv[c]) { cv[c] = x; cj[c] = j0 + 4 * e + u; }
+                if (x < cv[c]) { cv[c] = x; cg[c] = g; }
             }
         }
     }
 }
 
+// Merge the chains of one point: smallest value, then smallest column (the sequential scan's
+// result). Returns the winning chain in *w (for the TOP2 second minimum).
+MPK_DEV void merge_chains(const float (&cv)[NCH], const int (&cg)[NCH], float& b1, int& j1,
+                          int* w) {
+    b1 = cv[0];
+    j1 = cg[0] * 8;
+    int wc = 0;
+#pragma unroll
+    for (int c = 1; c < NCH; ++c) {
+        const int j = cg[c] * 8 + c;
+        if (cv[c] < b1 || (cv[c] == b1 && j < j1)) { b1 = cv[c]; j1 = j; wc = c; }
+    }
+    if (w) *w = wc;
+}
 
 // ---------------------------------------------------------------- CTA-pair (cta_group::2) helpers
 MPK_DEV uint32_t cluster_ctarank() {
@@ -149,7 +170,7 @@ MPK_DEV uint32_t mapa(uint32_t local, uint32_t rank) {
     return r;
 }
 MPK_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                  : "memory");
 }
 // TMA load issued by either CTA of the pair; bytes complete on the LEADER's barrier (peer bit
