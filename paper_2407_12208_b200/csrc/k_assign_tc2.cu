@@ -186,26 +186,25 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 const uint32_t col0 = tmem_base + lane_addr + buf * p.NB + col_off;
                 const int jbase = t * p.NB + col_off;
                 {
+                    // software-pipelined TMEM reads: the load of chunk c+1 is in flight while
+                    // chunk c is folded (tcgen05.wait::ld waits for all outstanding loads).
+                    uint32_t va[32], vb[32];
+                    tmem_ld32(col0, va);
+                    tmem_wait_ld();
                     int c = 0;
                     for (; c + 64 <= half; c += 64) {
-                        uint32_t v0[32], v1[32];
-                        tmem_ld32(col0 + c, v0);
-                        tmem_ld32(col0 + c + 32, v1);
+                        tmem_ld32(col0 + c + 32, vb);
+                        if (p.guard) fold32<true, FINAL>(va, cn_s, sc_s, m2, jbase + c, cv, cj, c2);
+                        else fold32<false, FINAL>(va, cn_s, sc_s, m2, jbase + c, cv, cj, c2);
                         tmem_wait_ld();
-                        if (p.guard) {
-                            fold32<true, FINAL>(v0, cn_s, sc_s, m2, jbase + c, cv, cj, c2);
-                            fold32<true, FINAL>(v1, cn_s, sc_s, m2, jbase + c + 32, cv, cj, c2);
-                        } else {
-                            fold32<false, FINAL>(v0, cn_s, sc_s, m2, jbase + c, cv, cj, c2);
-                            fold32<false, FINAL>(v1, cn_s, sc_s, m2, jbase + c + 32, cv, cj, c2);
-                        }
+                        if (c + 64 < half) tmem_ld32(col0 + c + 64, va);
+                        if (p.guard) fold32<true, FINAL>(vb, cn_s, sc_s, m2, jbase + c + 32, cv, cj, c2);
+                        else fold32<false, FINAL>(vb, cn_s, sc_s, m2, jbase + c + 32, cv, cj, c2);
+                        tmem_wait_ld();
                     }
-                    if (c < half) {   // remaining 32 columns (half is a multiple of 32)
-                        uint32_t v0[32];
-                        tmem_ld32(col0 + c, v0);
-                        tmem_wait_ld();
-                        if (p.guard) fold32<true, FINAL>(v0, cn_s, sc_s, m2, jbase + c, cv, cj, c2);
-                        else fold32<false, FINAL>(v0, cn_s, sc_s, m2, jbase + c, cv, cj, c2);
+                    if (c < half) {   // last 32 columns (already in va)
+                        if (p.guard) fold32<true, FINAL>(va, cn_s, sc_s, m2, jbase + c, cv, cj, c2);
+                        else fold32<false, FINAL>(va, cn_s, sc_s, m2, jbase + c, cv, cj, c2);
                     }
                 }
                 tc_fence_before();

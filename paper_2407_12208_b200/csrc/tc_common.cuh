@@ -99,8 +99,14 @@ MPK_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[32]) {
 MPK_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 
-// Fold 32 accumulator columns j0..j0+31 into the chains: v = fma(acc, -2 s_i s_j, ||c_j||^2).
-// TOP2 also tracks the second-smallest value of each chain.
+MPK_DEV float4 lds_f4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr));
+    return v;
+}
+
 // Fold 32 accumulator columns j0..j0+31 (j0 a multiple of 8) into the chains:
 //   v = fma(acc, -2 s_i s_j, ||c_j||^2).
 // Chain c takes the columns j = 8g + c; it records the GROUP g of its minimum (one add per 8
@@ -109,15 +115,15 @@ MPK_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: 
 template <bool GUARD, bool TOP2>
 MPK_DEV void fold32(const uint32_t (&v)[32], const float* cn_s, const float* sc_s, float m2,
                     int j0, float (&cv)[NCH], int (&cg)[NCH], float (&c2)[NCH]) {
-    const float4* cn4 = reinterpret_cast<const float4*>(cn_s + j0);
-    const float4* sc4 = reinterpret_cast<const float4*>(sc_s + j0);
+    const uint32_t cn_a = smem_u32(cn_s + j0);
+    const uint32_t sc_a = smem_u32(sc_s + j0);
     const int g0 = j0 >> 3;
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-        const float4 cc = cn4[e];
+        const float4 cc = lds_f4(cn_a + 16 * e);
         float s[4] = {-2.0f, -2.0f, -2.0f, -2.0f};
         if (GUARD) {
-            const float4 ss = sc4[e];
+            const float4 ss = lds_f4(sc_a + 16 * e);
             s[0] = m2 * ss.x; s[1] = m2 * ss.y; s[2] = m2 * ss.z; s[3] = m2 * ss.w;
         }
         const float cnv[4] = {cc.x, cc.y, cc.z, cc.w};
