@@ -19,6 +19,8 @@
 #include "tc_common.cuh"
 #include "tc_pair.h"
 
+#include <stdlib.h>
+
 namespace mpk {
 namespace tcdev {
 
@@ -297,7 +299,12 @@ bool pair_plan(int dist, int d, int d_pad, int k, PairParams* pp, size_t* smem_b
     const int RB = d_pad * es;
     const int SWZ = RB >= 128 ? 128 : RB;
     const int KB = RB / SWZ;
-    int NB = k >= 256 ? 256 : ((k + 63) / 64) * 64;
+    // Centroid tile width: 128 keeps 4 TMEM accumulators in flight (the MMA runs up to three
+    // tiles ahead of the epilogue); MPK_PAIR_NB overrides (64/128/256) for experiments.
+    int nb_cap = 128;
+    if (const char* e = getenv("MPK_PAIR_NB")) nb_cap = atoi(e);
+    if (nb_cap != 64 && nb_cap != 128 && nb_cap != 256) nb_cap = 128;
+    int NB = k >= nb_cap ? nb_cap : ((k + 63) / 64) * 64;
     const int NT = (k + NB - 1) / NB;
     const int k_pad = NT * NB;
     const size_t b_half = (size_t)(NB / 2) * RB;
