@@ -322,6 +322,7 @@ def main():
                     "dist": st["t_dist_ms"], "update": st["t_update_ms"],
                     "allreduce": st["t_allreduce_ms"], "finalize": st["t_finalize_ms"]},
                 "dist_kernel": kern, "last_sse": sse,
+                "final_pass_cuda_core_rows": st["n_final_fallback"],
                 "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

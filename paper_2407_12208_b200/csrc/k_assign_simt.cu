@@ -271,16 +271,28 @@ __global__ void final_sse_kernel(const W* __restrict__ X, int64_t n, int d,
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    // 4 rows per warp per step: their labels and first column chunks are loaded together so
+    // the pass is bandwidth- rather than latency-bound.
+    constexpr int RW = 4;
     double acc = 0.0;
-    for (int64_t i = warp; i < n; i += nwarps) {
-        const W* x = X + i * d;
-        const W* c = C + (int64_t)labels[i] * d;
-        double a = 0.0;
+    for (int64_t i0 = warp * RW; i0 < n; i0 += nwarps * RW) {
+        int lab[RW];
+#pragma unroll
+        for (int r = 0; r < RW; ++r) lab[r] = (i0 + r < n) ? labels[i0 + r] : 0;
         for (int t = lane; t < d; t += 32) {
-            double df = (double)x[t] - (double)c[t];
-            a = fma(df, df, a);
+            W xv[RW], cv[RW];
+#pragma unroll
+            for (int r = 0; r < RW; ++r) {
+                const bool ok = i0 + r < n;
+                xv[r] = ok ? X[(i0 + r) * d + t] : (W)0;
+                cv[r] = ok ? C[(int64_t)lab[r] * d + t] : (W)0;
+            }
+#pragma unroll
+            for (int r = 0; r < RW; ++r) {
+                const double df = (double)xv[r] - (double)cv[r];
+                acc = fma(df, df, acc);
+            }
         }
-        acc += a;
     }
     acc = warp_sum(acc);
     __shared__ double red[8];

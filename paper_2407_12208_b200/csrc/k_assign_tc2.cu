@@ -149,6 +149,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                             const uint64_t ad = umma_desc(a_addr + kb * p.kb_a_bytes + ks * 32, p.SWZ);
                             const uint64_t bd = umma_desc(b_addr + kb * p.kb_b_bytes + ks * 32, p.SWZ);
                             const uint32_t accum = (kb | ks) ? 1u : 0u;
+                            if (p.dbg & 2) continue;
                             if (p.is_f8) mma2_f8(d_tmem, ad, bd, p.idesc, accum);
                             else mma2_f16(d_tmem, ad, bd, p.idesc, accum);
                         }
@@ -187,7 +188,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 tc_fence_after();
                 const uint32_t col0 = tmem_base + lane_addr + buf * p.NB + col_off;
                 const int jbase = t * p.NB + col_off;
-                {
+                if (!(p.dbg & 1)) {
                     // software-pipelined TMEM reads: the load of chunk c+1 is in flight while
                     // chunk c is folded (tcgen05.wait::ld waits for all outstanding loads).
                     uint32_t va[32], vb[32];
@@ -327,6 +328,7 @@ bool pair_plan(int dist, int d, int d_pad, int k, PairParams* pp, size_t* smem_b
     p.kb_a_bytes = (uint32_t)P_BM * SWZ;
     p.kb_b_bytes = (uint32_t)(NB / 2) * SWZ;
     p.is_f8 = dist == KMEANS_E5M2;
+    if (const char* e = getenv("MPK_PAIR_DBG")) p.dbg = atoi(e);
     p.u_low = dist == KMEANS_FP16 ? 0x1p-11 : (dist == KMEANS_BF16 ? 0x1p-8 : 0x1p-3);
     p.eta_low = dist == KMEANS_FP16 ? 0x1p-25 : (dist == KMEANS_BF16 ? 0x1p-134 : 0x1p-17);
     const uint32_t fmt = dist == KMEANS_BF16 ? 1u : (dist == KMEANS_E5M2 ? 1u : 0u);

@@ -19,10 +19,17 @@ namespace {
 
 constexpr int kStatThreads = 256;
 
+// One kernel for the three column statistics: mode 0 = sum x, mode 1 = sum (x - mu)^2,
+// mode 2 = (min, max). Thread layout: column c = tid % d, row lane = tid / d (d <= 256), else a
+// loop over column blocks. Rows are read in batches of kUnroll per thread (all loads issued
+// before the compensated accumulation, in the same order), so the pass is HBM-bound instead of
+// load-latency-bound; the per-thread summation order is unchanged (deterministic).
+constexpr int kUnroll = 8;
+
 template <typename W>
-__global__ void norm_stats_kernel(int norm, const W* __restrict__ X, int64_t n, int d,
-                                  double* __restrict__ partials /* [nblocks][d][2] */) {
-    // Thread layout: column c = tid % d, row lane r = tid / d (d <= 256), else column loop.
+__global__ void __launch_bounds__(kStatThreads)
+norm_col_stats_kernel(int mode, const W* __restrict__ X, int64_t n, int d,
+                      const double* __restrict__ mu, double* __restrict__ partials) {
     const int tid = threadIdx.x;
     const int lanes = d <= kStatThreads ? kStatThreads / d : 1;
     const int64_t rows_per_block = (n + gridDim.x - 1) / gridDim.x;
@@ -37,18 +44,31 @@ __global__ void norm_stats_kernel(int norm, const W* __restrict__ X, int64_t n, 
         } else {
             c = cbase + tid; lane = 0; active = c < d;
         }
-        double s = 0.0, comp = 0.0;   // ZSCORE: Neumaier sum; MINMAX: s = min, comp = max
-        if (norm == KMEANS_NORM_MINMAX) { s = INFINITY; comp = -INFINITY; }
+        double s = 0.0, comp = 0.0;   // sums: Neumaier (s, comp); minmax: s = min, comp = max
+        if (mode == 2) { s = INFINITY; comp = -INFINITY; }
         if (active) {
-            for (int64_t i = r0 + lane; i < r1; i += lanes) {
-                double x = (double)X[i * d + c];
-                if (norm == KMEANS_NORM_MINMAX) {
-                    s = fmin(s, x);
-                    comp = fmax(comp, x);
-                } else {
-                    double t = s + x;
-                    comp += (fabs(s) >= fabs(x)) ? ((s - t) + x) : ((x - t) + s);
-                    s = t;
+            const double m = (mode == 1) ? mu[c] : 0.0;
+            for (int64_t i0 = r0 + lane; i0 < r1; i0 += (int64_t)lanes * kUnroll) {
+                double xv[kUnroll];
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    const int64_t i = i0 + (int64_t)u * lanes;
+                    xv[u] = i < r1 ? (double)X[i * d + c] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    const int64_t i = i0 + (int64_t)u * lanes;
+                    if (i >= r1) break;
+                    double x = xv[u];
+                    if (mode == 2) {
+                        s = fmin(s, x);
+                        comp = fmax(comp, x);
+                    } else {
+                        if (mode == 1) { const double z = x - m; x = z * z; }
+                        const double t = s + x;
+                        comp += (fabs(s) >= fabs(x)) ? ((s - t) + x) : ((x - t) + s);
+                        s = t;
+                    }
                 }
             }
         }
@@ -59,63 +79,15 @@ __global__ void norm_stats_kernel(int norm, const W* __restrict__ X, int64_t n, 
         if (active && lane == 0) {
             double S = s, Cc = comp;
             for (int l = 1; l < lanes; ++l) {
-                double s2 = sh_s[l * d + c], c2 = sh_c[l * d + c];
-                if (norm == KMEANS_NORM_MINMAX) {
+                const double s2 = sh_s[l * d + c], c2 = sh_c[l * d + c];
+                if (mode == 2) {
                     S = fmin(S, s2);
                     Cc = fmax(Cc, c2);
                 } else {
-                    double t = S + s2;
+                    const double t = S + s2;
                     Cc += ((fabs(S) >= fabs(s2)) ? ((S - t) + s2) : ((s2 - t) + S)) + c2;
                     S = t;
                 }
-            }
-            partials[((int64_t)blockIdx.x * d + c) * 2 + 0] = S;
-            partials[((int64_t)blockIdx.x * d + c) * 2 + 1] = Cc;
-        }
-        __syncthreads();
-        if (d <= kStatThreads) break;
-    }
-}
-
-// Sum of squared deviations from the (final) mean, compensated.
-template <typename W>
-__global__ void norm_var_kernel(const W* __restrict__ X, int64_t n, int d,
-                                const double* __restrict__ mu, double* __restrict__ partials) {
-    const int tid = threadIdx.x;
-    const int lanes = d <= kStatThreads ? kStatThreads / d : 1;
-    const int64_t rows_per_block = (n + gridDim.x - 1) / gridDim.x;
-    const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
-    const int64_t r1 = min(n, r0 + rows_per_block);
-    __shared__ double sh_s[kStatThreads], sh_c[kStatThreads];
-    for (int cbase = 0; cbase < d; cbase += (d <= kStatThreads ? d : kStatThreads)) {
-        int c, lane;
-        bool active;
-        if (d <= kStatThreads) {
-            c = tid % d; lane = tid / d; active = lane < lanes;
-        } else {
-            c = cbase + tid; lane = 0; active = c < d;
-        }
-        double s = 0.0, comp = 0.0;
-        if (active) {
-            const double m = mu[c];
-            for (int64_t i = r0 + lane; i < r1; i += lanes) {
-                double z = (double)X[i * d + c] - m;
-                double x = z * z;
-                double t = s + x;
-                comp += (fabs(s) >= fabs(x)) ? ((s - t) + x) : ((x - t) + s);
-                s = t;
-            }
-        }
-        sh_s[tid] = s;
-        sh_c[tid] = comp;
-        __syncthreads();
-        if (active && lane == 0) {
-            double S = s, Cc = comp;
-            for (int l = 1; l < lanes; ++l) {
-                double s2 = sh_s[l * d + c], c2 = sh_c[l * d + c];
-                double t = S + s2;
-                Cc += ((fabs(S) >= fabs(s2)) ? ((S - t) + s2) : ((s2 - t) + S)) + c2;
-                S = t;
             }
             partials[((int64_t)blockIdx.x * d + c) * 2 + 0] = S;
             partials[((int64_t)blockIdx.x * d + c) * 2 + 1] = Cc;
@@ -172,11 +144,19 @@ template <typename W>
 __global__ void norm_apply_kernel(W* __restrict__ X, int64_t total, int d,
                                   const double* __restrict__ shift,
                                   const double* __restrict__ scale) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int c = (int)(i % d);
-        double z = ((double)X[i] - shift[c]) / scale[c];
-        X[i] = rounder<sizeof(W) == 8 ? KMEANS_FP64 : KMEANS_FP32>::from(z);
+    // x <- round_u((x - shift_c) / scale_c), fp64 arithmetic (correctly rounded division, as
+    // the oracle's O1); the column index is tracked incrementally (no 64-bit modulo).
+    constexpr int WORK = sizeof(W) == 8 ? KMEANS_FP64 : KMEANS_FP32;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    int c = (int)(i % d);
+    const int cstep = (int)(stride % d);
+    for (; i < total; i += stride) {
+        const double z = ((double)X[i] - shift[c]) / scale[c];
+        X[i] = rounder<WORK>::from(z);
+        c += cstep;
+        if (c >= d) c -= d;
     }
 }
 
@@ -267,14 +247,14 @@ cudaError_t launch_norm_stats(int work, int norm, const void* X, int64_t n, int 
                               double* partials, int nblocks, double* a, double* b,
                               cudaStream_t s) {
     launches_add(2);
+    const int mode = norm == KMEANS_NORM_MINMAX ? 2 : 0;
     if (work == KMEANS_FP64)
-        norm_stats_kernel<double><<<nblocks, kStatThreads, 0, s>>>(norm, (const double*)X, n, d,
-                                                                   partials);
+        norm_col_stats_kernel<double><<<nblocks, kStatThreads, 0, s>>>(mode, (const double*)X, n,
+                                                                       d, nullptr, partials);
     else
-        norm_stats_kernel<float><<<nblocks, kStatThreads, 0, s>>>(norm, (const float*)X, n, d,
-                                                                  partials);
-    norm_combine_kernel<<<(d + 127) / 128, 128, 0, s>>>(norm == KMEANS_NORM_MINMAX ? 2 : 0,
-                                                         partials, nblocks, d, a, b);
+        norm_col_stats_kernel<float><<<nblocks, kStatThreads, 0, s>>>(mode, (const float*)X, n,
+                                                                      d, nullptr, partials);
+    norm_combine_kernel<<<(d + 127) / 128, 128, 0, s>>>(mode, partials, nblocks, d, a, b);
     return cudaGetLastError();
 }
 
@@ -282,11 +262,11 @@ cudaError_t launch_norm_ssq(int work, const void* X, int64_t n, int d, double* p
                             int nblocks, const double* mean, double* ssq, cudaStream_t s) {
     launches_add(2);
     if (work == KMEANS_FP64)
-        norm_var_kernel<double><<<nblocks, kStatThreads, 0, s>>>((const double*)X, n, d, mean,
-                                                                 partials);
+        norm_col_stats_kernel<double><<<nblocks, kStatThreads, 0, s>>>(1, (const double*)X, n, d,
+                                                                       mean, partials);
     else
-        norm_var_kernel<float><<<nblocks, kStatThreads, 0, s>>>((const float*)X, n, d, mean,
-                                                                partials);
+        norm_col_stats_kernel<float><<<nblocks, kStatThreads, 0, s>>>(1, (const float*)X, n, d,
+                                                                      mean, partials);
     norm_combine_kernel<<<(d + 127) / 128, 128, 0, s>>>(0, partials, nblocks, d, ssq, nullptr);
     return cudaGetLastError();
 }

@@ -25,6 +25,7 @@ struct PairParams {
     int* fb_count;
     int* fb_rows;
     double u_low, eta_low;
+    int dbg;                 // debug: bit0 skip epilogue folding, bit1 skip MMAs (timing only)
 };
 
 // Fill the static part of PairParams and the dynamic smem size for (dist, d_pad, k); false if
