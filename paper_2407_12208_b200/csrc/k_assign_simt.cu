@@ -146,6 +146,132 @@ assign_simt_kernel(Problem p, const LT* __restrict__ Xl, const W* __restrict__ x
 }
 
 // ------------------------------------------------------------------------------------------
+// K6b: register-tiled (8 x 8 per thread, 128 x 128 per block) CUDA-core variant for fp32
+// accumulation — the fp32 working mode and the final pass's CUDA-core rows. Same arithmetic as
+// K6: products summed in order t = 0..d-1 by fp32 FMA, v = fma(-2 s_i s_j, dot, ||c_j||^2),
+// (value, index) argmin with lowest index on ties.
+// ------------------------------------------------------------------------------------------
+constexpr int B2M = 128, B2N = 128, B2K = 16, B2T = 256;
+
+template <typename LT, typename W>
+__global__ void __launch_bounds__(B2T)
+assign_simt_big_kernel(Problem p, const LT* __restrict__ Xl, const W* __restrict__ xn,
+                       const W* __restrict__ sx, const LT* __restrict__ Cl,
+                       const W* __restrict__ cn, const W* __restrict__ sc,
+                       int32_t* __restrict__ labels, double* acc_sse, double* acc_changed,
+                       const int* __restrict__ rows) {
+    __shared__ __align__(16) float As[B2K][B2M + 4];
+    __shared__ __align__(16) float Bs[B2K][B2N + 4];
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;
+    const int64_t row0 = (int64_t)blockIdx.x * B2M;
+
+    float bestv[8];
+    int bestj[8];
+    W srow[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        bestv[r] = INFINITY;
+        bestj[r] = 0;
+        const int64_t li = row0 + ty * 8 + r;
+        const int64_t row = (rows && li < p.n) ? (int64_t)rows[li] : li;
+        srow[r] = (p.guard && sx && li < p.n) ? sx[row] : (W)1;
+    }
+    // source rows of this block's A tile (each thread loads rows tid/16 + 16 e, column tid%16)
+    int64_t arow[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int64_t li = row0 + (tid >> 4) + 16 * e;
+        arow[e] = li < p.n ? (rows ? (int64_t)rows[li] : li) : -1;
+    }
+    for (int n0 = 0; n0 < p.k; n0 += B2N) {
+        float acc[8][8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[r][c] = 0.0f;
+        for (int k0 = 0; k0 < p.d; k0 += B2K) {
+            const int kk = tid & 15;
+            const int col = k0 + kk;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int r = (tid >> 4) + 16 * e;
+                As[kk][r] = (arow[e] >= 0 && col < p.d) ? (float)widen(Xl[arow[e] * p.d_pad + col]) : 0.0f;
+                const int cj = n0 + r;
+                Bs[kk][r] = (cj < p.k && col < p.d) ? (float)widen(Cl[(int64_t)cj * p.d_pad + col]) : 0.0f;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < B2K; ++q) {
+                const float4 a0 = *reinterpret_cast<const float4*>(&As[q][ty * 8]);
+                const float4 a1 = *reinterpret_cast<const float4*>(&As[q][ty * 8 + 4]);
+                const float4 b0 = *reinterpret_cast<const float4*>(&Bs[q][tx * 8]);
+                const float4 b1 = *reinterpret_cast<const float4*>(&Bs[q][tx * 8 + 4]);
+                const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) acc[r][c] = fmaf(a[r], b[c], acc[r][c]);
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const int j = n0 + tx * 8 + c;
+            if (j < p.k) {
+                const W cnj = cn[j];
+                const W scj = (p.guard && sc) ? sc[j] : (W)1;
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const W m2 = (W)-2 * (srow[r] * scj);
+                    const float v = (float)fma(m2, (W)acc[r][c], cnj);
+                    if (v < bestv[r]) { bestv[r] = v; bestj[r] = j; }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+            const float v2 = __shfl_xor_sync(0xffffffffu, bestv[r], o);
+            const int j2 = __shfl_xor_sync(0xffffffffu, bestj[r], o);
+            argmin_merge(bestv[r], bestj[r], v2, j2);
+        }
+    }
+    double my_sse = 0.0, my_changed = 0.0;
+    if (tx == 0) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int64_t li = row0 + ty * 8 + r;
+            if (li < p.n) {
+                const int64_t row = rows ? (int64_t)rows[li] : li;
+                if (acc_changed && labels[row] != bestj[r]) my_changed += 1.0;
+                labels[row] = bestj[r];
+                if (acc_sse) {
+                    const double md = (double)xn[row] + (double)bestv[r];
+                    my_sse += md > 0.0 ? md : 0.0;
+                }
+            }
+        }
+    }
+    if (acc_sse || acc_changed) {
+        my_sse = warp_sum(my_sse);
+        my_changed = warp_sum(my_changed);
+        __shared__ double red[2][B2T / 32];
+        if ((tid & 31) == 0) { red[0][tid >> 5] = my_sse; red[1][tid >> 5] = my_changed; }
+        __syncthreads();
+        if (tid == 0) {
+            double a = 0, b = 0;
+            for (int w = 0; w < B2T / 32; ++w) { a += red[0][w]; b += red[1][w]; }
+            if (acc_sse) atomicAdd(acc_sse, a);
+            if (acc_changed && b != 0.0) atomicAdd(acc_changed, b);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 // K5 small-d fused assign + update.
 // ------------------------------------------------------------------------------------------
 constexpr int SD_D = 4, SD_K = 8, SD_T = 256;
@@ -310,8 +436,16 @@ cudaError_t simt_dispatch_acc(int dist, const Problem& p, const void* Xl, const 
                               const void* sx, const void* Cl, const void* cn, const void* sc,
                               int32_t* labels, double* acc_sse, double* acc_changed,
                               cudaStream_t s, const int* rows) {
+    if (p.n <= 0) return cudaSuccess;
+    if constexpr (!std::is_same<LT, double>::value && std::is_same<W, float>::value) {
+        // fp32 accumulation with fp32 working precision: the 8 x 8 register-tiled kernel
+        const int64_t b2 = (p.n + B2M - 1) / B2M;
+        assign_simt_big_kernel<LT, W><<<(unsigned)b2, B2T, 0, s>>>(
+            p, (const LT*)Xl, (const W*)xn, (const W*)sx, (const LT*)Cl, (const W*)cn,
+            (const W*)sc, labels, acc_sse, acc_changed, rows);
+        return cudaGetLastError();
+    }
     int64_t blocks = (p.n + BM - 1) / BM;
-    if (blocks == 0) return cudaSuccess;
     // fp64 operands accumulate in fp64; every other operand type in fp32 (reading Z2/Z3)
     using AT = typename std::conditional<std::is_same<LT, double>::value, double, float>::type;
     assign_simt_kernel<LT, AT, W><<<(unsigned)blocks, NT, 0, s>>>(

@@ -74,6 +74,39 @@ __global__ void scan_kernel(const int* __restrict__ cnt, int k, int* __restrict_
     if (threadIdx.x == 0) offs[k] = carry;
 }
 
+// U3 (k <= kHistMax): block-aggregated slot claims. Each block ranks its rows per label in a
+// shared-memory histogram (integer smem atomics), reserves one contiguous range per label with
+// a single global atomic, then writes perm. Global atomics drop from one per row to one per
+// (block, label present).
+constexpr int kScatterRows = 16;
+__global__ void __launch_bounds__(256)
+scatter_block_kernel(const int32_t* __restrict__ labels, int64_t n, int k,
+                     int* __restrict__ cursor, int* __restrict__ perm) {
+    extern __shared__ int sh[];
+    const int64_t base = (int64_t)blockIdx.x * blockDim.x * kScatterRows;
+    for (int j = threadIdx.x; j < k; j += blockDim.x) sh[j] = 0;
+    __syncthreads();
+    int lab[kScatterRows], rk[kScatterRows];
+#pragma unroll
+    for (int r = 0; r < kScatterRows; ++r) {
+        const int64_t i = base + (int64_t)r * blockDim.x + threadIdx.x;
+        lab[r] = i < n ? labels[i] : -1;
+    }
+#pragma unroll
+    for (int r = 0; r < kScatterRows; ++r) rk[r] = lab[r] >= 0 ? atomicAdd(&sh[lab[r]], 1) : 0;
+    __syncthreads();
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        const int c = sh[j];
+        if (c) sh[j] = atomicAdd(&cursor[j], c);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kScatterRows; ++r) {
+        const int64_t i = base + (int64_t)r * blockDim.x + threadIdx.x;
+        if (lab[r] >= 0) perm[sh[lab[r]] + rk[r]] = (int)i;
+    }
+}
+
 __global__ void scatter_kernel(const int32_t* __restrict__ labels, int64_t n,
                                int* __restrict__ cursor, int* __restrict__ perm) {
     const int lane = threadIdx.x & 31;
@@ -167,17 +200,31 @@ segsum_kernel(const W* __restrict__ X, int64_t n, int d, int k, const int* __res
                     for (int q = 0; q < VEC; ++q) xv[u][q] = (W)0;
                 }
             }
+            const int64_t elast = e + u0 + U - 1;
+            if (u0 + U <= cnt && elast < next_boundary) {
+                // common case: the whole batch belongs to the current cluster. Sum the U rows
+                // in the working type first (one conversion to fp64 per batch instead of per
+                // row; the conversion unit, not HBM, bounded the per-row form).
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (u0 + u < cnt) {
-                    int64_t epos = e + u0 + u;
-                    while (epos >= next_boundary) {   // label changes (uniform across the warp)
-                        flush(cur);
-                        ++cur;
-                        next_boundary = offs[cur + 1];
+                for (int q = 0; q < VEC; ++q) {
+                    W s = xv[0][q];
+#pragma unroll
+                    for (int u = 1; u < U; ++u) s += xv[u][q];
+                    acc[q] += (double)s;
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (u0 + u < cnt) {
+                        int64_t epos = e + u0 + u;
+                        while (epos >= next_boundary) {   // label changes (warp-uniform)
+                            flush(cur);
+                            ++cur;
+                            next_boundary = offs[cur + 1];
+                        }
+#pragma unroll
+                        for (int q = 0; q < VEC; ++q) acc[q] += (double)xv[u][q];
                     }
-#pragma unroll
-                    for (int q = 0; q < VEC; ++q) acc[q] += (double)xv[u][q];
                 }
             }
         }
@@ -233,7 +280,12 @@ cudaError_t update_dispatch(const W* X, int64_t n, int d, int k, const int32_t* 
     size_t hist_bytes = k <= kHistMax ? sizeof(int) * k : 0;
     count_kernel<<<g, 256, hist_bytes, s>>>(labels, n, k, cnt);
     scan_kernel<<<1, 1024, 0, s>>>(cnt, k, offs, cursor, acc + L.counts());
-    scatter_kernel<<<g, 256, 0, s>>>(labels, n, cursor, perm);
+    if (k <= kHistMax) {
+        const int64_t sb = (n + 256LL * kScatterRows - 1) / (256LL * kScatterRows);
+        scatter_block_kernel<<<(unsigned)sb, 256, sizeof(int) * k, s>>>(labels, n, k, cursor, perm);
+    } else {
+        scatter_kernel<<<g, 256, 0, s>>>(labels, n, cursor, perm);
+    }
     // segmented sums: ~8 warps per SM-slot, chunks of >= 256 rows
     const int VEC = (sizeof(W) == 8) ? (d <= 32 ? 1 : 2) : (d <= 32 ? 1 : (d <= 64 ? 2 : 4));
     const int colblk = 32 * VEC;
