@@ -300,11 +300,11 @@ bool pair_plan(int dist, int d, int d_pad, int k, PairParams* pp, size_t* smem_b
     const int RB = d_pad * es;
     const int SWZ = RB >= 128 ? 128 : RB;
     const int KB = RB / SWZ;
-    // Centroid tile width: 128 keeps 4 TMEM accumulators in flight (the MMA runs up to three
-    // tiles ahead of the epilogue); MPK_PAIR_NB overrides (64/128/256) for experiments.
-    int nb_cap = 128;
+    // Centroid tile width: 256 (M = 256 x N = 256 MMAs; measured fastest: the per-tile handshake
+    // cost dominates narrower tiles); MPK_PAIR_NB overrides (64/128/256) for experiments.
+    int nb_cap = 256;
     if (const char* e = getenv("MPK_PAIR_NB")) nb_cap = atoi(e);
-    if (nb_cap != 64 && nb_cap != 128 && nb_cap != 256) nb_cap = 128;
+    if (nb_cap != 64 && nb_cap != 128 && nb_cap != 256) nb_cap = 256;
     int NB = k >= nb_cap ? nb_cap : ((k + 63) / 64) * 64;
     const int NT = (k + NB - 1) / NB;
     const int k_pad = NT * NB;
