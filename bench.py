@@ -112,7 +112,7 @@ def cpu_baseline(cfg, dist, norm, guard, target_s=12.0):
     work = cfg.work
     iters = 2
     n_s = min(cfg.n, 4096)
-    X, _, C0 = synth.make(cfg, n=max(n_s, min(cfg.n, 65536)), seed=0)
+    X, _, C0 = synth.make(cfg, n=min(cfg.n, 1 << 20), seed=0)
     C0 = C0[:cfg.k]
     t0 = time.perf_counter()
     oracle.fit(X[:n_s], C0, work=work, dist=dist, norm=norm, guard=guard, max_iter=iters, tol=-1)
@@ -180,6 +180,7 @@ def main():
 
     import paper_2407_12208_b200 as mpk
     import synth
+    from paper_2407_12208_b200 import dist as pdist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -192,8 +193,7 @@ def main():
     norm = cfg.norms[0].replace("+guard", "")
     guard = "+guard" in cfg.norms[0]
     n_total = args.n or cfg.n
-    per = (n_total + world - 1) // world
-    r0, r1 = rank * per, min(n_total, (rank + 1) * per)
+    r0, r1 = pdist.shard_range(n_total, world, rank)
     X, _, C0 = synth.make(cfg, n=n_total, seed=0, row_range=(r0, r1))
     n_local, d, k = X.shape[0], cfg.d, cfg.k
     tdt = torch.float32 if cfg.work == "fp32" else torch.float64
@@ -204,10 +204,8 @@ def main():
     flags = mpk.NORM[norm] | (mpk.KMEANS_GUARD_SCALE if guard else 0) | \
         (mpk.KMEANS_FORCE_SIMT if args.force_simt else 0)
     if world > 1:
-        nid = bytearray(mpk.kmeans_nccl_unique_id() if rank == 0 else bytes(128))
-        t = torch.tensor(list(nid), dtype=torch.uint8, device="cuda")
-        tdist.broadcast(t, 0)
-        h = mpk.kmeans_create_dist(n_local, d, k, cfg.work, dist, flags, bytes(t.cpu().tolist()),
+        nid = pdist.broadcast_nccl_id(mpk.kmeans_nccl_unique_id() if rank == 0 else None)
+        h = mpk.kmeans_create_dist(n_local, d, k, cfg.work, dist, flags, nid,
                                    world, rank)
     else:
         h = mpk.kmeans_create(n_local, d, k, cfg.work, dist, flags)
@@ -240,10 +238,8 @@ def main():
             tdist.barrier()
     ms = e0.elapsed_time(e1)
     st = mpk.stats_dict(mpk.kmeans_get_stats(h))
-    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
-        tdist.all_reduce(ms_t, op=tdist.ReduceOp.MAX)
-    ms = float(ms_t.item())
+        ms = pdist.max_over_ranks(ms)
     evals = n_total * k * args.iters * args.steps
     value = evals / (ms / 1e3)
     iters_per_s = args.iters * args.steps / (ms / 1e3)
@@ -290,10 +286,9 @@ def main():
             mpk.kmeans_fit(h, Xh, Ch, args.iters, -1.0, lab_h, cent_h)
         b.record(stream)
         torch.cuda.synchronize()
-        ems = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device="cuda")
+        ems = a.elapsed_time(b)
         if world > 1:
-            tdist.all_reduce(ems, op=tdist.ReduceOp.MAX)
-        ems = float(ems.item())
+            ems = pdist.max_over_ranks(ems)
         e2e = {"value": n_total * k * args.iters * e_steps / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(X.nbytes + C0.nbytes),
                "d2h_bytes_per_step": int(lab_h.numel() * 4 + cent_h.numel() * cent_h.element_size()

@@ -413,10 +413,26 @@ __global__ void final_sse_kernel(const W* __restrict__ X, int64_t n, int d,
                 xv[r] = ok ? X[(i0 + r) * d + t] : (W)0;
                 cv[r] = ok ? C[(int64_t)lab[r] * d + t] : (W)0;
             }
+            if constexpr (sizeof(W) == 4) {
+                // fp32 differences, squares split exactly (p + e), one conversion per step
+                float s = 0.0f, comp = 0.0f;
 #pragma unroll
-            for (int r = 0; r < RW; ++r) {
-                const double df = (double)xv[r] - (double)cv[r];
-                acc = fma(df, df, acc);
+                for (int r = 0; r < RW; ++r) {
+                    const float df = xv[r] - cv[r];
+                    const float p2 = df * df;
+                    const float e2 = fmaf(df, df, -p2);
+                    const float t = s + p2;
+                    const float z = t - s;
+                    comp += (s - (t - z)) + (p2 - z) + e2;
+                    s = t;
+                }
+                acc += (double)s + (double)comp;
+            } else {
+#pragma unroll
+                for (int r = 0; r < RW; ++r) {
+                    const double df = (double)xv[r] - (double)cv[r];
+                    acc = fma(df, df, acc);
+                }
             }
         }
     }

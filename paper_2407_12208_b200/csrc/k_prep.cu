@@ -152,17 +152,54 @@ __global__ void norm_apply_kernel(W* __restrict__ X, int64_t total, int d,
     if (i >= total) return;
     int c = (int)(i % d);
     const int cstep = (int)(stride % d);
-    for (; i < total; i += stride) {
-        const double z = ((double)X[i] - shift[c]) / scale[c];
-        X[i] = rounder<WORK>::from(z);
-        c += cstep;
-        if (c >= d) c -= d;
+    // 4 elements per thread per step, loads first (memory-level parallelism)
+    for (; i < total; i += 4 * stride) {
+        W xv[4];
+        int cc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t iu = i + (int64_t)u * stride;
+            xv[u] = iu < total ? X[iu] : (W)0;
+            cc[u] = c;
+            c += cstep;
+            if (c >= d) c -= d;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t iu = i + (int64_t)u * stride;
+            if (iu < total) X[iu] = rounder<WORK>::from(((double)xv[u] - shift[cc[u]]) / scale[cc[u]]);
+        }
     }
 }
 
+// ||x||^2 of one row's lane-local values, returned as an fp64 warp total. fp32 rows: each
+// product x*x is split exactly (p + e, e = fma(x, x, -p)) and summed with a compensated fp32
+// TwoSum, then converted once per lane: as accurate as an fp64 sum without one fp32->fp64
+// conversion per element (the conversion unit bounded the per-element form).
+MPK_DEV double lane_sumsq(const float* v, int cnt) {
+    float s = 0.0f, c = 0.0f;
+    for (int q = 0; q < cnt; ++q) {
+        const float p = v[q] * v[q];
+        const float e = fmaf(v[q], v[q], -p);
+        const float t = s + p;
+        const float z = t - s;
+        c += (s - (t - z)) + (p - z) + e;
+        s = t;
+    }
+    return warp_sum((double)s + (double)c);
+}
+MPK_DEV double lane_sumsq(const double* v, int cnt) {
+    double s = 0.0;
+    for (int q = 0; q < cnt; ++q) s = __dadd_rn(s, __dmul_rn(v[q], v[q]));
+    return warp_sum(s);
+}
+
 // ------------------------------------------------------------------------------------------
-// K1 / K3 prep: one warp per row.
+// K1 / K3 prep: one warp per row, the row held in registers (up to 32 * kPrepVPL columns per
+// pass), all loads of a row issued before use.
 // ------------------------------------------------------------------------------------------
+constexpr int kPrepVPL = 8;
+
 template <typename W, int DIST>
 __global__ void prep_kernel(const W* __restrict__ X, int64_t rows, int d, int d_pad, int guard,
                             W* __restrict__ norms, W* __restrict__ scales,
@@ -178,36 +215,57 @@ __global__ void prep_kernel(const W* __restrict__ X, int64_t rows, int d, int d_
     for (int64_t i = warp; i < rows; i += nwarps) {
         const W* x = X + i * d;
         double acc = 0.0;
-        double amax = 0.0;
-        for (int c = lane; c < d; c += 32) {
-            double v = (double)x[c];
-            acc = __dadd_rn(acc, __dmul_rn(v, v));
-            amax = fmax(amax, fabs(v));
+        W amax = (W)0;
+        W v[kPrepVPL];
+        const bool one_pass = d <= 32 * kPrepVPL;
+        // pass 1: norm and infinity norm
+        for (int c0 = 0; c0 < d; c0 += 32 * kPrepVPL) {
+            int cnt = 0;
+#pragma unroll
+            for (int q = 0; q < kPrepVPL; ++q) {
+                const int c = c0 + lane + 32 * q;
+                v[q] = c < d ? x[c] : (W)0;
+                if (c < d) cnt = q + 1;
+            }
+#pragma unroll
+            for (int q = 0; q < kPrepVPL; ++q) amax = fmax(amax, fabs(v[q]));
+            acc += lane_sumsq(v, cnt);
         }
-        acc = warp_sum(acc);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-        double s = 1.0;
-        if (guard && !same) s = (amax == 0.0 || isnan(amax)) ? 1.0 : amax;
+        W s = (W)1;
+        if (guard && !same) s = (amax == (W)0 || isnan(amax)) ? (W)1 : amax;
         if (lane == 0) {
             norms[i] = rounder<WORK>::from(acc);
-            if (scales) scales[i] = (W)s;
+            if (scales) scales[i] = s;
         }
-        const W sw = (W)s;
-        for (int c = lane; c < d_pad; c += 32) {
-            L o;
-            if (c < d) {
-                W v = x[c];
-                W q = (s == 1.0) ? v : v / sw;     // precision-u division (IEEE, RN)
-                o = rounder<DIST>::from(q);
-                if (!same) {
-                    if (is_nonfinite_low(o)) n_nonfinite++;
-                    else if (q != (W)0 && is_zero_or_subnormal_low(o)) n_under++;
+        // pass 2: low-precision operands (from registers when the row fit in one pass)
+        for (int c0 = 0; c0 < d_pad; c0 += 32 * kPrepVPL) {
+            if (!one_pass || c0 > 0) {
+#pragma unroll
+                for (int q = 0; q < kPrepVPL; ++q) {
+                    const int c = c0 + lane + 32 * q;
+                    v[q] = c < d ? x[c] : (W)0;
                 }
-            } else {
-                o = rounder<DIST>::from((W)0);
             }
-            Xl[i * d_pad + c] = o;
+#pragma unroll
+            for (int q = 0; q < kPrepVPL; ++q) {
+                const int c = c0 + lane + 32 * q;
+                if (c >= d_pad) break;
+                L o;
+                if (c < d) {
+                    const W vv = v[q];
+                    const W qv = (s == (W)1) ? vv : vv / s;     // precision-u division (IEEE, RN)
+                    o = rounder<DIST>::from(qv);
+                    if (!same) {
+                        if (is_nonfinite_low(o)) n_nonfinite++;
+                        else if (qv != (W)0 && is_zero_or_subnormal_low(o)) n_under++;
+                    }
+                } else {
+                    o = rounder<DIST>::from((W)0);
+                }
+                Xl[i * d_pad + c] = o;
+            }
         }
     }
     if (census) {

@@ -261,3 +261,28 @@ def test_convergence_stops_early():
     g = gpu_fit(X, C0, "fp64", "fp16", max_iter=300, tol=1e-4)
     assert g["stats"]["converged"] and g["iters"] < 300
     assert not (g["rc"] & mpk.KMEANS_WARN_MAXITER)
+
+
+def test_dist_handle_single_rank_matches_plain_handle():
+    """The NCCL path (kmeans_create_dist, one packed ncclAllReduce per iteration, allreduced
+    normalisation statistics and final SSE) with a 1-rank communicator gives the plain handle's
+    results: exercises every collective call site on the one GPU a gpurun box has."""
+    X, _, C0 = synth.make("c3_blobs_1m_d64", n=20000, seed=9)
+    C0 = C0[:64].copy()
+    n, d, k = X.shape[0], 64, 64
+    outs = []
+    for use_dist in (False, True):
+        flags = mpk.KMEANS_NORM_ZSCORE
+        if use_dist:
+            h = mpk.kmeans_create_dist(n, d, k, "fp32", "fp16", flags, mpk.kmeans_nccl_unique_id(),
+                                       1, 0)
+        else:
+            h = mpk.kmeans_create(n, d, k, "fp32", "fp16", flags)
+        lab = torch.empty(n, dtype=torch.int32, device="cuda")
+        cent = torch.empty((k, d), dtype=torch.float32, device="cuda")
+        rc, sse, it = mpk.kmeans_fit(h, dev(X), dev(C0), 8, -1.0, lab, cent)
+        outs.append((lab.cpu().numpy(), cent.cpu().numpy(), sse))
+        mpk.kmeans_destroy(h)
+    assert np.mean(outs[0][0] == outs[1][0]) > 0.999
+    assert np.allclose(outs[0][1], outs[1][1], rtol=1e-5, atol=1e-6)
+    assert abs(outs[0][2] - outs[1][2]) <= 1e-6 * outs[0][2]
