@@ -188,6 +188,32 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 tc_fence_after();
                 const uint32_t col0 = tmem_base + lane_addr + buf * p.NB + col_off;
                 const int jbase = t * p.NB + col_off;
+                if (half == 128 && !(p.dbg & 1)) {
+                    // Copy-out: this warp's 128 columns go to registers, the accumulator is
+                    // released at once (the next MMA into this buffer overlaps the fold), then
+                    // the values are folded from registers.
+                    uint32_t v0[32], v1[32], v2[32], v3[32];
+                    tmem_ld32(col0, v0);
+                    tmem_ld32(col0 + 32, v1);
+                    tmem_ld32(col0 + 64, v2);
+                    tmem_ld32(col0 + 96, v3);
+                    tmem_wait_ld();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&t_empty[buf]), 0));
+                    if (p.guard) {
+                        fold32<true, FINAL>(v0, cn_s, sc_s, m2, jbase, cv, cj, c2);
+                        fold32<true, FINAL>(v1, cn_s, sc_s, m2, jbase + 32, cv, cj, c2);
+                        fold32<true, FINAL>(v2, cn_s, sc_s, m2, jbase + 64, cv, cj, c2);
+                        fold32<true, FINAL>(v3, cn_s, sc_s, m2, jbase + 96, cv, cj, c2);
+                    } else {
+                        fold32<false, FINAL>(v0, cn_s, sc_s, m2, jbase, cv, cj, c2);
+                        fold32<false, FINAL>(v1, cn_s, sc_s, m2, jbase + 32, cv, cj, c2);
+                        fold32<false, FINAL>(v2, cn_s, sc_s, m2, jbase + 64, cv, cj, c2);
+                        fold32<false, FINAL>(v3, cn_s, sc_s, m2, jbase + 96, cv, cj, c2);
+                    }
+                    continue;
+                }
                 if (!(p.dbg & 1)) {
                     // software-pipelined TMEM reads: the load of chunk c+1 is in flight while
                     // chunk c is folded (tcgen05.wait::ld waits for all outstanding loads).
