@@ -26,7 +26,8 @@ namespace tcdev {
 
 constexpr int P_BM = 128;
 constexpr int P_NON_EPI = 4;
-constexpr int P_EPI = 8;
+constexpr int P_EWG = 4;                 // epilogue warpgroups
+constexpr int P_EPI = 4 * P_EWG;
 constexpr int P_THREADS = (P_NON_EPI + P_EPI) * 32;
 constexpr int P_MAX_ACC = 4;
 constexpr size_t P_BUDGET = 227 * 1024;
@@ -48,10 +49,10 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
     uint8_t* a_base = b_base + (size_t)p.NT * p.b_half_bytes;           // X~ ring
     float* cn_s = (float*)(a_base + (size_t)p.SA * p.a_tile_bytes);
     float* sc_s = cn_s + p.k_pad;
-    float* mg_v = sc_s + p.k_pad;              // [2][128] warpgroup-1 partial minima
-    float* mg_v2 = mg_v + 2 * P_BM;            // [2][128] second minima (FINAL)
-    int* mg_j = (int*)(mg_v2 + 2 * P_BM);      // [2][128]
-    uint64_t* bars = (uint64_t*)(((uintptr_t)(mg_j + 2 * P_BM) + 7) & ~(uintptr_t)7);
+    float* mg_v = sc_s + p.k_pad;              // [2][P_EWG-1][128] partial minima
+    float* mg_v2 = mg_v + 2 * (P_EWG - 1) * P_BM;   // second minima (FINAL)
+    int* mg_j = (int*)(mg_v2 + 2 * (P_EWG - 1) * P_BM);
+    uint64_t* bars = (uint64_t*)(((uintptr_t)(mg_j + 2 * (P_EWG - 1) * P_BM) + 7) & ~(uintptr_t)7);
     uint64_t* a_full = bars;
     uint64_t* a_empty = a_full + p.SA;
     uint64_t* b_full = a_empty + p.SA;
@@ -73,7 +74,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
         mbar_init(smem_u32(b_full), 1);
         for (int i = 0; i < p.nacc; ++i) {
             mbar_init(smem_u32(&t_full[i]), 1);
-            mbar_init(smem_u32(&t_empty[i]), 2 * P_EPI);   // 8 epilogue warps x 2 CTAs
+            mbar_init(smem_u32(&t_empty[i]), 2 * P_EPI);   // every epilogue warp of both CTAs
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x)) : "memory");
@@ -160,12 +161,14 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             }
         }
     } else if (warp >= P_NON_EPI) {
-        // ------------------------------------------------ epilogue: 2 warpgroups split columns
+        // ------------------------------------------------ epilogue: P_EWG warpgroups split the
+        // NB columns of every accumulator (4 warps per SM sub-partition hide TMEM/smem latency)
         const int wg = (warp - P_NON_EPI) >> 2;
         const int quarter = warp & 3;
         const int q = quarter * 32 + lane;                 // row within this CTA's 128
         const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
-        const int col_off = wg * half;
+        const int wcols = p.NB / P_EWG;                    // multiple of 16
+        const int col_off = wg * wcols;
         float cn_max = 0.0f, s_max = 1.0f;
         if (FINAL) {
             for (int j = 0; j < p.k; ++j) {
@@ -177,7 +180,15 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
         uint32_t ai = 0, rbi = 0;
         for (int64_t rb = pair; rb < num_rb; rb += npairs, ++rbi) {
             const int64_t row = rb * rows_per_rb + rank * P_BM + q;
-            const float m2 = (p.guard && row < p.n) ? -2.0f * p.sx[row] : -2.0f;
+            const bool valid = row < p.n;
+            const float m2 = (p.guard && valid) ? -2.0f * p.sx[row] : -2.0f;
+            // prefetch what the row-block epilogue needs (hidden behind the tile loop)
+            int old_label = 0;
+            float xn_row = 0.0f;
+            if (wg == 0 && valid) {
+                xn_row = p.xn[row];
+                if (!FINAL) old_label = p.labels[row];
+            }
             float cv[NCH], c2[NCH];
             int cj[NCH];
 #pragma unroll
@@ -188,52 +199,36 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 tc_fence_after();
                 const uint32_t col0 = tmem_base + lane_addr + buf * p.NB + col_off;
                 const int jbase = t * p.NB + col_off;
-                if (half == 128 && !(p.dbg & 1)) {
-                    // Copy-out: this warp's 128 columns go to registers, the accumulator is
-                    // released at once (the next MMA into this buffer overlaps the fold), then
-                    // the values are folded from registers.
-                    uint32_t v0[32], v1[32], v2[32], v3[32];
-                    tmem_ld32(col0, v0);
-                    tmem_ld32(col0 + 32, v1);
-                    tmem_ld32(col0 + 64, v2);
-                    tmem_ld32(col0 + 96, v3);
-                    tmem_wait_ld();
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&t_empty[buf]), 0));
-                    if (p.guard) {
-                        fold32<true, FINAL>(v0, cn_s, sc_s, m2, jbase, cv, cj, c2);
-                        fold32<true, FINAL>(v1, cn_s, sc_s, m2, jbase + 32, cv, cj, c2);
-                        fold32<true, FINAL>(v2, cn_s, sc_s, m2, jbase + 64, cv, cj, c2);
-                        fold32<true, FINAL>(v3, cn_s, sc_s, m2, jbase + 96, cv, cj, c2);
-                    } else {
-                        fold32<false, FINAL>(v0, cn_s, sc_s, m2, jbase, cv, cj, c2);
-                        fold32<false, FINAL>(v1, cn_s, sc_s, m2, jbase + 32, cv, cj, c2);
-                        fold32<false, FINAL>(v2, cn_s, sc_s, m2, jbase + 64, cv, cj, c2);
-                        fold32<false, FINAL>(v3, cn_s, sc_s, m2, jbase + 96, cv, cj, c2);
-                    }
-                    continue;
-                }
                 if (!(p.dbg & 1)) {
-                    // software-pipelined TMEM reads: the load of chunk c+1 is in flight while
-                    // chunk c is folded (tcgen05.wait::ld waits for all outstanding loads).
-                    uint32_t va[32], vb[32];
-                    tmem_ld32(col0, va);
-                    tmem_wait_ld();
-                    int c = 0;
-                    for (; c + 64 <= half; c += 64) {
-                        tmem_ld32(col0 + c + 32, vb);
-                        if (p.guard) fold32<true, FINAL>(va, cn_s, sc_s, m2, jbase + c, cv, cj, c2);
-                        else fold32<false, FINAL>(va, cn_s, sc_s, m2, jbase + c, cv, cj, c2);
+                    if ((wcols & 31) == 0) {
+                        for (int c = 0; c < wcols; c += 32) {
+                            uint32_t va[32];
+                            tmem_ld32(col0 + c, va);
+                            tmem_wait_ld();
+                            if (p.guard) fold32<true, FINAL>(va, cn_s, sc_s, m2, jbase + c, cv, cj, c2);
+                            else fold32<false, FINAL>(va, cn_s, sc_s, m2, jbase + c, cv, cj, c2);
+                        }
+                    } else {   // wcols == 16
+                        uint32_t va[32];
+                        tmem_ld16(col0, va);
                         tmem_wait_ld();
-                        if (c + 64 < half) tmem_ld32(col0 + c + 64, va);
-                        if (p.guard) fold32<true, FINAL>(vb, cn_s, sc_s, m2, jbase + c + 32, cv, cj, c2);
-                        else fold32<false, FINAL>(vb, cn_s, sc_s, m2, jbase + c + 32, cv, cj, c2);
-                        tmem_wait_ld();
-                    }
-                    if (c < half) {   // last 32 columns (already in va)
-                        if (p.guard) fold32<true, FINAL>(va, cn_s, sc_s, m2, jbase + c, cv, cj, c2);
-                        else fold32<false, FINAL>(va, cn_s, sc_s, m2, jbase + c, cv, cj, c2);
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) {
+                            const int j = jbase + e;
+                            const float s = p.guard ? m2 * sc_s[j] : -2.0f;
+                            const float x = fmaf(__uint_as_float(va[e]), s, cn_s[j]);
+                            const int c = e & 7, grp = j >> 3;
+                            if (FINAL) {
+                                const bool pr = x < cv[c];
+                                const float t2 = fminf(c2[c], x);
+                                c2[c] = pr ? cv[c] : t2;
+                                cv[c] = pr ? x : cv[c];
+                                cj[c] = pr ? grp : cj[c];
+                            } else if (x < cv[c]) {
+                                cv[c] = x;
+                                cj[c] = grp;
+                            }
+                        }
                     }
                 }
                 tc_fence_before();
@@ -250,19 +245,23 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
 #pragma unroll
                 for (int c = 0; c < NCH; ++c) b2 = fminf(b2, c == w ? c2[c] : cv[c]);
             }
+            // warpgroups 1..P_EWG-1 hand their partial to warpgroup 0 through smem
             const int ms = rbi & 1;
-            if (wg == 1) {
-                mg_v[ms * P_BM + q] = b1;
-                mg_j[ms * P_BM + q] = j1;
-                if (FINAL) mg_v2[ms * P_BM + q] = b2;
-                named_bar_arrive(1, 2 * 4 * 32);
+            if (wg != 0) {
+                const int slot = (ms * (P_EWG - 1) + (wg - 1)) * P_BM + q;
+                mg_v[slot] = b1;
+                mg_j[slot] = j1;
+                if (FINAL) mg_v2[slot] = b2;
+                named_bar_arrive(1, P_EPI * 32);
                 continue;
             }
-            named_bar_sync(1, 2 * 4 * 32);
-            {
-                const float ob1 = mg_v[ms * P_BM + q];
-                const int oj1 = mg_j[ms * P_BM + q];
-                const float ob2 = FINAL ? mg_v2[ms * P_BM + q] : INFINITY;
+            named_bar_sync(1, P_EPI * 32);
+#pragma unroll
+            for (int o = 0; o < P_EWG - 1; ++o) {
+                const int slot = (ms * (P_EWG - 1) + o) * P_BM + q;
+                const float ob1 = mg_v[slot];
+                const int oj1 = mg_j[slot];
+                const float ob2 = FINAL ? mg_v2[slot] : INFINITY;
                 if (ob1 < b1 || (ob1 == b1 && oj1 < j1)) {
                     b2 = fminf(ob2, b1);
                     b1 = ob1;
@@ -271,16 +270,15 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                     b2 = fminf(b2, ob1);
                 }
             }
-            if (row >= p.n) continue;
+            if (!valid) continue;
             if (!FINAL) {
-                const int old = p.labels[row];
-                if (old != j1) my_changed += 1.0;
+                if (old_label != j1) my_changed += 1.0;
                 p.labels[row] = j1;
-                const double md = (double)p.xn[row] + (double)b1;
-                my_sse += md > 0.0 ? md : 0.0;
+                const float md = xn_row + b1;
+                my_sse += md > 0.0f ? (double)md : 0.0;
             } else {
                 p.labels[row] = j1;
-                const double xn = (double)p.xn[row];
+                const double xn = (double)xn_row;
                 const double si = p.guard ? (double)p.sx[row] : 1.0;
                 const double cmax = (double)cn_max, smax = (double)s_max;
                 const double S = sqrt(fmax(xn, 0.0) * fmax(cmax, 0.0)) * (1.0 + 1e-6);
@@ -336,7 +334,7 @@ bool pair_plan(int dist, int d, int d_pad, int k, PairParams* pp, size_t* smem_b
     const int k_pad = NT * NB;
     const size_t b_half = (size_t)(NB / 2) * RB;
     const size_t a_tile = (size_t)P_BM * RB;
-    const size_t fixed = 1024 + (size_t)k_pad * 8 + 3 * 2 * P_BM * 4 + 8 +
+    const size_t fixed = 1024 + (size_t)k_pad * 8 + 3 * 2 * (P_EWG - 1) * P_BM * 4 + 8 +
                          (size_t)(2 * 8 + 1 + 2 * P_MAX_ACC) * 8 + 16;
     const size_t bres = (size_t)NT * b_half;
     if (fixed + bres + 2 * a_tile > P_BUDGET) return false;
