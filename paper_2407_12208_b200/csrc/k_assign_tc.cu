@@ -208,13 +208,11 @@ assign_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         double my_sse = 0.0, my_changed = 0.0;
         uint32_t gi = 0;
         for (int64_t g = blockIdx.x; g < num_groups; g += gridDim.x, ++gi) {
-            float cv[RH][NCH], c2[RH][NCH];
-            int cj[RH][NCH];
+            float cv[RH][NCH], c2[RH][NCH], cs[RH][NCH];
             float m2[RH];
 #pragma unroll
             for (int h = 0; h < RH; ++h) {
-#pragma unroll
-                for (int c = 0; c < NCH; ++c) { cv[h][c] = INFINITY; c2[h][c] = INFINITY; cj[h][c] = 0; }
+                chains_init(cv[h], cs[h], c2[h]);
                 const int64_t row = g * rows_per_group + (2 * h + wg) * BM + q;
                 m2[h] = (p.guard && row < p.n) ? -2.0f * p.sx[row] : -2.0f;
             }
@@ -235,11 +233,11 @@ assign_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                             tmem_wait_ld();
                             const int j0 = t * p.BN + c;
                             if (p.guard) {
-                                fold32<true, FINAL>(v0, cn_s, sc_s, m2[h], j0, cv[h], cj[h], c2[h]);
-                                fold32<true, FINAL>(v1, cn_s, sc_s, m2[h], j0 + 32, cv[h], cj[h], c2[h]);
+                                fold32<true, FINAL>(v0, cn_s, sc_s, m2[h], j0, cv[h], cs[h], c2[h]);
+                                fold32<true, FINAL>(v1, cn_s, sc_s, m2[h], j0 + 32, cv[h], cs[h], c2[h]);
                             } else {
-                                fold32<false, FINAL>(v0, cn_s, sc_s, m2[h], j0, cv[h], cj[h], c2[h]);
-                                fold32<false, FINAL>(v1, cn_s, sc_s, m2[h], j0 + 32, cv[h], cj[h], c2[h]);
+                                fold32<false, FINAL>(v0, cn_s, sc_s, m2[h], j0, cv[h], cs[h], c2[h]);
+                                fold32<false, FINAL>(v1, cn_s, sc_s, m2[h], j0 + 32, cv[h], cs[h], c2[h]);
                             }
                         }
                     } else if ((p.BN & 31) == 0) {
@@ -247,8 +245,8 @@ assign_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                         tmem_ld32(col0, v0);
                         tmem_wait_ld();
                         const int j0 = t * p.BN;
-                        if (p.guard) fold32<true, FINAL>(v0, cn_s, sc_s, m2[h], j0, cv[h], cj[h], c2[h]);
-                        else fold32<false, FINAL>(v0, cn_s, sc_s, m2[h], j0, cv[h], cj[h], c2[h]);
+                        if (p.guard) fold32<true, FINAL>(v0, cn_s, sc_s, m2[h], j0, cv[h], cs[h], c2[h]);
+                        else fold32<false, FINAL>(v0, cn_s, sc_s, m2[h], j0, cv[h], cs[h], c2[h]);
                     } else {   // BN == 16
                         uint32_t v[32];
                         tmem_ld16(col0, v);
@@ -258,18 +256,9 @@ assign_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                         for (int e = 0; e < 16; ++e) {
                             const float s = p.guard ? m2[h] * sc_s[j0 + e] : -2.0f;
                             const float x = fmaf(__uint_as_float(v[e]), s, cn_s[j0 + e]);
-                            const int c = e & 7;
-                            const int grp = (j0 + e) >> 3;   // chain c = (j0 + e) & 7
-                            if (FINAL) {
-                                const bool pr = x < cv[h][c];
-                                const float t2 = fminf(c2[h][c], x);
-                                c2[h][c] = pr ? cv[h][c] : t2;
-                                cv[h][c] = pr ? x : cv[h][c];
-                                cj[h][c] = pr ? grp : cj[h][c];
-                            } else if (x < cv[h][c]) {
-                                cv[h][c] = x;
-                                cj[h][c] = grp;
-                            }
+                            const int c = e & 7;                 // chain c = (j0 + e) & 7
+                            if (FINAL) chain_step2(x, cv[h][c], c2[h][c], cs[h][c]);
+                            else chain_step(x, cv[h][c], cs[h][c]);
                         }
                     }
                     tc_fence_before();
@@ -279,10 +268,14 @@ assign_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
             }
 #pragma unroll
             for (int h = 0; h < RH; ++h) {
+                // every thread visits all groups of all tiles in order: ordinal = group
+                int jj[NCH];
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) jj[c] = 8 * chain_ordinal(cs[h][c], p.NT * (p.BN >> 3)) + c;
                 int w = 0;
                 float b1;
                 int j1;
-                merge_chains(cv[h], cj[h], b1, j1, &w);
+                merge_chains(cv[h], jj, b1, j1, &w);
                 const int64_t row = g * rows_per_group + (2 * h + wg) * BM + q;
                 if (row >= p.n) continue;
                 if (!FINAL) {

@@ -9,16 +9,25 @@
 //     shared memory for the whole kernel, so C~ (up to 256 KB) crosses L2 -> SM once per CTA and
 //     only X~ streams (TMA, ring of SA slots per CTA, both CTAs' bytes complete on the leader's
 //     barrier);
-//   * the leader CTA's single MMA thread issues, tcgen05.commit multicasts "accumulator full" /
-//     "slot free" to both CTAs; each CTA's two epilogue warpgroups split the NB columns of an
-//     accumulator, merge per row-block through shared memory, and arrive remotely on the leader's
-//     "accumulator empty" barrier.
+//   * the leader CTA's MMA warp (one elected lane issues) fills up to nacc TMEM accumulators
+//     ahead of the epilogue; tcgen05.commit multicasts "accumulator full" / "slot free" to both
+//     CTAs;
+//   * two epilogue warpgroups (2 warps per SM sub-partition) split the NB columns of every
+//     accumulator and fold them into per-point argmin chains (chain_step, 2 alu-pipe ops per
+//     distance); per tile they meet at a named barrier and one thread arrives remotely on the
+//     leader's "accumulator empty" barrier;
+//   * the row-block end is OFF the epilogue's critical path: each warpgroup only merges its
+//     chains and hands a (value, column) partial per point to warp 3 through double-buffered
+//     shared memory; warp 3 merges the two partials and does the label store, the changed
+//     count and the SSE (or, in FINAL mode, the certification).
+// DESIGN.md "pair kernel" has the measured per-tile budget this layout comes from.
 // FINAL mode: certified top-2 filter for Alg 3 step 7, as in k_assign_tc.cu.
 #include "common.cuh"
 #include "internal.h"
 #include "tc_common.cuh"
 #include "tc_pair.h"
 
+#include <stdio.h>
 #include <stdlib.h>
 
 namespace mpk {
@@ -26,11 +35,16 @@ namespace tcdev {
 
 constexpr int P_BM = 128;
 constexpr int P_NON_EPI = 4;
-constexpr int P_EWG = 4;                 // epilogue warpgroups
+constexpr int P_EWG = 2;                 // epilogue warpgroups (split the columns)
 constexpr int P_EPI = 4 * P_EWG;
 constexpr int P_THREADS = (P_NON_EPI + P_EPI) * 32;
 constexpr int P_MAX_ACC = 4;
 constexpr size_t P_BUDGET = 227 * 1024;
+constexpr uint32_t TRACE_T = 256;        // tiles traced under MPK_PAIR_TRACE
+// named barriers (0 is __syncthreads)
+constexpr int BAR_TILE = 1;              // the epilogue warps, once per tile
+constexpr int BAR_PART = 2;              // + parity: partials written (epilogue -> warp 3)
+constexpr int BAR_FREE = 4;              // + parity: partials consumed (warp 3 -> epilogue)
 
 MPK_DEV void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -49,16 +63,17 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
     uint8_t* a_base = b_base + (size_t)p.NT * p.b_half_bytes;           // X~ ring
     float* cn_s = (float*)(a_base + (size_t)p.SA * p.a_tile_bytes);
     float* sc_s = cn_s + p.k_pad;
-    float* mg_v = sc_s + p.k_pad;              // [2][P_EWG-1][128] partial minima
-    float* mg_v2 = mg_v + 2 * (P_EWG - 1) * P_BM;   // second minima (FINAL)
-    int* mg_j = (int*)(mg_v2 + 2 * (P_EWG - 1) * P_BM);
-    uint64_t* bars = (uint64_t*)(((uintptr_t)(mg_j + 2 * (P_EWG - 1) * P_BM) + 7) & ~(uintptr_t)7);
+    uint64_t* bars = (uint64_t*)(((uintptr_t)(sc_s + p.k_pad) + 7) & ~(uintptr_t)7);
     uint64_t* a_full = bars;
     uint64_t* a_empty = a_full + p.SA;
     uint64_t* b_full = a_empty + p.SA;
     uint64_t* t_full = b_full + 1;
     uint64_t* t_empty = t_full + P_MAX_ACC;
     uint32_t* tmem_slot = (uint32_t*)(t_empty + P_MAX_ACC);
+    // per-point partials of the two warpgroups, [parity][wg][128]
+    __shared__ float part_v[2 * P_EWG * P_BM];
+    __shared__ float part_v2[2 * P_EWG * P_BM];        // second minima (FINAL)
+    __shared__ int part_j[2 * P_EWG * P_BM];
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -74,7 +89,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
         mbar_init(smem_u32(b_full), 1);
         for (int i = 0; i < p.nacc; ++i) {
             mbar_init(smem_u32(&t_full[i]), 1);
-            mbar_init(smem_u32(&t_empty[i]), 2 * P_EPI);   // every epilogue warp of both CTAs
+            mbar_init(smem_u32(&t_empty[i]), 2);           // one arrival per CTA
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x)) : "memory");
@@ -96,12 +111,14 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
     const int64_t num_rb = (p.n + rows_per_rb - 1) / rows_per_rb;
     const int64_t pair = blockIdx.x >> 1;
     const int64_t npairs = gridDim.x >> 1;
+    const int64_t my_rbs = pair < num_rb ? (num_rb - 1 - pair) / npairs + 1 : 0;
     const int eps = p.SWZ / (p.is_f8 ? 1 : 2);      // elements per swizzle row
     const int half = p.NB / 2;
+    const int dbg = p.dbg;
 
     if (warp == 2) {
         // ------------------------------------------------ resident centroid halves (once)
-        if (lane == 0) {
+        if (elect_one()) {
             const uint32_t fb = smem_u32(b_full);
             if (leader) mbar_expect_tx(fb, 2u * p.NT * p.b_half_bytes);
             for (int t = 0; t < p.NT; ++t) {
@@ -111,64 +128,84 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                                      t * p.NB + (int)rank * half, fb);
             }
         }
+        __syncwarp();
     } else if (warp == 0) {
-        // ------------------------------------------------ X~ producer (this CTA's 128 rows)
-        if (lane == 0) {
-            uint32_t u = 0;
-            for (int64_t rb = pair; rb < num_rb; rb += npairs, ++u) {
-                const int slot = u % p.SA;
-                mbar_wait(smem_u32(&a_empty[slot]), ((u / p.SA) & 1) ^ 1);
+        // ------------------------------------------------ X~ producer (this CTA's 128 rows);
+        // the whole warp waits, one elected lane issues
+        const int SA = p.SA, KB = p.KB;
+        const uint32_t a_tile = p.a_tile_bytes, kb_a = p.kb_a_bytes;
+        const uint32_t a0 = smem_u32(a_base);
+        int slot = 0;
+        uint32_t ph = 0;
+        for (int64_t rb = pair; rb < num_rb; rb += npairs) {
+            mbar_wait(smem_u32(&a_empty[slot]), ph ^ 1);
+            if (elect_one()) {
                 const uint32_t fb = smem_u32(&a_full[slot]);
-                if (leader) mbar_expect_tx(fb, 2u * p.a_tile_bytes);
-                const uint32_t dst = smem_u32(a_base + (size_t)slot * p.a_tile_bytes);
+                if (leader) mbar_expect_tx(fb, 2u * a_tile);
+                const uint32_t dst = a0 + slot * a_tile;
                 const int row0 = (int)(rb * rows_per_rb + rank * P_BM);
-                for (int kb = 0; kb < p.KB; ++kb)
-                    tma_load_2d_pair(dst + kb * p.kb_a_bytes, &tmap_x, kb * eps, row0, fb);
+                for (int kb = 0; kb < KB; ++kb)
+                    tma_load_2d_pair(dst + kb * kb_a, &tmap_x, kb * eps, row0, fb);
             }
+            __syncwarp();
+            if (++slot == SA) { slot = 0; ph ^= 1; }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------ MMA issuer (leader CTA only)
-        if (leader && lane == 0) {
+        // ------------------------------------------------ MMA issuer (leader CTA only): the
+        // whole warp runs the loop (descriptor words stay warp-uniform), one lane issues
+        if (leader) {
+            const int SA = p.SA, KB = p.KB, NT = p.NT, nacc = p.nacc;
+            const int ksteps = p.SWZ / 32;
+            const uint32_t idesc = p.idesc, NB = (uint32_t)p.NB;
+            const bool f8 = p.is_f8 != 0;
+            unsigned long long* trace = p.trace;
+            const bool trace_me = trace != nullptr && blockIdx.x == 0;
+            const uint32_t dhi = umma_desc_hi(p.SWZ);
+            const uint32_t b_lo0 = umma_desc_lo(smem_u32(b_base));
+            const uint32_t a_lo0 = umma_desc_lo(smem_u32(a_base));
+            const uint32_t a_tile16 = p.a_tile_bytes >> 4, b_half16 = p.b_half_bytes >> 4;
+            const uint32_t kb_a16 = p.kb_a_bytes >> 4, kb_b16 = p.kb_b_bytes >> 4;
             mbar_wait(smem_u32(b_full), 0);
             tc_fence_after();
-            const int ksteps = p.SWZ / 32;
-            const uint32_t b0 = smem_u32(b_base);
-            uint32_t u = 0, ai = 0;
-            for (int64_t rb = pair; rb < num_rb; rb += npairs, ++u) {
-                const int slot = u % p.SA;
-                mbar_wait(smem_u32(&a_full[slot]), (u / p.SA) & 1);
+            int slot = 0, buf = 0;
+            uint32_t aph = 0, tph = 0, ai = 0;
+            for (int64_t rb = pair; rb < num_rb; rb += npairs) {
+                mbar_wait(smem_u32(&a_full[slot]), aph);
                 tc_fence_after();
-                const uint32_t a_addr = smem_u32(a_base + (size_t)slot * p.a_tile_bytes);
-                for (int t = 0; t < p.NT; ++t, ++ai) {
-                    const int buf = ai % p.nacc;
-                    mbar_wait(smem_u32(&t_empty[buf]), ((ai / p.nacc) & 1) ^ 1);
+                const uint32_t a_lo = a_lo0 + slot * a_tile16;
+                for (int t = 0; t < NT; ++t, ++ai) {
+                    mbar_wait(smem_u32(&t_empty[buf]), tph ^ 1);
                     tc_fence_after();
-                    const uint32_t d_tmem = tmem_base + buf * p.NB;
-                    const uint32_t b_addr = b0 + t * p.b_half_bytes;
-                    for (int kb = 0; kb < p.KB; ++kb) {
-                        for (int ks = 0; ks < ksteps; ++ks) {
-                            const uint64_t ad = umma_desc(a_addr + kb * p.kb_a_bytes + ks * 32, p.SWZ);
-                            const uint64_t bd = umma_desc(b_addr + kb * p.kb_b_bytes + ks * 32, p.SWZ);
-                            const uint32_t accum = (kb | ks) ? 1u : 0u;
-                            if (p.dbg & 2) continue;
-                            if (p.is_f8) mma2_f8(d_tmem, ad, bd, p.idesc, accum);
-                            else mma2_f16(d_tmem, ad, bd, p.idesc, accum);
+                    if (elect_one()) {
+                        const bool tr = trace_me && ai < TRACE_T;
+                        if (tr) trace[ai * 8 + 0] = clock64();
+                        const uint32_t d_tmem = tmem_base + (uint32_t)buf * NB;
+                        const uint32_t b_lo = b_lo0 + t * b_half16;
+                        if (!(dbg & 2)) {
+                            for (int kb = 0; kb < KB; ++kb) {
+                                for (int ks = 0; ks < ksteps; ++ks) {
+                                    const uint64_t ad = desc_join(dhi, a_lo + kb * kb_a16 + ks * 2);
+                                    const uint64_t bd = desc_join(dhi, b_lo + kb * kb_b16 + ks * 2);
+                                    const uint32_t accum = (kb | ks) ? 1u : 0u;
+                                    if (f8) mma2_f8(d_tmem, ad, bd, idesc, accum);
+                                    else mma2_f16(d_tmem, ad, bd, idesc, accum);
+                                }
+                            }
                         }
+                        tc_commit_pair(smem_u32(&t_full[buf]));
+                        // X~ slot free for the producer once this row-block's last MMAs finish
+                        if (t == NT - 1) tc_commit_pair(smem_u32(&a_empty[slot]));
+                        if (tr) trace[ai * 8 + 1] = clock64();
                     }
-                    tc_commit_pair(smem_u32(&t_full[buf]));
+                    __syncwarp();
+                    if (++buf == nacc) { buf = 0; tph ^= 1; }
                 }
-                tc_commit_pair(smem_u32(&a_empty[slot]));
+                if (++slot == SA) { slot = 0; aph ^= 1; }
             }
         }
-    } else if (warp >= P_NON_EPI) {
-        // ------------------------------------------------ epilogue: P_EWG warpgroups split the
-        // NB columns of every accumulator (4 warps per SM sub-partition hide TMEM/smem latency)
-        const int wg = (warp - P_NON_EPI) >> 2;
-        const int quarter = warp & 3;
-        const int q = quarter * 32 + lane;                 // row within this CTA's 128
-        const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
-        const int wcols = p.NB / P_EWG;                    // multiple of 16
-        const int col_off = wg * wcols;
+    } else if (warp == 3) {
+        // ------------------------------------------------ row-block end (both CTAs): merge the
+        // two warpgroups' partials; labels, changed count and SSE (FINAL: certification)
         float cn_max = 0.0f, s_max = 1.0f;
         if (FINAL) {
             for (int j = 0; j < p.k; ++j) {
@@ -176,92 +213,31 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 s_max = fmaxf(s_max, sc_s[j]);
             }
         }
+        const int64_t n = p.n;
+        const bool guard = p.guard != 0;
         double my_sse = 0.0, my_changed = 0.0;
-        uint32_t ai = 0, rbi = 0;
+        int64_t rbi = 0;
         for (int64_t rb = pair; rb < num_rb; rb += npairs, ++rbi) {
-            const int64_t row = rb * rows_per_rb + rank * P_BM + q;
-            const bool valid = row < p.n;
-            const float m2 = (p.guard && valid) ? -2.0f * p.sx[row] : -2.0f;
-            // prefetch what the row-block epilogue needs (hidden behind the tile loop)
-            int old_label = 0;
-            float xn_row = 0.0f;
-            if (wg == 0 && valid) {
-                xn_row = p.xn[row];
-                if (!FINAL) old_label = p.labels[row];
-            }
-            float cv[NCH], c2[NCH];
-            int cj[NCH];
+            const int par = (int)(rbi & 1);
+            // this row-block's point data (issued before waiting for the partials)
+            float xn_r[4];
+            int old_r[4];
 #pragma unroll
-            for (int c = 0; c < NCH; ++c) { cv[c] = INFINITY; c2[c] = INFINITY; cj[c] = 0; }
-            for (int t = 0; t < p.NT; ++t, ++ai) {
-                const int buf = ai % p.nacc;
-                mbar_wait(smem_u32(&t_full[buf]), (ai / p.nacc) & 1);
-                tc_fence_after();
-                const uint32_t col0 = tmem_base + lane_addr + buf * p.NB + col_off;
-                const int jbase = t * p.NB + col_off;
-                if (!(p.dbg & 1)) {
-                    if ((wcols & 31) == 0) {
-                        for (int c = 0; c < wcols; c += 32) {
-                            uint32_t va[32];
-                            tmem_ld32(col0 + c, va);
-                            tmem_wait_ld();
-                            if (p.guard) fold32<true, FINAL>(va, cn_s, sc_s, m2, jbase + c, cv, cj, c2);
-                            else fold32<false, FINAL>(va, cn_s, sc_s, m2, jbase + c, cv, cj, c2);
-                        }
-                    } else {   // wcols == 16
-                        uint32_t va[32];
-                        tmem_ld16(col0, va);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int e = 0; e < 16; ++e) {
-                            const int j = jbase + e;
-                            const float s = p.guard ? m2 * sc_s[j] : -2.0f;
-                            const float x = fmaf(__uint_as_float(va[e]), s, cn_s[j]);
-                            const int c = e & 7, grp = j >> 3;
-                            if (FINAL) {
-                                const bool pr = x < cv[c];
-                                const float t2 = fminf(c2[c], x);
-                                c2[c] = pr ? cv[c] : t2;
-                                cv[c] = pr ? x : cv[c];
-                                cj[c] = pr ? grp : cj[c];
-                            } else if (x < cv[c]) {
-                                cv[c] = x;
-                                cj[c] = grp;
-                            }
-                        }
-                    }
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&t_empty[buf]), 0));
+            for (int u = 0; u < 4; ++u) {
+                const int64_t row = rb * rows_per_rb + rank * P_BM + u * 32 + lane;
+                xn_r[u] = row < n ? p.xn[row] : 0.0f;
+                old_r[u] = (!FINAL && row < n) ? p.labels[row] : 0;
             }
-            // merge the 8 chains: lowest value, then lowest index (sequential-scan semantics)
-            int w = 0;
-            float b1;
-            int j1;
-            merge_chains(cv, cj, b1, j1, &w);
-            float b2 = INFINITY;
-            if (FINAL) {
+            named_bar_sync(BAR_PART + par, P_EPI * 32 + 32);
 #pragma unroll
-                for (int c = 0; c < NCH; ++c) b2 = fminf(b2, c == w ? c2[c] : cv[c]);
-            }
-            // warpgroups 1..P_EWG-1 hand their partial to warpgroup 0 through smem
-            const int ms = rbi & 1;
-            if (wg != 0) {
-                const int slot = (ms * (P_EWG - 1) + (wg - 1)) * P_BM + q;
-                mg_v[slot] = b1;
-                mg_j[slot] = j1;
-                if (FINAL) mg_v2[slot] = b2;
-                named_bar_arrive(1, P_EPI * 32);
-                continue;
-            }
-            named_bar_sync(1, P_EPI * 32);
-#pragma unroll
-            for (int o = 0; o < P_EWG - 1; ++o) {
-                const int slot = (ms * (P_EWG - 1) + o) * P_BM + q;
-                const float ob1 = mg_v[slot];
-                const int oj1 = mg_j[slot];
-                const float ob2 = FINAL ? mg_v2[slot] : INFINITY;
+            for (int u = 0; u < 4; ++u) {
+                const int q = u * 32 + lane;
+                const int s0 = (par * P_EWG + 0) * P_BM + q, s1 = (par * P_EWG + 1) * P_BM + q;
+                float b1 = part_v[s0], b2 = FINAL ? part_v2[s0] : INFINITY;
+                int j1 = part_j[s0];
+                const float ob1 = part_v[s1];
+                const int oj1 = part_j[s1];
+                const float ob2 = FINAL ? part_v2[s1] : INFINITY;
                 if (ob1 < b1 || (ob1 == b1 && oj1 < j1)) {
                     b2 = fminf(ob2, b1);
                     b1 = ob1;
@@ -269,44 +245,143 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 } else {
                     b2 = fminf(b2, ob1);
                 }
-            }
-            if (!valid) continue;
-            if (!FINAL) {
-                if (old_label != j1) my_changed += 1.0;
+                const int64_t row = rb * rows_per_rb + rank * P_BM + q;
+                if (row >= n) continue;
                 p.labels[row] = j1;
-                const float md = xn_row + b1;
-                my_sse += md > 0.0f ? (double)md : 0.0;
-            } else {
-                p.labels[row] = j1;
-                const double xn = (double)xn_row;
-                const double si = p.guard ? (double)p.sx[row] : 1.0;
-                const double cmax = (double)cn_max, smax = (double)s_max;
-                const double S = sqrt(fmax(xn, 0.0) * fmax(cmax, 0.0)) * (1.0 + 1e-6);
-                const double u32 = 5.9604644775390625e-08;
-                const double ul = p.u_low;
-                const double gacc = (double)(p.d_pad + 2) * 2.384185791015625e-07;
-                const double gd = (double)p.d * u32 / (1.0 - (double)p.d * u32);
-                const double E = 2.0 * (2.0 * ul + ul * ul + gacc + 2.0 * u32) * S +
-                                 2.0 * p.eta_low * sqrt((double)p.d) *
-                                     (si * sqrt(fmax(cmax, 0.0)) + smax * sqrt(fmax(xn, 0.0))) +
-                                 u32 * (cmax + 2.0 * S);
-                const double B32 = gd * 2.0 * S + u32 * (cmax + 2.0 * S);
-                const double thr = 2.0 * (E + B32) * 1.001;
-                const bool ok = isfinite(b1) && isfinite(xn) && isfinite(cmax) &&
-                                ((double)b2 - (double)b1 > thr);
-                if (!ok) {
-                    const int slot = atomicAdd(p.fb_count, 1);
-                    p.fb_rows[slot] = (int)row;
+                if (!FINAL) {
+                    if (old_r[u] != j1) my_changed += 1.0;
+                    const float md = xn_r[u] + b1;
+                    my_sse += md > 0.0f ? (double)md : 0.0;
+                } else {
+                    // certification: |v^ - v| <= E, |fl32(v) - v| <= B32
+                    const double xn = (double)xn_r[u];
+                    const double si = guard ? (double)p.sx[row] : 1.0;
+                    const double cmax = (double)cn_max, smax = (double)s_max;
+                    const double S = sqrt(fmax(xn, 0.0) * fmax(cmax, 0.0)) * (1.0 + 1e-6);
+                    const double u32 = 5.9604644775390625e-08;
+                    const double ul = p.u_low;
+                    const double gacc = (double)(p.d_pad + 2) * 2.384185791015625e-07;
+                    const double gd = (double)p.d * u32 / (1.0 - (double)p.d * u32);
+                    const double E = 2.0 * (2.0 * ul + ul * ul + gacc + 2.0 * u32) * S +
+                                     2.0 * p.eta_low * sqrt((double)p.d) *
+                                         (si * sqrt(fmax(cmax, 0.0)) + smax * sqrt(fmax(xn, 0.0))) +
+                                     u32 * (cmax + 2.0 * S);
+                    const double B32 = gd * 2.0 * S + u32 * (cmax + 2.0 * S);
+                    const double thr = 2.0 * (E + B32) * 1.001;
+                    const bool ok = isfinite(b1) && isfinite(xn) && isfinite(cmax) &&
+                                    ((double)b2 - (double)b1 > thr);
+                    if (!ok) {
+                        const int slot = atomicAdd(p.fb_count, 1);
+                        p.fb_rows[slot] = (int)row;
+                    }
                 }
             }
+            // hand the parity's partial buffer back (only if the epilogue will write it again)
+            if (rbi + 2 < my_rbs) named_bar_arrive(BAR_FREE + par, P_EPI * 32 + 32);
         }
-        if (!FINAL && wg == 0) {
+        if (!FINAL) {
             my_sse = warp_sum(my_sse);
             my_changed = warp_sum(my_changed);
             if (lane == 0) {
                 if (p.acc_sse) atomicAdd(p.acc_sse, my_sse);
                 if (p.acc_changed && my_changed != 0.0) atomicAdd(p.acc_changed, my_changed);
             }
+        }
+    } else {
+        // ------------------------------------------------ epilogue: P_EWG warpgroups split the
+        // NB columns of every accumulator (2 warps per SM sub-partition)
+        const int wg = (warp - P_NON_EPI) >> 2;
+        const int quarter = warp & 3;
+        const int q = quarter * 32 + lane;                 // row within this CTA's 128
+        const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
+        const int NT = p.NT, NB = p.NB, nacc = p.nacc;
+        const int wcols = NB / P_EWG;                      // multiple of 16
+        const int col_off = wg * wcols;
+        const int gpt = wcols >> 3;                        // groups of 8 columns per tile
+        // ordinal -> tile: gpt is a power of two whenever NT > 1 (NB = 256 then, or a
+        // power-of-two MPK_PAIR_NB); with NT == 1 the tile is 0
+        const int gsh = (NT > 1) ? __ffs(gpt) - 1 : 30;
+        const int64_t n = p.n;
+        const bool guard = p.guard != 0;
+        unsigned long long* trace = p.trace;
+        const bool trace_me = trace != nullptr && blockIdx.x == 0 && warp == P_NON_EPI && lane == 0;
+        int buf = 0;
+        uint32_t tph = 0, ai = 0;
+        int64_t rbi = 0;
+        for (int64_t rb = pair; rb < num_rb; rb += npairs, ++rbi) {
+            const int64_t row = rb * rows_per_rb + rank * P_BM + q;
+            const float m2 = (guard && row < n) ? -2.0f * p.sx[row] : -2.0f;
+            if (trace_me && ai < TRACE_T) trace[ai * 8 + 5] = clock64();   // row-block top
+            float cv[NCH], c2[NCH], cs[NCH];
+            chains_init(cv, cs, c2);
+            for (int t = 0; t < NT; ++t, ++ai) {
+                mbar_wait(smem_u32(&t_full[buf]), tph);
+                tc_fence_after();
+                const bool tr = trace_me && ai < TRACE_T;
+                if (tr) trace[ai * 8 + 2] = clock64();
+                const uint32_t col0 = tmem_base + lane_addr + (uint32_t)buf * NB + col_off;
+                const int jbase = t * NB + col_off;
+                if (!(dbg & 1)) {
+                    int c = 0;
+                    for (; c + 32 <= wcols; c += 32) {
+                        uint32_t va[32];
+                        tmem_ld32(col0 + c, va);
+                        tmem_wait_ld_dep(va);
+                        if (guard) fold32<true, FINAL>(va, cn_s, sc_s, m2, jbase + c, cv, cs, c2);
+                        else fold32<false, FINAL>(va, cn_s, sc_s, m2, jbase + c, cv, cs, c2);
+                    }
+                    if (c < wcols) {   // a 16-column remainder (wcols is a multiple of 16)
+                        uint32_t va[32];
+                        tmem_ld16(col0 + c, va);
+                        tmem_wait_ld_dep(va);
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) {
+                            const int j = jbase + c + e;
+                            const float s = guard ? m2 * sc_s[j] : -2.0f;
+                            const float x = fmaf(__uint_as_float(va[e]), s, cn_s[j]);
+                            const int ch = e & 7;
+                            if (FINAL) chain_step2(x, cv[ch], c2[ch], cs[ch]);
+                            else chain_step(x, cv[ch], cs[ch]);
+                        }
+                    }
+                }
+                if (tr) trace[ai * 8 + 3] = clock64();
+                // one arrival per CTA: the epilogue warps meet at a named barrier, then a single
+                // thread signals the leader's "accumulator empty"
+                tc_fence_before();
+                named_bar_sync(BAR_TILE, P_EPI * 32);
+                if (warp == P_NON_EPI && lane == 0)
+                    mbar_arrive_cluster(mapa(smem_u32(&t_empty[buf]), 0));
+                if (tr) trace[ai * 8 + 4] = clock64();
+                if (++buf == nacc) { buf = 0; tph ^= 1; }
+            }
+            // chains -> columns: ordinal v = t * gpt + g' (tile t, g'-th group of this
+            // warpgroup's columns in it); merge: lowest value, then lowest column
+            int jj[NCH];
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+                const int v = chain_ordinal(cs[c], NT * gpt);
+                const int t = v >> gsh;
+                jj[c] = 8 * (t * (NB >> 3) + (col_off >> 3) + (v - t * gpt)) + c;
+            }
+            int w = 0;
+            float b1;
+            int j1;
+            merge_chains(cv, jj, b1, j1, &w);
+            float b2 = INFINITY;
+            if (FINAL) {
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) b2 = fminf(b2, c == w ? c2[c] : cv[c]);
+            }
+            // hand the partial to warp 3 (double-buffered by row-block parity)
+            const int par = (int)(rbi & 1);
+            if (rbi >= 2) named_bar_sync(BAR_FREE + par, P_EPI * 32 + 32);
+            const int slot = (par * P_EWG + wg) * P_BM + q;
+            part_v[slot] = b1;
+            part_j[slot] = j1;
+            if (FINAL) part_v2[slot] = b2;
+            named_bar_arrive(BAR_PART + par, P_EPI * 32 + 32);
+            if (trace_me && ai - 1 < TRACE_T) trace[(ai - 1) * 8 + 6] = clock64();
         }
     }
     tc_fence_before();
@@ -334,7 +409,9 @@ bool pair_plan(int dist, int d, int d_pad, int k, PairParams* pp, size_t* smem_b
     const int k_pad = NT * NB;
     const size_t b_half = (size_t)(NB / 2) * RB;
     const size_t a_tile = (size_t)P_BM * RB;
-    const size_t fixed = 1024 + (size_t)k_pad * 8 + 3 * 2 * (P_EWG - 1) * P_BM * 4 + 8 +
+    // static shared (the warp-3 partial buffers) counts against the same 227 KB
+    const size_t stat = 3 * 2 * P_EWG * P_BM * 4;
+    const size_t fixed = 1024 + stat + (size_t)k_pad * 8 + 8 +
                          (size_t)(2 * 8 + 1 + 2 * P_MAX_ACC) * 8 + 16;
     const size_t bres = (size_t)NT * b_half;
     if (fixed + bres + 2 * a_tile > P_BUDGET) return false;
@@ -353,12 +430,13 @@ bool pair_plan(int dist, int d, int d_pad, int k, PairParams* pp, size_t* smem_b
     p.kb_b_bytes = (uint32_t)(NB / 2) * SWZ;
     p.is_f8 = dist == KMEANS_E5M2;
     if (const char* e = getenv("MPK_PAIR_DBG")) p.dbg = atoi(e);
+
     p.u_low = dist == KMEANS_FP16 ? 0x1p-11 : (dist == KMEANS_BF16 ? 0x1p-8 : 0x1p-3);
     p.eta_low = dist == KMEANS_FP16 ? 0x1p-25 : (dist == KMEANS_BF16 ? 0x1p-134 : 0x1p-17);
     const uint32_t fmt = dist == KMEANS_BF16 ? 1u : (dist == KMEANS_E5M2 ? 1u : 0u);
     p.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(NB >> 3) << 17) |
               ((uint32_t)(256 >> 4) << 24);
-    *smem_bytes = fixed + bres + (size_t)SA * a_tile;
+    *smem_bytes = fixed - stat + bres + (size_t)SA * a_tile;
     return true;
 }
 
@@ -379,6 +457,27 @@ cudaError_t pair_launch(const CUtensorMap& tmap_x, const CUtensorMap& tmap_c, co
     grid &= ~int64_t(1);
     if (grid < 2) grid = 2;
     launches_add(1);
+    if (const char* tf = getenv("MPK_PAIR_TRACE"); tf && !final_mode) {
+        // debug: one traced launch, stamps dumped as text (tile, 5 clock64 values)
+        PairParams q = p;
+        static unsigned long long* buf = nullptr;
+        const size_t bytes = TRACE_T * 8 * sizeof(unsigned long long);
+        if (!buf) cudaMalloc(&buf, bytes);
+        cudaMemsetAsync(buf, 0, bytes, s);
+        q.trace = buf;
+        assign_pair_kernel<false><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, q);
+        cudaStreamSynchronize(s);
+        static unsigned long long h[TRACE_T * 8];
+        cudaMemcpy(h, buf, bytes, cudaMemcpyDeviceToHost);
+        if (FILE* f = fopen(tf, "w")) {
+            for (uint32_t t = 0; t < TRACE_T; ++t)
+                fprintf(f, "%u %llu %llu %llu %llu %llu %llu %llu %llu\n", t, h[t * 8], h[t * 8 + 1],
+                        h[t * 8 + 2], h[t * 8 + 3], h[t * 8 + 4], h[t * 8 + 5], h[t * 8 + 6],
+                        h[t * 8 + 7]);
+            fclose(f);
+        }
+        return cudaGetLastError();
+    }
     if (final_mode)
         assign_pair_kernel<true><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, p);
     else

@@ -233,8 +233,21 @@ int create_impl(int64_t n, int32_t d, int32_t k, int work, int dist, int flags,
     CA(dalloc(&h->sx, (size_t)n * W));
     CA(dalloc(&h->Cw, (size_t)k * d * W));
     CA(dalloc(&h->Cl, (size_t)k * std::max(h->d_pad, d) * std::max(h->lsize, h->wsize)));
-    CA(dalloc(&h->cn, (size_t)k * W));
-    CA(dalloc(&h->sc, (size_t)k * W));
+    {
+        // ||c||^2 and the guard scales are padded to a multiple of 256 columns: the pair kernel
+        // reads them from global memory (L1-resident) for whole centroid tiles, and a padded
+        // centroid (TMA zero-fills its row) must never win: cn = +inf, sc = 0 there. Prep only
+        // ever writes j < k, so the tail is set once here.
+        const size_t kp = ((size_t)k + 255) / 256 * 256;
+        CA(dalloc(&h->cn, kp * W));
+        CA(dalloc(&h->sc, kp * W));
+        CA(cudaMemset(h->sc, 0, kp * W));
+        if (W == sizeof(float) && kp > (size_t)k) {
+            std::vector<float> inf(kp - k, INFINITY);
+            CA(cudaMemcpy((float*)h->cn + k, inf.data(), inf.size() * sizeof(float),
+                          cudaMemcpyHostToDevice));
+        }
+    }
     CA(dalloc(&h->labels, (size_t)n * sizeof(int32_t)));
     CA(dalloc(&h->acc, (size_t)h->L.total() * sizeof(double)));
     CA(dalloc(&h->cnt, (size_t)k * sizeof(int)));
@@ -395,7 +408,10 @@ int final_assign(kmeans_ctx* h, const Problem& pf) {
                 cudaError_t e1 = cudaMalloc(&h->fin_Xl, (size_t)n * h->fin_dpad * 2);
                 cudaError_t e2 = cudaMalloc(&h->fin_Cl, (size_t)k * h->fin_dpad * 2);
                 cudaError_t e3 = cudaMalloc(&h->fin_sx, (size_t)n * 4);
-                cudaError_t e4 = cudaMalloc(&h->fin_sc, (size_t)k * 4);
+                // padded like h->sc (see create_impl)
+                const size_t kp = ((size_t)k + 255) / 256 * 256;
+                cudaError_t e4 = cudaMalloc(&h->fin_sc, kp * 4);
+                if (e4 == cudaSuccess) e4 = cudaMemset(h->fin_sc, 0, kp * 4);
                 std::string err;
                 if (e1 == cudaSuccess && e2 == cudaSuccess && e3 == cudaSuccess &&
                     e4 == cudaSuccess && tc_supported(KMEANS_FP16, h->fin_dpad, k))

@@ -24,13 +24,16 @@ MPK_DEV void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 MPK_DEV void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// try_wait with a suspend-time hint: the waiting warp is parked until the phase flips (or the
+// hint expires) instead of re-polling; bare try_wait loops of the idle role warps measurably
+// slowed the epilogue's memory instructions on the same SM.
 MPK_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
         "@!P1 bra WAIT_%=;\n\t}" ::"r"(bar),
-        "r"(parity)
+        "r"(parity), "r"(0x989680)
         : "memory");
 }
 MPK_DEV void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
@@ -97,6 +100,20 @@ MPK_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[32]) {
         : "r"(taddr));
 }
 MPK_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// wait::ld that also "defines" r, so the compiler cannot schedule reads of a prefetched
+// tcgen05.ld destination above the wait (needed when loads are double-buffered)
+MPK_DEV void tmem_wait_ld_dep(uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.wait::ld.sync.aligned;"
+        : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+          "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]),
+          "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]),
+          "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]),
+          "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]),
+          "+r"(r[31])
+        :
+        : "memory");
+}
 
 
 MPK_DEV float4 lds_f4(uint32_t addr) {
@@ -112,53 +129,129 @@ MPK_DEV float4 lds_f4(uint32_t addr) {
 // Chain c takes the columns j = 8g + c; it records the GROUP g of its minimum (one add per 8
 // columns instead of per column); the column is recovered as 8 g + c when chains merge.
 // TOP2 also tracks the second-smallest value of each chain.
-template <bool GUARD, bool TOP2>
+// Argmin chains. Chain c of a point takes the columns j = 8 g + c; its state is
+//   v : the running minimum of its values,
+//   s : the position of its last STRICT improvement, as an offset (-1, -2, ...) from the next
+//       group the chain will visit (a float; exact, |s| << 2^24),
+// so that one column costs two alu-pipe ops and one fma-pipe op:
+//   nf = !(x < v) ? 1 : 0   (set.geu: alu; NaN -> 1, no improvement)
+//   v  = min(v, x)          (FMNMX: alu; keeps v for NaN x, equal values stay equal)
+//   s  = s * nf - 1         (FFMA: fma pipe; 0 * s - 1 = -1 after an improvement)
+// instead of FSETP + FSEL + SEL (three alu ops at rt 2, which bounded the fold at 6 cycles per
+// warp-column). Ties keep the earlier group, the sequential scan's rule; merge_chains() then
+// breaks ties across chains by the smaller column.
+MPK_DEV void chain_step(float x, float& v, float& s) {
+    float nf;
+    asm("set.geu.f32.f32 %0, %1, %2;" : "=f"(nf) : "f"(x), "f"(v));
+    v = fminf(v, x);
+    s = fmaf(s, nf, -1.0f);
+}
+// Same with the chain's second minimum: new second = min(second, max(x, v)) (x < v: the old v,
+// which is <= second; otherwise min(second, x)).
+MPK_DEV void chain_step2(float x, float& v, float& v2, float& s) {
+    v2 = fminf(v2, fmaxf(x, v));
+    chain_step(x, v, s);
+}
+MPK_DEV void chains_init(float (&cv)[NCH], float (&cs)[NCH], float (&c2)[NCH]) {
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) { cv[c] = INFINITY; c2[c] = INFINITY; cs[c] = -1.0f; }
+}
+// Visited-group ordinal of chain c's last improvement after V groups (0 if it never improved,
+// i.e. all its values were +inf or NaN — the scan's default label).
+MPK_DEV int chain_ordinal(float s, int V) {
+    const int v = V + (int)s;
+    return v < 0 ? 0 : v;
+}
+
+// Warp-uniform 16-byte read of a small, hot, read-only global array (||c||^2, guard scales),
+// kept in L1 (evict_last): the pair kernel spends its shared memory on the resident centroids
+// and the X~ ring instead.
+MPK_DEV float4 ldg_f4_keep(const float* p) {
+    float4 r;
+    asm("ld.global.nc.L1::evict_last.v4.f32 {%0, %1, %2, %3}, [%4];"
+        : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+        : "l"(p));
+    return r;
+}
+MPK_DEV float ldg_keep(const float* p) {
+    float r;
+    asm("ld.global.nc.L1::evict_last.f32 %0, [%1];" : "=f"(r) : "l"(p));
+    return r;
+}
+
+// Fold 32 TMEM accumulator columns (j0 .. j0+31, four groups) of one point into its 8 chains.
+// GCN: cn / sc are global arrays (padded, see ldg_f4_keep) instead of shared memory.
+template <bool GUARD, bool TOP2, bool GCN = false>
 MPK_DEV void fold32(const uint32_t (&v)[32], const float* cn_s, const float* sc_s, float m2,
-                    int j0, float (&cv)[NCH], int (&cg)[NCH], float (&c2)[NCH]) {
-    const uint32_t cn_a = smem_u32(cn_s + j0);
-    const uint32_t sc_a = smem_u32(sc_s + j0);
-    const int g0 = j0 >> 3;
+                    int j0, float (&cv)[NCH], float (&cs)[NCH], float (&c2)[NCH]) {
+    const uint32_t cn_a = GCN ? 0u : smem_u32(cn_s + j0);
+    const uint32_t sc_a = GCN ? 0u : smem_u32(sc_s + j0);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-        const float4 cc = lds_f4(cn_a + 16 * e);
+        const float4 cc = GCN ? ldg_f4_keep(cn_s + j0 + 4 * e) : lds_f4(cn_a + 16 * e);
         float s[4] = {-2.0f, -2.0f, -2.0f, -2.0f};
         if (GUARD) {
-            const float4 ss = lds_f4(sc_a + 16 * e);
+            const float4 ss = GCN ? ldg_f4_keep(sc_s + j0 + 4 * e) : lds_f4(sc_a + 16 * e);
             s[0] = m2 * ss.x; s[1] = m2 * ss.y; s[2] = m2 * ss.z; s[3] = m2 * ss.w;
         }
         const float cnv[4] = {cc.x, cc.y, cc.z, cc.w};
-        const int g = g0 + (e >> 1);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const float x = fmaf(__uint_as_float(v[4 * e + u]), s[u], cnv[u]);
             const int c = (e & 1) * 4 + u;
-            if (TOP2) {
-                const bool p = x < cv[c];
-                const float t2 = fminf(c2[c], x);
-                c2[c] = p ? cv[c] : t2;
-                cv[c] = p ? x : cv[c];
-                cg[c] = p ? g : cg[c];
-            } else {
-                if (x < cv[c]) { cv[c] = x; cg[c] = g; }
-            }
+            if (TOP2) chain_step2(x, cv[c], c2[c], cs[c]);
+            else chain_step(x, cv[c], cs[c]);
         }
     }
 }
 
-// Merge the chains of one point: smallest value, then smallest column (the sequential scan's
-// result). Returns the winning chain in *w (for the TOP2 second minimum).
-MPK_DEV void merge_chains(const float (&cv)[NCH], const int (&cg)[NCH], float& b1, int& j1,
+// Merge the chains of one point given each chain's column jj[c]: smallest value, then smallest
+// column (the sequential scan's result). Returns the winning chain in *w (for TOP2).
+MPK_DEV void merge_chains(const float (&cv)[NCH], const int (&jj)[NCH], float& b1, int& j1,
                           int* w) {
     b1 = cv[0];
-    j1 = cg[0] * 8;
+    j1 = jj[0];
     int wc = 0;
 #pragma unroll
     for (int c = 1; c < NCH; ++c) {
-        const int j = cg[c] * 8 + c;
-        if (cv[c] < b1 || (cv[c] == b1 && j < j1)) { b1 = cv[c]; j1 = j; wc = c; }
+        if (cv[c] < b1 || (cv[c] == b1 && jj[c] < j1)) { b1 = cv[c]; j1 = jj[c]; wc = c; }
     }
     if (w) *w = wc;
 }
+
+// Opaque register copy of a kernel parameter: ptxas otherwise rematerialises parameters from
+// the constant bank inside hot loops (LDC/LDCU on every iteration), which measured as hundreds of
+// cycles per row-block in the pair kernel. The empty asm makes the value unknown, so it stays in
+// a register.
+MPK_DEV int pin(int v) { asm volatile("" : "+r"(v)); return v; }
+MPK_DEV uint32_t pin(uint32_t v) { asm volatile("" : "+r"(v)); return v; }
+MPK_DEV int64_t pin(int64_t v) { asm volatile("" : "+l"(v)); return v; }
+MPK_DEV float pin(float v) { asm volatile("" : "+f"(v)); return v; }
+template <typename T>
+MPK_DEV T* pin(T* v) {
+    asm volatile("" : "+l"(v));
+    return v;
+}
+
+// One lane of a converged warp (elect.sync). Role loops run on the whole warp so that their
+// barrier/descriptor arithmetic stays in uniform registers, and only the issue is elected:
+// branching on `lane == 0` first makes every tcgen05/TMA operand divergent and ptxas wraps each
+// issue in an R2UR.BROADCAST waterfall loop (~120 dependent cycles per MMA, measured).
+MPK_DEV bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+// Upper / lower words of umma_desc(): the K-advance inside a tile only touches the start
+// address (bits 0-13, in 16-byte units), so a loop adds (bytes >> 4) to a precomputed low word.
+MPK_DEV uint32_t umma_desc_lo(uint32_t saddr) { return ((saddr >> 4) & 0x3FFFu) | (1u << 16); }
+MPK_DEV uint32_t umma_desc_hi(int swz) {
+    const uint32_t layout = swz == 128 ? 2u : (swz == 64 ? 4u : 6u);
+    return ((8u * (uint32_t)swz) >> 4) | (1u << 14) | (layout << 29);
+}
+MPK_DEV uint64_t desc_join(uint32_t hi, uint32_t lo) { return ((uint64_t)hi << 32) | lo; }
 
 // ---------------------------------------------------------------- CTA-pair (cta_group::2) helpers
 MPK_DEV uint32_t cluster_ctarank() {

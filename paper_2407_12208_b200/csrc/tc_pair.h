@@ -26,6 +26,7 @@ struct PairParams {
     int* fb_rows;
     double u_low, eta_low;
     int dbg;                 // debug: bit0 skip epilogue folding, bit1 skip MMAs (timing only)
+    unsigned long long* trace;   // debug (MPK_PAIR_TRACE): per-tile clock64 stamps of CTA 0
 };
 
 // Fill the static part of PairParams and the dynamic smem size for (dist, d_pad, k); false if
