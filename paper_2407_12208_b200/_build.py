@@ -35,9 +35,11 @@ def _nccl_dir() -> str:
 
 def _flags() -> list[str]:
     nccl = _nccl_dir()
+    # MPK_NVCC_EXTRA: extra flags for experiments (e.g. -DMPK_PAIR_EWG=4); not used by build()
+    extra = os.environ.get("MPK_NVCC_EXTRA", "").split()
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                    "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills",
-                   "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include")]
+                   "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include")] + extra
 
 
 def _stale(srcs: list[str], target: str) -> bool:

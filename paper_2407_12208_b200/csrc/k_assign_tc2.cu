@@ -35,7 +35,13 @@ namespace tcdev {
 
 constexpr int P_BM = 128;
 constexpr int P_NON_EPI = 4;
-constexpr int P_EWG = 2;                 // epilogue warpgroups (split the columns)
+#ifndef MPK_PAIR_EWG
+#define MPK_PAIR_EWG 2
+#endif
+#ifndef MPK_PAIR_DBUF
+#define MPK_PAIR_DBUF 0                  // double-buffered TMEM loads (measured slower: 2.88 vs 2.77 ms)
+#endif
+constexpr int P_EWG = MPK_PAIR_EWG;      // epilogue warpgroups (split the columns)
 constexpr int P_EPI = 4 * P_EWG;
 constexpr int P_THREADS = (P_NON_EPI + P_EPI) * 32;
 constexpr int P_MAX_ACC = 4;
@@ -232,18 +238,22 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int q = u * 32 + lane;
-                const int s0 = (par * P_EWG + 0) * P_BM + q, s1 = (par * P_EWG + 1) * P_BM + q;
+                const int s0 = (par * P_EWG + 0) * P_BM + q;
                 float b1 = part_v[s0], b2 = FINAL ? part_v2[s0] : INFINITY;
                 int j1 = part_j[s0];
-                const float ob1 = part_v[s1];
-                const int oj1 = part_j[s1];
-                const float ob2 = FINAL ? part_v2[s1] : INFINITY;
-                if (ob1 < b1 || (ob1 == b1 && oj1 < j1)) {
-                    b2 = fminf(ob2, b1);
-                    b1 = ob1;
-                    j1 = oj1;
-                } else {
-                    b2 = fminf(b2, ob1);
+#pragma unroll
+                for (int o = 1; o < P_EWG; ++o) {
+                    const int so = (par * P_EWG + o) * P_BM + q;
+                    const float ob1 = part_v[so];
+                    const int oj1 = part_j[so];
+                    const float ob2 = FINAL ? part_v2[so] : INFINITY;
+                    if (ob1 < b1 || (ob1 == b1 && oj1 < j1)) {
+                        b2 = fminf(ob2, b1);
+                        b1 = ob1;
+                        j1 = oj1;
+                    } else {
+                        b2 = fminf(b2, ob1);
+                    }
                 }
                 const int64_t row = rb * rows_per_rb + rank * P_BM + q;
                 if (row >= n) continue;
@@ -314,6 +324,9 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             if (trace_me && ai < TRACE_T) trace[ai * 8 + 5] = clock64();   // row-block top
             float cv[NCH], c2[NCH], cs[NCH];
             chains_init(cv, cs, c2);
+            uint64_t s2[NCH / 2];               // packed chain offsets (non-FINAL fold)
+#pragma unroll
+            for (int m = 0; m < NCH / 2; ++m) s2[m] = pack2(-1.0f, -1.0f);
             for (int t = 0; t < NT; ++t, ++ai) {
                 mbar_wait(smem_u32(&t_full[buf]), tph);
                 tc_fence_after();
@@ -322,14 +335,41 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 const uint32_t col0 = tmem_base + lane_addr + (uint32_t)buf * NB + col_off;
                 const int jbase = t * NB + col_off;
                 if (!(dbg & 1)) {
-                    int c = 0;
-                    for (; c + 32 <= wcols; c += 32) {
-                        uint32_t va[32];
-                        tmem_ld32(col0 + c, va);
+                    // 32-column chunks with the TMEM loads double-buffered: chunk i+1 is in
+                    // flight while chunk i folds (both warps of a sub-partition start a tile
+                    // together, so an unhidden load stalls the pair; measured ~150 cycles/chunk)
+                    const int nch = wcols >> 5;
+                    const int c = nch << 5;
+                    auto fold = [&](const uint32_t (&vr)[32], int cc) {
+                        if (FINAL) {
+                            if (guard) fold32<true, true>(vr, cn_s, sc_s, m2, jbase + cc, cv, cs, c2);
+                            else fold32<false, true>(vr, cn_s, sc_s, m2, jbase + cc, cv, cs, c2);
+                        } else {
+                            if (guard) fold32_x2<true>(vr, cn_s, sc_s, m2, jbase + cc, cv, s2);
+                            else fold32_x2<false>(vr, cn_s, sc_s, m2, jbase + cc, cv, s2);
+                        }
+                    };
+                    uint32_t va[32];
+#if MPK_PAIR_DBUF
+                    uint32_t vb[32];
+                    if (nch > 0) tmem_ld32(col0, va);
+                    for (int i = 0; i < nch; i += 2) {
                         tmem_wait_ld_dep(va);
-                        if (guard) fold32<true, FINAL>(va, cn_s, sc_s, m2, jbase + c, cv, cs, c2);
-                        else fold32<false, FINAL>(va, cn_s, sc_s, m2, jbase + c, cv, cs, c2);
+                        if (i + 1 < nch) tmem_ld32(col0 + (i + 1) * 32, vb);
+                        fold(va, i * 32);
+                        if (i + 1 < nch) {
+                            tmem_wait_ld_dep(vb);
+                            if (i + 2 < nch) tmem_ld32(col0 + (i + 2) * 32, va);
+                            fold(vb, (i + 1) * 32);
+                        }
                     }
+#else
+                    for (int i = 0; i < nch; ++i) {
+                        tmem_ld32(col0 + i * 32, va);
+                        tmem_wait_ld_dep(va);
+                        fold(va, i * 32);
+                    }
+#endif
                     if (c < wcols) {   // a 16-column remainder (wcols is a multiple of 16)
                         uint32_t va[32];
                         tmem_ld16(col0 + c, va);
@@ -340,8 +380,14 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                             const float s = guard ? m2 * sc_s[j] : -2.0f;
                             const float x = fmaf(__uint_as_float(va[e]), s, cn_s[j]);
                             const int ch = e & 7;
-                            if (FINAL) chain_step2(x, cv[ch], c2[ch], cs[ch]);
-                            else chain_step(x, cv[ch], cs[ch]);
+                            if (FINAL) {
+                                chain_step2(x, cv[ch], c2[ch], cs[ch]);
+                            } else {
+                                float lo, hi;
+                                unpack2(s2[ch >> 1], lo, hi);
+                                chain_step(x, cv[ch], (ch & 1) ? hi : lo);
+                                s2[ch >> 1] = pack2(lo, hi);
+                            }
                         }
                     }
                 }
@@ -357,6 +403,10 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             }
             // chains -> columns: ordinal v = t * gpt + g' (tile t, g'-th group of this
             // warpgroup's columns in it); merge: lowest value, then lowest column
+            if (!FINAL) {
+#pragma unroll
+                for (int m = 0; m < NCH / 2; ++m) unpack2(s2[m], cs[2 * m], cs[2 * m + 1]);
+            }
             int jj[NCH];
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {

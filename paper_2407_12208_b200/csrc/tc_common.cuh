@@ -205,6 +205,63 @@ MPK_DEV void fold32(const uint32_t (&v)[32], const float* cn_s, const float* sc_
     }
 }
 
+// Packed form of chain_step for two adjacent chains (c, c+1) and the two columns of one group
+// that feed them: the two values x = acc * m + cn and the two offset updates s = s * nf - 1 are
+// single FFMA2 (fp32x2) instructions, so a column costs 2 alu-pipe ops (set.geu, min) plus half
+// of two fma-pipe ops, and the alu pipe — not instruction issue — bounds the fold.
+// acc2 / cn2 / m2 hold (column c, column c+1) as the low / high words; s2 likewise.
+MPK_DEV void chain_step_x2(uint64_t acc2, uint64_t cn2, uint64_t m2, float& va, float& vb,
+                           uint64_t& s2, uint64_t m1) {
+    asm("{\n\t"
+        ".reg .b64 x2, nf2;\n\t"
+        ".reg .f32 xa, xb, na, nb;\n\t"
+        "fma.rn.f32x2 x2, %3, %4, %5;\n\t"
+        "mov.b64 {xa, xb}, x2;\n\t"
+        "set.geu.f32.f32 na, xa, %0;\n\t"
+        "set.geu.f32.f32 nb, xb, %1;\n\t"
+        "min.f32 %0, %0, xa;\n\t"
+        "min.f32 %1, %1, xb;\n\t"
+        "mov.b64 nf2, {na, nb};\n\t"
+        "fma.rn.f32x2 %2, %2, nf2, %6;\n\t"
+        "}"
+        : "+f"(va), "+f"(vb), "+l"(s2)
+        : "l"(acc2), "l"(m2), "l"(cn2), "l"(m1));
+}
+MPK_DEV uint64_t pack2(float lo, float hi) {
+    return ((uint64_t)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+}
+MPK_DEV uint64_t pack2u(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
+MPK_DEV void unpack2(uint64_t v, float& lo, float& hi) {
+    lo = __uint_as_float((uint32_t)v);
+    hi = __uint_as_float((uint32_t)(v >> 32));
+}
+// fold32 without the second minimum, chain offsets kept packed in pairs (s2[m] = chains 2m,
+// 2m+1). Same results as fold32<GUARD, false>: x is the same single-rounding fma per column and
+// the chain update is the same three operations.
+template <bool GUARD, bool GCN = false>
+MPK_DEV void fold32_x2(const uint32_t (&v)[32], const float* cn_s, const float* sc_s, float m2,
+                       int j0, float (&cv)[NCH], uint64_t (&s2)[NCH / 2]) {
+    const uint32_t cn_a = GCN ? 0u : smem_u32(cn_s + j0);
+    const uint32_t sc_a = GCN ? 0u : smem_u32(sc_s + j0);
+    const uint64_t m1 = pack2(-1.0f, -1.0f);
+    const uint64_t mm = pack2(-2.0f, -2.0f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const float4 cc = GCN ? ldg_f4_keep(cn_s + j0 + 4 * e) : lds_f4(cn_a + 16 * e);
+        uint64_t s01 = mm, s23 = mm;
+        if (GUARD) {
+            const float4 ss = GCN ? ldg_f4_keep(sc_s + j0 + 4 * e) : lds_f4(sc_a + 16 * e);
+            s01 = pack2(m2 * ss.x, m2 * ss.y);
+            s23 = pack2(m2 * ss.z, m2 * ss.w);
+        }
+        const int c0 = (e & 1) * 4;          // chains c0 .. c0+3 take columns 4e .. 4e+3
+        chain_step_x2(pack2u(v[4 * e + 0], v[4 * e + 1]), pack2(cc.x, cc.y), s01, cv[c0 + 0],
+                      cv[c0 + 1], s2[c0 / 2 + 0], m1);
+        chain_step_x2(pack2u(v[4 * e + 2], v[4 * e + 3]), pack2(cc.z, cc.w), s23, cv[c0 + 2],
+                      cv[c0 + 3], s2[c0 / 2 + 1], m1);
+    }
+}
+
 // Merge the chains of one point given each chain's column jj[c]: smallest value, then smallest
 // column (the sequential scan's result). Returns the winning chain in *w (for TOP2).
 MPK_DEV void merge_chains(const float (&cv)[NCH], const int (&jj)[NCH], float& b1, int& j1,

@@ -1,0 +1,60 @@
+// fold_bench.cu — the pair kernel's fold (fold32_x2 / fold32) in isolation: 8 warps per SM
+// (2 per SM sub-partition), register "accumulators", ||c||^2 from shared memory as in the
+// kernel. Cycles per 32-column chunk per warp vs the alu-pipe model (64 alu ops x 2 = 128).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2407_12208_b200/csrc \
+//        -o tools/fold_bench tools/fold_bench.cu
+#include <cstdio>
+#include "common.cuh"
+#include "tc_common.cuh"
+
+using namespace mpk::tcdev;
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 1) k(int iters, unsigned long long* out, float* sink) {
+    __shared__ __align__(16) float cn_s[1024];
+    for (int j = threadIdx.x; j < 1024; j += blockDim.x) cn_s[j] = 0.5f * j;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    uint32_t va[32];
+    for (int e = 0; e < 32; ++e) va[e] = __float_as_uint(lane * 0.25f + e);
+    float cv[NCH], cs[NCH], c2[NCH];
+    chains_init(cv, cs, c2);
+    uint64_t s2[NCH / 2];
+    for (int m = 0; m < NCH / 2; ++m) s2[m] = pack2(-1.f, -1.f);
+    const unsigned long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+        const int j0 = (i * 32) & 1023;
+        if (MODE == 0) fold32_x2<false>(va, cn_s, cn_s, -2.f, j0, cv, s2);
+        else fold32<false, false>(va, cn_s, cn_s, -2.f, j0, cv, cs, c2);
+        va[0] ^= 1;   // keep the data live / varying
+    }
+    const unsigned long long t1 = clock64();
+    float acc = 0.f;
+    for (int c = 0; c < NCH; ++c) acc += cv[c] + cs[c];
+    for (int m = 0; m < NCH / 2; ++m) acc += __uint_as_float((uint32_t)s2[m]);
+    sink[blockIdx.x * 256 + threadIdx.x] = acc;
+    if (lane == 0) atomicAdd(out, t1 - t0);
+}
+
+template <int MODE>
+void run(const char* nm) {
+    unsigned long long* d;
+    float* sink;
+    cudaMalloc(&d, 8);
+    cudaMalloc(&sink, 148 * 256 * 4);
+    cudaMemset(d, 0, 8);
+    const int iters = 20000;
+    k<MODE><<<148, 256>>>(iters, d, sink);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return; }
+    unsigned long long c;
+    cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+    printf("%-28s %.1f cycles per 32-column chunk per warp (alu model 128, 2 warps/SMSP)\n", nm,
+           (double)c / (148.0 * 8) / iters);
+}
+
+int main() {
+    run<0>("fold32_x2 (FFMA2)");
+    run<1>("fold32 (scalar)");
+    return 0;
+}
