@@ -93,7 +93,12 @@ typedef struct kmeans_stats {
     int64_t changed_t[KMEANS_MAX_TRACE]; /* labels that changed in iteration t              */
     int32_t empty_t[KMEANS_MAX_TRACE];   /* empty clusters in iteration t                   */
     int64_t n_kernel_launches;           /* kernels this library launched during the fit    */
-    int64_t n_final_fallback;            /* final-pass rows re-evaluated on CUDA cores (-1: all) */
+    int64_t n_final_fallback;            /* final-pass rows re-evaluated on CUDA cores over all
+                                            k centroids (-1: all rows)                     */
+    int64_t n_final_uncertified;         /* final-pass rows the tensor-core filter could not
+                                            certify; those with at most 32 candidate columns
+                                            are resolved by exact fp32 evaluation of the
+                                            candidates only (R2)                 */
 } kmeans_stats;
 
 /*

@@ -46,7 +46,8 @@ class kmeans_stats(ct.Structure):
                 ("shift2_t", ct.c_double * KMEANS_MAX_TRACE),
                 ("changed_t", ct.c_int64 * KMEANS_MAX_TRACE),
                 ("empty_t", ct.c_int32 * KMEANS_MAX_TRACE),
-                ("n_kernel_launches", ct.c_int64), ("n_final_fallback", ct.c_int64)]
+                ("n_kernel_launches", ct.c_int64), ("n_final_fallback", ct.c_int64),
+                ("n_final_uncertified", ct.c_int64)]
 
 
 def _load():
@@ -203,7 +204,8 @@ def stats_dict(st: kmeans_stats) -> dict:
                 t_finalize_ms=st.t_finalize_ms, t_allreduce_ms=st.t_allreduce_ms,
                 sse_t=list(st.sse_t[:t]), shift2_t=list(st.shift2_t[:t]),
                 changed_t=list(st.changed_t[:t]), empty_t=list(st.empty_t[:t]),
-                n_kernel_launches=st.n_kernel_launches, n_final_fallback=st.n_final_fallback)
+                n_kernel_launches=st.n_kernel_launches, n_final_fallback=st.n_final_fallback,
+                n_final_uncertified=st.n_final_uncertified)
 
 
 class KMeans:

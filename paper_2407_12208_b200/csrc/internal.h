@@ -109,9 +109,31 @@ cudaError_t launch_assign_tc(TcPlan* plan, const Problem& p, const float* xn, co
 // Final pass (Alg 3 step 7) as a certified tensor-core filter: rows whose top-2 gap exceeds the
 // error bound get the filter's argmin (= the working-precision argmin); the others are appended
 // to fb_rows (count in *fb_count) for launch_assign_simt(row_list = fb_rows).
+// fb_thr (optional): per fallback slot, the candidate threshold T = v^(1) + 2 (E + B32) (NaN
+// when the row's values are not finite).
 cudaError_t launch_final_tc(TcPlan* plan, const Problem& p, const float* xn, const float* sx,
                             const float* cn, const float* sc, int32_t* labels, int* fb_count,
-                            int* fb_rows, cudaStream_t s);
+                            int* fb_rows, float* fb_thr, cudaStream_t s);
+// Candidate stage of the final pass (CTA-pair plans only): for nc gathered operand rows Xc (same
+// layout as the plan's rows) with thresholds thr, append every column j with v^_j <= thr[r] to
+// cand[r * cand_q ...] (count in cand_cnt[r], which may exceed cand_q: overflow).
+bool tc_plan_has_cand(const TcPlan* plan);
+const void* tc_plan_operands(const TcPlan* plan, int* row_bytes);
+cudaError_t launch_cand_tc(TcPlan* plan, const void* Xc, int64_t nc, int guard, const float* sxc,
+                           const float* cn, const float* sc, const float* thr, int* cand_cnt,
+                           int* cand, int cand_q, cudaStream_t s);
+// Gather rows[0..nr) of a row-major byte matrix (row_bytes, multiple of 16) and, optionally,
+// of a float vector.
+cudaError_t launch_gather_rows(const void* src, int row_bytes, const int* rows, int nr, void* dst,
+                               const float* vsrc, float* vdst, cudaStream_t s);
+// Exact stage: for gathered row r (original index rows[r]) evaluate the working-precision (fp32)
+// distance of each candidate exactly as launch_assign_simt does (dot accumulated t = 0..d-1 by
+// FMA, v = fma(-2, dot, ||c_j||^2)) and store the (value, lowest index) argmin in labels[rows[r]];
+// rows with no candidates or more than cand_q go to left_rows (count in *left_count).
+cudaError_t launch_cand_exact(const float* Xw, const float* Cw, const float* cn, int d,
+                              const int* rows, int nr, const int* cand_cnt, const int* cand,
+                              int cand_q, int32_t* labels, int* left_count, int* left_rows,
+                              cudaStream_t s);
 
 // K7: update = bucket by label (count, scan, scatter) + segmented fp64 sums.
 cudaError_t launch_update(int work, const void* Xw, int64_t n, int d, int k,

@@ -345,6 +345,7 @@ struct TcPlan {
     tcdev::Params prm;             // kind 1
     tcdev::PairParams pp;          // kind 2
     size_t smem_bytes;
+    const void* Xl;                // the operand rows tmap_x covers (for gathers)
 };
 
 static int esize_of(int dist) { return dist == KMEANS_E5M2 ? 1 : 2; }
@@ -417,6 +418,7 @@ TcPlan* tc_plan_create(int dist, int64_t n, int d, int d_pad, int k, const void*
                        const void* Cl, std::string* err) {
     TcPlan* pl = new TcPlan();
     pl->dist = dist; pl->n = n; pl->d = d; pl->d_pad = d_pad; pl->k = k;
+    pl->Xl = Xl;
     const int es = esize_of(dist);
     pl->esize = es;
     // Preferred: CTA pairs with the centroid tiles resident in shared memory (k_assign_tc2.cu).
@@ -556,14 +558,14 @@ cudaError_t launch_assign_tc(TcPlan* pl, const Problem& pb, const float* xn, con
         tcdev::PairParams q = pl->pp;
         q.n = pb.n; q.guard = pb.guard; q.xn = xn; q.sx = sx; q.cn = cn; q.sc = sc;
         q.labels = labels; q.acc_sse = acc_sse; q.acc_changed = acc_changed;
-        return tcdev::pair_launch(pl->tmap_x, pl->tmap_c, q, false, pl->smem_bytes, s);
+        return tcdev::pair_launch(pl->tmap_x, pl->tmap_c, q, tcdev::PAIR_ASSIGN, pl->smem_bytes, s);
     }
     return launch_impl(pl, p, false, s);
 }
 
 cudaError_t launch_final_tc(TcPlan* pl, const Problem& pb, const float* xn, const float* sx,
                             const float* cn, const float* sc, int32_t* labels, int* fb_count,
-                            int* fb_rows, cudaStream_t s) {
+                            int* fb_rows, float* fb_thr, cudaStream_t s) {
     tcdev::Params p = pl->prm;
     p.n = pb.n;
     p.guard = pb.guard;
@@ -574,10 +576,31 @@ cudaError_t launch_final_tc(TcPlan* pl, const Problem& pb, const float* xn, cons
     if (pl->kind == 2) {
         tcdev::PairParams q = pl->pp;
         q.n = pb.n; q.guard = pb.guard; q.xn = xn; q.sx = sx; q.cn = cn; q.sc = sc;
-        q.labels = labels; q.fb_count = fb_count; q.fb_rows = fb_rows;
-        return tcdev::pair_launch(pl->tmap_x, pl->tmap_c, q, true, pl->smem_bytes, s);
+        q.labels = labels; q.fb_count = fb_count; q.fb_rows = fb_rows; q.fb_thr = fb_thr;
+        return tcdev::pair_launch(pl->tmap_x, pl->tmap_c, q, tcdev::PAIR_FINAL, pl->smem_bytes, s);
     }
     return launch_impl(pl, p, true, s);
+}
+
+bool tc_plan_has_cand(const TcPlan* pl) { return pl && pl->kind == 2; }
+const void* tc_plan_operands(const TcPlan* pl, int* row_bytes) {
+    *row_bytes = pl->d_pad * pl->esize;
+    return pl->Xl;
+}
+
+cudaError_t launch_cand_tc(TcPlan* pl, const void* Xc, int64_t nc, int guard, const float* sxc,
+                           const float* cn, const float* sc, const float* thr, int* cand_cnt,
+                           int* cand, int cand_q, cudaStream_t s) {
+    if (pl->kind != 2) return cudaErrorNotSupported;
+    if (nc <= 0) return cudaSuccess;
+    CUtensorMap tmx;
+    std::string err;
+    if (!encode(&tmx, pl->dist, Xc, nc, pl->d_pad, pl->pp.SWZ, 128, &err))
+        return cudaErrorInvalidValue;
+    tcdev::PairParams q = pl->pp;
+    q.n = nc; q.guard = guard; q.sx = sxc; q.cn = cn; q.sc = sc;
+    q.thr = thr; q.cand_cnt = cand_cnt; q.cand = cand; q.cand_q = cand_q;
+    return tcdev::pair_launch(tmx, pl->tmap_c, q, tcdev::PAIR_CAND, pl->smem_bytes, s);
 }
 
 }  // namespace mpk

@@ -21,7 +21,11 @@
 //     shared memory; warp 3 merges the two partials and does the label store, the changed
 //     count and the SSE (or, in FINAL mode, the certification).
 // DESIGN.md "pair kernel" has the measured per-tile budget this layout comes from.
-// FINAL mode: certified top-2 filter for Alg 3 step 7, as in k_assign_tc.cu.
+// FINAL mode: certified top-2 filter for Alg 3 step 7, as in k_assign_tc.cu; each uncertified
+// row also gets its candidate threshold T = v^(1) + 2 (E + B32) (rounded up).
+// CAND mode (same operands, gathered uncertified rows): emit every column j with v^_j <= T —
+// the working-precision argmin of the row, and every column tied with it, is among them
+// (R2), so the exact fp32 re-evaluation only needs those columns.
 #include "common.cuh"
 #include "internal.h"
 #include "tc_common.cuh"
@@ -59,10 +63,38 @@ MPK_DEV void named_bar_arrive(int id, int nthreads) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-template <bool FINAL>
+// CAND: one 32-column chunk -> candidate columns (value computed exactly as in fold32)
+template <bool GUARD>
+MPK_DEV void cand32(const uint32_t (&v)[32], const float* cn_s, const float* sc_s, float m2,
+                    int j0, float T, int* cnt, int* cand, int Q) {
+    const uint32_t cn_a = smem_u32(cn_s + j0);
+    const uint32_t sc_a = smem_u32(sc_s + j0);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const float4 cc = lds_f4(cn_a + 16 * e);
+        float s[4] = {-2.0f, -2.0f, -2.0f, -2.0f};
+        if (GUARD) {
+            const float4 ss = lds_f4(sc_a + 16 * e);
+            s[0] = m2 * ss.x; s[1] = m2 * ss.y; s[2] = m2 * ss.z; s[3] = m2 * ss.w;
+        }
+        const float cnv[4] = {cc.x, cc.y, cc.z, cc.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float x = fmaf(__uint_as_float(v[4 * e + u]), s[u], cnv[u]);
+            if (x <= T) {
+                const int sl = atomicAdd(cnt, 1);
+                if (sl < Q) cand[sl] = j0 + 4 * e + u;
+            }
+        }
+    }
+}
+
+template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                    const __grid_constant__ CUtensorMap tmap_c, PairParams p) {
+    constexpr bool FINAL = MODE == PAIR_FINAL;
+    constexpr bool CAND = MODE == PAIR_CAND;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* b_base = smem;                                             // resident centroid halves
@@ -209,6 +241,8 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 if (++slot == SA) { slot = 0; aph ^= 1; }
             }
         }
+    } else if (warp == 3 && CAND) {
+        // no row-block end in CAND mode
     } else if (warp == 3) {
         // ------------------------------------------------ row-block end (both CTAs): merge the
         // two warpgroups' partials; labels, changed count and SSE (FINAL: certification)
@@ -283,6 +317,10 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                     if (!ok) {
                         const int slot = atomicAdd(p.fb_count, 1);
                         p.fb_rows[slot] = (int)row;
+                        if (p.fb_thr) {
+                            const bool fin = isfinite(b1) && isfinite(xn) && isfinite(cmax);
+                            p.fb_thr[slot] = fin ? __double2float_ru((double)b1 + thr) : NAN;
+                        }
                     }
                 }
             }
@@ -321,6 +359,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
         for (int64_t rb = pair; rb < num_rb; rb += npairs, ++rbi) {
             const int64_t row = rb * rows_per_rb + rank * P_BM + q;
             const float m2 = (guard && row < n) ? -2.0f * p.sx[row] : -2.0f;
+            const float T = (CAND && row < n) ? p.thr[row] : NAN;          // CAND threshold
             if (trace_me && ai < TRACE_T) trace[ai * 8 + 5] = clock64();   // row-block top
             float cv[NCH], c2[NCH], cs[NCH];
             chains_init(cv, cs, c2);
@@ -341,7 +380,12 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                     const int nch = wcols >> 5;
                     const int c = nch << 5;
                     auto fold = [&](const uint32_t (&vr)[32], int cc) {
-                        if (FINAL) {
+                        if (CAND) {
+                            int* ccnt = p.cand_cnt + (row < n ? row : 0);
+                            int* cl = p.cand + (row < n ? row : 0) * (int64_t)p.cand_q;
+                            if (guard) cand32<true>(vr, cn_s, sc_s, m2, jbase + cc, T, ccnt, cl, p.cand_q);
+                            else cand32<false>(vr, cn_s, sc_s, m2, jbase + cc, T, ccnt, cl, p.cand_q);
+                        } else if (FINAL) {
                             if (guard) fold32<true, true>(vr, cn_s, sc_s, m2, jbase + cc, cv, cs, c2);
                             else fold32<false, true>(vr, cn_s, sc_s, m2, jbase + cc, cv, cs, c2);
                         } else {
@@ -380,7 +424,12 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                             const float s = guard ? m2 * sc_s[j] : -2.0f;
                             const float x = fmaf(__uint_as_float(va[e]), s, cn_s[j]);
                             const int ch = e & 7;
-                            if (FINAL) {
+                            if (CAND) {
+                                if (x <= T) {
+                                    const int sl = atomicAdd(p.cand_cnt + row, 1);
+                                    if (sl < p.cand_q) p.cand[row * (int64_t)p.cand_q + sl] = j;
+                                }
+                            } else if (FINAL) {
                                 chain_step2(x, cv[ch], c2[ch], cs[ch]);
                             } else {
                                 float lo, hi;
@@ -401,6 +450,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 if (tr) trace[ai * 8 + 4] = clock64();
                 if (++buf == nacc) { buf = 0; tph ^= 1; }
             }
+            if (CAND) continue;
             // chains -> columns: ordinal v = t * gpt + g' (tile t, g'-th group of this
             // warpgroup's columns in it); merge: lowest value, then lowest column
             if (!FINAL) {
@@ -493,21 +543,25 @@ bool pair_plan(int dist, int d, int d_pad, int k, PairParams* pp, size_t* smem_b
 int pair_box_rows(const PairParams& p) { return p.NB / 2; }
 
 cudaError_t pair_set_smem(size_t bytes) {
-    cudaError_t e = cudaFuncSetAttribute(assign_pair_kernel<false>,
+    cudaError_t e = cudaFuncSetAttribute(assign_pair_kernel<PAIR_ASSIGN>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(assign_pair_kernel<true>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(assign_pair_kernel<PAIR_FINAL>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(assign_pair_kernel<PAIR_CAND>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    return e;
 }
 
 cudaError_t pair_launch(const CUtensorMap& tmap_x, const CUtensorMap& tmap_c, const PairParams& p,
-                        bool final_mode, size_t smem_bytes, cudaStream_t s) {
+                        int mode, size_t smem_bytes, cudaStream_t s) {
     const int64_t num_rb = (p.n + 2 * P_BM - 1) / (2 * P_BM);
     int64_t grid = std::min<int64_t>(kNumSMs, 2 * num_rb);
     grid &= ~int64_t(1);
     if (grid < 2) grid = 2;
     launches_add(1);
-    if (const char* tf = getenv("MPK_PAIR_TRACE"); tf && !final_mode) {
+    if (const char* tf = getenv("MPK_PAIR_TRACE"); tf && mode == PAIR_ASSIGN) {
         // debug: one traced launch, stamps dumped as text (tile, 5 clock64 values)
         PairParams q = p;
         static unsigned long long* buf = nullptr;
@@ -515,7 +569,7 @@ cudaError_t pair_launch(const CUtensorMap& tmap_x, const CUtensorMap& tmap_c, co
         if (!buf) cudaMalloc(&buf, bytes);
         cudaMemsetAsync(buf, 0, bytes, s);
         q.trace = buf;
-        assign_pair_kernel<false><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, q);
+        assign_pair_kernel<PAIR_ASSIGN><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, q);
         cudaStreamSynchronize(s);
         static unsigned long long h[TRACE_T * 8];
         cudaMemcpy(h, buf, bytes, cudaMemcpyDeviceToHost);
@@ -528,10 +582,12 @@ cudaError_t pair_launch(const CUtensorMap& tmap_x, const CUtensorMap& tmap_c, co
         }
         return cudaGetLastError();
     }
-    if (final_mode)
-        assign_pair_kernel<true><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, p);
+    if (mode == PAIR_FINAL)
+        assign_pair_kernel<PAIR_FINAL><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, p);
+    else if (mode == PAIR_CAND)
+        assign_pair_kernel<PAIR_CAND><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, p);
     else
-        assign_pair_kernel<false><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, p);
+        assign_pair_kernel<PAIR_ASSIGN><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, p);
     return cudaGetLastError();
 }
 

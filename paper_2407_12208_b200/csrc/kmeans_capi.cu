@@ -60,8 +60,17 @@ struct kmeans_ctx {
     void* fin_sc = nullptr;
     int fin_dpad = 0;
     bool fin_failed = false;
-    int* fbc = nullptr;            // fallback-row counter
+    int* fbc = nullptr;            // [0] uncertified rows, [1] rows left for the full evaluation
     int64_t last_fallback = 0;     // rows re-evaluated on CUDA cores in the last final pass
+    int64_t last_uncertified = 0;  // rows the certified filter left open in the last final pass
+    // final-pass candidate path (grown to the uncertified row count on demand)
+    int64_t cand_cap = 0;
+    float* fb_thr = nullptr;       // per uncertified row: threshold T (size n)
+    void* cand_X = nullptr;        // gathered operand rows
+    float* cand_sx = nullptr;
+    int* cand_cnt = nullptr;
+    int* cand = nullptr;           // [cap][kCandQ]
+    int* cand_left = nullptr;      // rows left for the full CUDA-core evaluation
     int dist_kernel = 0;
     AccLayout L{0, 0};
 
@@ -147,7 +156,8 @@ cudaError_t dalloc(T** p, size_t bytes) {
 void free_all(kmeans_ctx* h) {
     if (h->tc) tc_plan_destroy(h->tc);
     if (h->fin) tc_plan_destroy(h->fin);
-    void* fin_bufs[] = {h->fin_Xl, h->fin_Cl, h->fin_sx, h->fin_sc, h->fbc};
+    void* fin_bufs[] = {h->fin_Xl, h->fin_Cl, h->fin_sx, h->fin_sc, h->fbc, h->fb_thr,
+                        h->cand_X, h->cand_sx, h->cand_cnt, h->cand, h->cand_left};
     for (void* b : fin_bufs)
         if (b) cudaFree(b);
     void* bufs[] = {h->Xw, h->xl_alias ? nullptr : h->Xl, h->xn, h->sx, h->Cw, h->Cl, h->cn,
@@ -374,11 +384,14 @@ int prep_centroids(kmeans_ctx* h) {
 // the filter's argmin, which equals the working-precision argmin; the remaining rows are
 // re-evaluated by the CUDA-core kernel in working precision. Otherwise the CUDA-core kernel
 // evaluates every row.
+constexpr int kCandQ = 32;   // candidate columns kept per uncertified row
+
 int final_assign(kmeans_ctx* h, const Problem& pf) {
     cudaStream_t s = h->stream;
     const int64_t n = h->n;
     const int d = h->d, k = h->k;
     h->last_fallback = -1;
+    h->last_uncertified = -1;
     // working-precision norms of the final centroids
     CK(launch_prep(h->work, h->work, h->Cw, k, d, d, 0, h->cn, nullptr, h->Cl, nullptr, s));
     TcPlan* plan = nullptr;
@@ -433,15 +446,56 @@ int final_assign(kmeans_ctx* h, const Problem& pf) {
     }
     if (plan) {
         Problem p{n, d, k, fdpad, fguard};
-        CK(cudaMemsetAsync(h->fbc, 0, sizeof(int), s));
+        const bool cand_path = tc_plan_has_cand(plan) && getenv("MPK_NO_CAND") == nullptr;
+        if (cand_path && !h->fb_thr) CK(cudaMalloc(&h->fb_thr, (size_t)std::max<int64_t>(n, 1) * 4));
+        CK(cudaMemsetAsync(h->fbc, 0, 2 * sizeof(int), s));
         CK(launch_final_tc(plan, p, (const float*)h->xn, (const float*)fx_sx,
                            (const float*)h->cn, (const float*)fx_sc, h->labels, h->fbc, h->perm,
-                           s));
+                           cand_path ? h->fb_thr : nullptr, s));
         int nfb = 0;
         CK(cudaMemcpyAsync(&nfb, h->fbc, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
+        h->last_uncertified = nfb;
         h->last_fallback = nfb;
-        if (nfb > 0) {
+        if (nfb > 0 && cand_path) {
+            // candidate path (R2): gather the uncertified rows' operands, list their
+            // candidate columns on the tensor cores, evaluate only those exactly in fp32
+            if (nfb > h->cand_cap) {
+                void* old[] = {h->cand_X, h->cand_sx, h->cand_cnt, h->cand, h->cand_left};
+                for (void* b : old)
+                    if (b) cudaFree(b);
+                h->cand_X = h->cand_sx = nullptr;
+                h->cand_cnt = h->cand = h->cand_left = nullptr;
+                const int64_t cap = std::min<int64_t>(n, (int64_t)nfb + nfb / 4 + 1024);
+                int rb = 0;
+                tc_plan_operands(plan, &rb);
+                CK(cudaMalloc(&h->cand_X, (size_t)cap * rb));
+                CK(cudaMalloc(&h->cand_sx, (size_t)cap * 4));
+                CK(cudaMalloc(&h->cand_cnt, (size_t)cap * 4));
+                CK(cudaMalloc(&h->cand, (size_t)cap * kCandQ * 4));
+                CK(cudaMalloc(&h->cand_left, (size_t)cap * 4));
+                h->cand_cap = cap;
+            }
+            int rb = 0;
+            const void* ops = tc_plan_operands(plan, &rb);
+            CK(launch_gather_rows(ops, rb, h->perm, nfb, h->cand_X, fguard ? (const float*)fx_sx : nullptr,
+                                  fguard ? h->cand_sx : nullptr, s));
+            CK(cudaMemsetAsync(h->cand_cnt, 0, (size_t)nfb * 4, s));
+            CK(launch_cand_tc(plan, h->cand_X, nfb, fguard, h->cand_sx, (const float*)h->cn,
+                              (const float*)fx_sc, h->fb_thr, h->cand_cnt, h->cand, kCandQ, s));
+            CK(launch_cand_exact((const float*)h->Xw, (const float*)h->Cw, (const float*)h->cn, d,
+                                 h->perm, nfb, h->cand_cnt, h->cand, kCandQ, h->labels,
+                                 h->fbc + 1, h->cand_left, s));
+            int nleft = 0;
+            CK(cudaMemcpyAsync(&nleft, h->fbc + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            h->last_fallback = nleft;
+            if (nleft > 0) {
+                Problem pl{nleft, d, k, d, 0};
+                CK(launch_assign_simt(h->work, h->work, pl, h->Xw, h->xn, nullptr, h->Cw, h->cn,
+                                      nullptr, h->labels, nullptr, nullptr, s, h->cand_left));
+            }
+        } else if (nfb > 0) {
             Problem pl{nfb, d, k, d, 0};
             CK(launch_assign_simt(h->work, h->work, pl, h->Xw, h->xn, nullptr, h->Cw, h->cn,
                                   nullptr, h->labels, nullptr, nullptr, s, h->perm));
@@ -589,6 +643,7 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
     st.n_dist_launches = it;
     st.n_kernel_launches = launches_read() - launches0;
     st.n_final_fallback = h->last_fallback;
+    st.n_final_uncertified = h->last_uncertified;
     int warn = 0;
     if (st.n_nonfinite > 0) warn |= KMEANS_WARN_NONFINITE;
     if (any_empty) warn |= KMEANS_WARN_EMPTY;

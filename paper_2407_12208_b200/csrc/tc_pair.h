@@ -25,6 +25,11 @@ struct PairParams {
     int* fb_count;
     int* fb_rows;
     double u_low, eta_low;
+    float* fb_thr;           // FINAL: per fallback slot, the candidate threshold T (NaN: none)
+    const float* thr;        // CAND: per row, T
+    int* cand_cnt;           // CAND: per row, number of candidates found
+    int* cand;               // CAND: [n][cand_q] candidate columns
+    int cand_q;
     int dbg;                 // debug: bit0 skip epilogue folding, bit1 skip MMAs (timing only)
     unsigned long long* trace;   // debug (MPK_PAIR_TRACE): per-tile clock64 stamps of CTA 0
 };
@@ -34,8 +39,11 @@ struct PairParams {
 bool pair_plan(int dist, int d, int d_pad, int k, PairParams* p, size_t* smem_bytes);
 int pair_box_rows(const PairParams& p);   // TMA box rows for the centroid map (NB / 2)
 cudaError_t pair_set_smem(size_t bytes);
+// mode: PAIR_ASSIGN (Lloyd step), PAIR_FINAL (certified final pass), PAIR_CAND (candidate
+// columns of the final pass's uncertified rows, R2)
+enum { PAIR_ASSIGN = 0, PAIR_FINAL = 1, PAIR_CAND = 2 };
 cudaError_t pair_launch(const CUtensorMap& tmap_x, const CUtensorMap& tmap_c, const PairParams& p,
-                        bool final_mode, size_t smem_bytes, cudaStream_t s);
+                        int mode, size_t smem_bytes, cudaStream_t s);
 
 }  // namespace tcdev
 }  // namespace mpk

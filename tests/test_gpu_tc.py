@@ -108,3 +108,31 @@ def test_final_pass_certified_filter(dist, guard):
         assert np.all(gap <= tol[bad]), gap.max()
     direct = float(np.sum((Xn - C[g]) ** 2))
     assert abs(sse - direct) <= 1e-6 * direct
+
+
+@pytest.mark.parametrize("dist,guard", [("fp16", False), ("e5m2", False), ("fp16", True)])
+def test_final_pass_candidates_match_full_evaluation(dist, guard, monkeypatch):
+    """DESIGN.md R2: the final pass resolves uncertified rows from their candidate columns
+    (v^_j <= T). The labels must be bit-identical to the full CUDA-core evaluation of every
+    uncertified row (MPK_NO_CAND=1), on a workload with many near-ties (1024 clusters in 128-d,
+    the C5 shape) so that the candidate path is exercised."""
+    X, _, C0 = synth.make("c5_vq_10m", n=60000, seed=11)
+    labs, stats = [], []
+    for no_cand in (False, True):
+        if no_cand:
+            monkeypatch.setenv("MPK_NO_CAND", "1")
+        else:
+            monkeypatch.delenv("MPK_NO_CAND", raising=False)
+        km = mpk.KMeans(len(X), 128, 1024, "fp32", dist, norm="zscore", guard=guard)
+        lab = torch.empty(len(X), dtype=torch.int32, device="cuda")
+        km.fit(dev(X), dev(C0), max_iter=3, tol=-1.0, labels=lab)
+        labs.append(lab.cpu().numpy())
+        stats.append(km.stats())
+        km.close()
+    cand, full = stats
+    assert cand["dist_kernel"] == "tcgen05"
+    assert cand["n_final_uncertified"] == full["n_final_uncertified"] > 100
+    # most uncertified rows are resolved from their candidates
+    assert cand["n_final_fallback"] < 0.2 * cand["n_final_uncertified"]
+    assert full["n_final_fallback"] == full["n_final_uncertified"]
+    np.testing.assert_array_equal(labs[0], labs[1])
