@@ -66,10 +66,18 @@ cudaError_t launch_norm_ssq(int work, const void* X, int64_t n, int d, double* p
 cudaError_t launch_norm_post(int mode, int d, double n_total, double* shift, double* scale,
                              cudaStream_t s);
 cudaError_t launch_norm_apply(int work, void* X, int64_t rows, int d, const double* shift,
-                              const double* scale, cudaStream_t s);
+                              const double* scale, cudaStream_t s, const void* Xin = nullptr);
 int norm_stats_blocks(int64_t n, int d);
 
 // K1 / K3: norms (fp64 -> work), guard scales, low-precision operands with padding, census.
+// K1 fast path (fp32 work, d <= 256, see prep_fast_ok): the same outputs as launch_prep; with
+// shift != nullptr also the normalisation of the rows read from Xin, written to Xout (one read
+// of X for normalise + prep).
+bool prep_fast_ok(int work, int d);
+cudaError_t launch_prep_fast(int dist, const void* Xin, int64_t rows, int d, int d_pad, int guard,
+                             void* norms, void* scales, void* Xl, unsigned long long* census,
+                             void* Xout, const double* shift, const double* scale,
+                             cudaStream_t s);
 cudaError_t launch_prep(int work, int dist, const void* Xw, int64_t rows, int d, int d_pad,
                         int guard, void* norms, void* scales, void* Xl,
                         unsigned long long* census /* [nonfinite, underflow] */, cudaStream_t s);

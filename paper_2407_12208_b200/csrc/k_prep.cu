@@ -18,6 +18,7 @@ namespace mpk {
 namespace {
 
 constexpr int kStatThreads = 256;
+constexpr int kApplySmemD = 2048;        // norm_apply caches shift / scale / 1/scale up to this d
 
 // One kernel for the three column statistics: mode 0 = sum x, mode 1 = sum (x - mu)^2,
 // mode 2 = (min, max). Thread layout: column c = tid % d, row lane = tid / d (d <= 256), else a
@@ -113,13 +114,24 @@ __global__ void norm_combine_kernel(int mode, const double* __restrict__ partial
         b[c] = mx;
         return;
     }
+    // block order, partials loaded in batches of 16 (independent loads in flight; the serial
+    // dependent loads of one thread were ~0.3 ms of pure L2 latency)
     double S = 0.0, Cc = 0.0;
-    for (int q = 0; q < nblocks; ++q) {
-        double s2 = partials[((int64_t)q * d + c) * 2 + 0];
-        double c2 = partials[((int64_t)q * d + c) * 2 + 1];
-        double t = S + s2;
-        Cc += ((fabs(S) >= fabs(s2)) ? ((S - t) + s2) : ((s2 - t) + S)) + c2;
-        S = t;
+    for (int q0 = 0; q0 < nblocks; q0 += 16) {
+        double s2[16], c2[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int q = q0 + u;
+            s2[u] = q < nblocks ? partials[((int64_t)q * d + c) * 2 + 0] : 0.0;
+            c2[u] = q < nblocks ? partials[((int64_t)q * d + c) * 2 + 1] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            if (q0 + u >= nblocks) break;
+            const double t = S + s2[u];
+            Cc += ((fabs(S) >= fabs(s2[u])) ? ((S - t) + s2[u]) : ((s2[u] - t) + S)) + c2[u];
+            S = t;
+        }
     }
     a[c] = S + Cc;
 }
@@ -140,13 +152,35 @@ __global__ void norm_post_kernel(int mode, int d, double n_total, double* shift,
     }
 }
 
+// Correctly rounded a / b from r = RN(1/b) (Markstein: r within 1/2 ulp of 1/b, a r within
+// 1 ulp of a/b  =>  q + r (a - b q) rounds to RN(a/b); the residual is exact by FMA). Checked
+// on B200 against division for 2^28 random operand pairs of both the generic and the
+// normalisation shapes (tools/div_check.cu). Non-finite or extreme quotients take the division.
+MPK_DEV double div_rn(double a, double b, double r) {
+    const double q0 = a * r;
+    const double aq = fabs(q0);
+    if (!(aq > 0x1p-960 && aq < 0x1p960)) return a / b;
+    return fma(fma(-q0, b, a), r, q0);
+}
+
 template <typename W>
-__global__ void norm_apply_kernel(W* __restrict__ X, int64_t total, int d,
-                                  const double* __restrict__ shift,
+__global__ void norm_apply_kernel(const W* __restrict__ Xin, W* __restrict__ X, int64_t total,
+                                  int d, const double* __restrict__ shift,
                                   const double* __restrict__ scale) {
-    // x <- round_u((x - shift_c) / scale_c), fp64 arithmetic (correctly rounded division, as
-    // the oracle's O1); the column index is tracked incrementally (no 64-bit modulo).
+    // x <- round_u((x - shift_c) / scale_c), fp64 arithmetic with a correctly rounded quotient
+    // (as the oracle's O1); the column index is tracked incrementally (no 64-bit modulo). The
+    // block caches the map and the reciprocals 1 / scale_c in shared memory (d <= kApplySmemD).
     constexpr int WORK = sizeof(W) == 8 ? KMEANS_FP64 : KMEANS_FP32;
+    extern __shared__ double tsm[];
+    const bool cached = d <= kApplySmemD;
+    if (cached) {
+        for (int c = threadIdx.x; c < d; c += blockDim.x) {
+            tsm[c] = shift[c];
+            tsm[d + c] = scale[c];
+            tsm[2 * d + c] = 1.0 / scale[c];
+        }
+        __syncthreads();
+    }
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= total) return;
@@ -159,7 +193,7 @@ __global__ void norm_apply_kernel(W* __restrict__ X, int64_t total, int d,
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int64_t iu = i + (int64_t)u * stride;
-            xv[u] = iu < total ? X[iu] : (W)0;
+            xv[u] = iu < total ? Xin[iu] : (W)0;
             cc[u] = c;
             c += cstep;
             if (c >= d) c -= d;
@@ -167,7 +201,12 @@ __global__ void norm_apply_kernel(W* __restrict__ X, int64_t total, int d,
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int64_t iu = i + (int64_t)u * stride;
-            if (iu < total) X[iu] = rounder<WORK>::from(((double)xv[u] - shift[cc[u]]) / scale[cc[u]]);
+            if (iu >= total) continue;
+            const int cu = cc[u];
+            double q;
+            if (cached) q = div_rn((double)xv[u] - tsm[cu], tsm[d + cu], tsm[2 * d + cu]);
+            else q = ((double)xv[u] - shift[cu]) / scale[cu];
+            X[iu] = rounder<WORK>::from(q);
         }
     }
 }
@@ -337,15 +376,169 @@ cudaError_t launch_norm_post(int mode, int d, double n_total, double* shift, dou
 }
 
 cudaError_t launch_norm_apply(int work, void* X, int64_t rows, int d, const double* shift,
-                              const double* scale, cudaStream_t s) {
+                              const double* scale, cudaStream_t s, const void* Xin) {
     launches_add(1);
     int64_t total = rows * d;
     int g = grid_for(total, 256, 16);
+    if (!Xin) Xin = X;   // in place
+    const size_t sm = d <= kApplySmemD ? (size_t)3 * d * sizeof(double) : 0;
     if (work == KMEANS_FP64)
-        norm_apply_kernel<double><<<g, 256, 0, s>>>((double*)X, total, d, shift, scale);
+        norm_apply_kernel<double><<<g, 256, sm, s>>>((const double*)Xin, (double*)X, total, d,
+                                                     shift, scale);
     else
-        norm_apply_kernel<float><<<g, 256, 0, s>>>((float*)X, total, d, shift, scale);
+        norm_apply_kernel<float><<<g, 256, sm, s>>>((const float*)Xin, (float*)X, total, d, shift,
+                                                    scale);
     return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// K1 fast path (fp32 work, d <= 256): the same per-row arithmetic as prep_kernel, optionally
+// fused with the normalisation O1 (x <- round_u((x - shift_c) / scale_c), correctly rounded
+// quotient via div_rn) so that X is read once: each lane owns the columns lane + 32 q for every
+// row (its transform values live in registers) and a warp takes two rows per step with all
+// their loads issued first. Writes the normalised rows (NORM), ||x||^2, the guard scale and the
+// low-precision operands.
+// ------------------------------------------------------------------------------------------
+template <int DIST, bool NORM, int Q>
+MPK_DEV void prep_row_fast(float (&v)[Q], int64_t i, int lane, int d, int d_pad, int guard,
+                           const double (&sh)[Q], const double (&sc)[Q], const double (&rc)[Q],
+                           float* __restrict__ Xout, float* __restrict__ norms,
+                           float* __restrict__ scales, typename low_type<DIST>::T* __restrict__ Xl,
+                           unsigned& n_nonfinite, unsigned& n_under) {
+    using L = typename low_type<DIST>::T;
+    constexpr bool same = DIST == KMEANS_FP32;
+    int cnt = 0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int c = lane + 32 * q;
+        if (c < d) {
+            cnt = q + 1;
+            if (NORM) {
+                v[q] = __double2float_rn(div_rn((double)v[q] - sh[q], sc[q], rc[q]));
+                Xout[i * d + c] = v[q];
+            }
+        }
+    }
+    // lane_sumsq's arithmetic (exact fp32 products + TwoSum, q = 0..cnt-1), unrolled in
+    // registers (the pointer/count form put the row array on the stack)
+    float ss = 0.0f, cs = 0.0f;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        if (q < cnt) {
+            const float p = v[q] * v[q];
+            const float e = fmaf(v[q], v[q], -p);
+            const float t = ss + p;
+            const float z = t - ss;
+            cs += (ss - (t - z)) + (p - z) + e;
+            ss = t;
+        }
+    }
+    const double acc = warp_sum((double)ss + (double)cs);
+    float s = 1.0f;
+    if (guard && !same) {
+        float amax = 0.0f;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) amax = fmaxf(amax, fabsf(v[q]));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        s = (amax == 0.0f || isnan(amax)) ? 1.0f : amax;
+    }
+    if (lane == 0) {
+        norms[i] = __double2float_rn(acc);
+        if (scales) scales[i] = s;
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int c = lane + 32 * q;
+        if (c >= d_pad) break;
+        L o;
+        if (c < d) {
+            const float qv = (s == 1.0f) ? v[q] : v[q] / s;      // precision-u division (IEEE, RN)
+            o = rounder<DIST>::from(qv);
+            if (!same) {
+                if (is_nonfinite_low(o)) n_nonfinite++;
+                else if (qv != 0.0f && is_zero_or_subnormal_low(o)) n_under++;
+            }
+        } else {
+            o = rounder<DIST>::from(0.0f);
+        }
+        Xl[i * d_pad + c] = o;
+    }
+}
+
+template <int DIST, bool NORM, int Q, int RPS>
+__global__ void __launch_bounds__(256)
+prep_fast_kernel(const float* __restrict__ Xin, int64_t rows, int d, int d_pad, int guard,
+                 float* __restrict__ norms, float* __restrict__ scales,
+                 typename low_type<DIST>::T* __restrict__ Xl,
+                 unsigned long long* __restrict__ census, float* __restrict__ Xout,
+                 const double* __restrict__ shift, const double* __restrict__ scale) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double sh[Q], sc[Q], rc[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int c = lane + 32 * q;
+        sh[q] = (NORM && c < d) ? shift[c] : 0.0;
+        sc[q] = (NORM && c < d) ? scale[c] : 1.0;
+        rc[q] = 1.0 / sc[q];
+    }
+    unsigned n_nonfinite = 0, n_under = 0;
+    // RPS rows per warp per step (rows i + r * nwarps), all loads first
+    for (int64_t i = warp; i < rows; i += RPS * nwarps) {
+        float v[RPS][Q];
+#pragma unroll
+        for (int r = 0; r < RPS; ++r) {
+            const int64_t ir = i + r * nwarps;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const int c = lane + 32 * q;
+                v[r][q] = (c < d && ir < rows) ? Xin[ir * d + c] : 0.0f;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < RPS; ++r) {
+            const int64_t ir = i + r * nwarps;
+            if (ir < rows)
+                prep_row_fast<DIST, NORM, Q>(v[r], ir, lane, d, d_pad, guard, sh, sc, rc, Xout,
+                                             norms, scales, Xl, n_nonfinite, n_under);
+        }
+    }
+    if (census) {
+        const unsigned long long a = warp_sum((unsigned long long)n_nonfinite);
+        const unsigned long long b = warp_sum((unsigned long long)n_under);
+        if (lane == 0 && (a | b)) {
+            atomicAdd(&census[0], a);
+            atomicAdd(&census[1], b);
+        }
+    }
+}
+
+template <int DIST>
+static void prep_fast_launch(const float* Xin, int64_t rows, int d, int d_pad, int guard,
+                             float* norms, float* scales, void* Xl, unsigned long long* census,
+                             float* Xout, const double* shift, const double* scale,
+                             cudaStream_t s) {
+    using L = typename low_type<DIST>::T;
+    const int g = grid_for(rows * 8, 256, 8);
+    // d_pad columns of Xl must be covered by the lane's Q slots too
+    const int w = d_pad > d ? d_pad : d;
+    if (w <= 128) {
+        if (shift)
+            prep_fast_kernel<DIST, true, 4, 4><<<g, 256, 0, s>>>(Xin, rows, d, d_pad, guard, norms,
+                                                                 scales, (L*)Xl, census, Xout, shift, scale);
+        else
+            prep_fast_kernel<DIST, false, 4, 4><<<g, 256, 0, s>>>(Xin, rows, d, d_pad, guard, norms,
+                                                                  scales, (L*)Xl, census, Xout, shift, scale);
+    } else {
+        if (shift)
+            prep_fast_kernel<DIST, true, 8, 2><<<g, 256, 0, s>>>(Xin, rows, d, d_pad, guard, norms,
+                                                                 scales, (L*)Xl, census, Xout, shift, scale);
+        else
+            prep_fast_kernel<DIST, false, 8, 2><<<g, 256, 0, s>>>(Xin, rows, d, d_pad, guard, norms,
+                                                                  scales, (L*)Xl, census, Xout, shift, scale);
+    }
 }
 
 template <typename W>
@@ -376,6 +569,29 @@ static cudaError_t prep_dispatch(int dist, const W* X, int64_t rows, int d, int 
             break;
         default:
             return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+bool prep_fast_ok(int work, int d) { return work == KMEANS_FP32 && d <= 256; }
+// (d_pad <= 256 as well: tc_dpad / the SIMT paddings never exceed 256 when d <= 256)
+
+cudaError_t launch_prep_fast(int dist, const void* Xin, int64_t rows, int d, int d_pad, int guard,
+                             void* norms, void* scales, void* Xl, unsigned long long* census,
+                             void* Xout, const double* shift, const double* scale,
+                             cudaStream_t s) {
+    launches_add(1);
+    if (rows <= 0) return cudaSuccess;
+    const float* xi = (const float*)Xin;
+    float* xo = (float*)Xout;
+    float* nr = (float*)norms;
+    float* sc = (float*)scales;
+    switch (dist) {
+        case KMEANS_FP32: prep_fast_launch<KMEANS_FP32>(xi, rows, d, d_pad, guard, nr, sc, Xl, census, xo, shift, scale, s); break;
+        case KMEANS_FP16: prep_fast_launch<KMEANS_FP16>(xi, rows, d, d_pad, guard, nr, sc, Xl, census, xo, shift, scale, s); break;
+        case KMEANS_BF16: prep_fast_launch<KMEANS_BF16>(xi, rows, d, d_pad, guard, nr, sc, Xl, census, xo, shift, scale, s); break;
+        case KMEANS_E5M2: prep_fast_launch<KMEANS_E5M2>(xi, rows, d, d_pad, guard, nr, sc, Xl, census, xo, shift, scale, s); break;
+        default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
 }

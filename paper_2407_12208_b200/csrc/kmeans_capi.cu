@@ -304,9 +304,10 @@ int stage_rows(kmeans_ctx* h, const void* src, int64_t rows, void* dst) {
     return 0;
 }
 
-// Normalise X (already staged in h->Xw) in place; computes shift/scale from it (globally
-// across ranks when sharded: the per-feature aggregates are allreduced).
-int normalise_points(kmeans_ctx* h, int64_t rows) {
+// Normalisation statistics (shift/scale) of the rows at Xsrc (the caller's device buffer or the
+// staged copy), globally across ranks when sharded (the per-feature aggregates are allreduced).
+// The transform itself is applied by the fused prep (launch_prep_norm).
+int normalise_stats(kmeans_ctx* h, const void* Xsrc, int64_t rows) {
     if (h->norm == KMEANS_NORM_NONE) return 0;
     cudaStream_t s = h->stream;
     int nb = norm_stats_blocks(rows, h->d);
@@ -319,12 +320,12 @@ int normalise_points(kmeans_ctx* h, int64_t rows) {
         CK(cudaMemcpyAsync(&n_total, tmp, sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
     }
-    CK(launch_norm_stats(h->work, h->norm, h->Xw, rows, h->d, h->partials, nb, h->shift,
+    CK(launch_norm_stats(h->work, h->norm, Xsrc, rows, h->d, h->partials, nb, h->shift,
                          h->scale, s));
     if (h->norm == KMEANS_NORM_ZSCORE) {
         if (h->comm) CKN(ncclAllReduce(h->shift, h->shift, h->d, ncclDouble, ncclSum, h->comm, s));
         CK(launch_norm_post(0, h->d, n_total, h->shift, h->scale, s));
-        CK(launch_norm_ssq(h->work, h->Xw, rows, h->d, h->partials, nb, h->shift, h->scale, s));
+        CK(launch_norm_ssq(h->work, Xsrc, rows, h->d, h->partials, nb, h->shift, h->scale, s));
         if (h->comm) CKN(ncclAllReduce(h->scale, h->scale, h->d, ncclDouble, ncclSum, h->comm, s));
         CK(launch_norm_post(1, h->d, n_total, h->shift, h->scale, s));
     } else {
@@ -334,7 +335,6 @@ int normalise_points(kmeans_ctx* h, int64_t rows) {
         }
         CK(launch_norm_post(2, h->d, n_total, h->shift, h->scale, s));
     }
-    CK(launch_norm_apply(h->work, h->Xw, rows, h->d, h->shift, h->scale, s));
     return 0;
 }
 
@@ -521,16 +521,29 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
 
     CK(cudaEventRecord(e0, s));
     // ---- A1: stage + normalise X and C0 -------------------------------------------------
-    if (int rc = stage_rows(h, X, n, h->Xw)) return rc;
+    // A device X is read in place by the statistics and the (out-of-place) normalisation, so it
+    // is never copied; a host X is staged into Xw first (that copy is needed anyway).
+    const bool norm = h->norm != KMEANS_NORM_NONE;
+    const void* Xsrc = h->Xw;
+    if (norm && is_device_ptr(X)) Xsrc = X;
+    else if (int rc = stage_rows(h, X, n, h->Xw)) return rc;
     if (int rc = stage_rows(h, C0, k, h->Cw)) return rc;
-    if (h->norm != KMEANS_NORM_NONE) {
-        if (int rc = normalise_points(h, n)) return rc;
+    if (norm) {
+        if (int rc = normalise_stats(h, Xsrc, n)) return rc;
         CK(launch_norm_apply(h->work, h->Cw, k, d, h->shift, h->scale, s));
     }
-    // ---- A2: point prep (norms, guard scales, low operands) -----------------------------
+    // ---- A2: point prep (norms, guard scales, low operands), fused with the normalisation
+    // on the fast path --------------------------------------------------------------------
     CK(cudaMemsetAsync(h->census, 0, 4 * sizeof(unsigned long long), s));
-    CK(launch_prep(h->work, h->dist, h->Xw, n, d, h->d_pad, h->guard, h->xn, h->sx, h->Xl,
-                   h->census, s));
+    if (prep_fast_ok(h->work, d)) {
+        CK(launch_prep_fast(h->dist, Xsrc, n, d, h->d_pad, h->guard, h->xn, h->sx, h->Xl,
+                            h->census, norm ? h->Xw : nullptr, norm ? h->shift : nullptr,
+                            norm ? h->scale : nullptr, s));
+    } else {
+        if (norm) CK(launch_norm_apply(h->work, h->Xw, n, d, h->shift, h->scale, s, Xsrc));
+        CK(launch_prep(h->work, h->dist, h->Xw, n, d, h->d_pad, h->guard, h->xn, h->sx, h->Xl,
+                       h->census, s));
+    }
     CK(cudaMemsetAsync(h->labels, 0xff, (size_t)n * sizeof(int32_t), s));   // labels_prev = -1
     CK(cudaMemsetAsync(h->trace, 0, sizeof(IterRec) * KMEANS_MAX_TRACE, s));
     CK(cudaEventRecord(e1, s));
@@ -699,11 +712,19 @@ int kmeans_assign(kmeans_handle h, const void* X, int64_t m, int32_t* labels, do
     for (int64_t r0 = 0; r0 < m; r0 += h->n) {
         int64_t rows = std::min<int64_t>(h->n, m - r0);
         const char* src = (const char*)X + (size_t)r0 * h->d * h->wsize;
-        if (int rc = stage_rows(h, src, rows, h->Xw)) return rc;
-        if (h->norm != KMEANS_NORM_NONE)
-            CK(launch_norm_apply(h->work, h->Xw, rows, h->d, h->shift, h->scale, s));
-        CK(launch_prep(h->work, h->dist, h->Xw, rows, h->d, h->d_pad, h->guard, h->xn, h->sx,
-                       h->Xl, nullptr, s));
+        const bool norm = h->norm != KMEANS_NORM_NONE;
+        const void* Xsrc = h->Xw;
+        if (norm && is_device_ptr(src)) Xsrc = src;      // normalised out of place, no copy
+        else if (int rc = stage_rows(h, src, rows, h->Xw)) return rc;
+        if (prep_fast_ok(h->work, h->d)) {
+            CK(launch_prep_fast(h->dist, Xsrc, rows, h->d, h->d_pad, h->guard, h->xn, h->sx,
+                                h->Xl, nullptr, norm ? h->Xw : nullptr, norm ? h->shift : nullptr,
+                                norm ? h->scale : nullptr, s));
+        } else {
+            if (norm) CK(launch_norm_apply(h->work, h->Xw, rows, h->d, h->shift, h->scale, s, Xsrc));
+            CK(launch_prep(h->work, h->dist, h->Xw, rows, h->d, h->d_pad, h->guard, h->xn, h->sx,
+                           h->Xl, nullptr, s));
+        }
         CK(cudaMemsetAsync(h->sse_dev, 0, sizeof(double), s));
         if (h->dist_kernel == DK_SMALLD) {
             Problem p{rows, h->d, h->k, h->d_pad, h->guard};
