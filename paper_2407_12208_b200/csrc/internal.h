@@ -141,7 +141,7 @@ cudaError_t launch_gather_rows(const void* src, int row_bytes, const int* rows, 
 cudaError_t launch_cand_exact(const float* Xw, const float* Cw, const float* cn, int d,
                               const int* rows, int nr, const int* cand_cnt, const int* cand,
                               int cand_q, int32_t* labels, int* left_count, int* left_rows,
-                              cudaStream_t s);
+                              unsigned long long* keys, cudaStream_t s);
 
 // K7: update = bucket by label (count, scan, scatter) + segmented fp64 sums.
 cudaError_t launch_update(int work, const void* Xw, int64_t n, int d, int k,

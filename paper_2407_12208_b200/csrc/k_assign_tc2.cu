@@ -69,6 +69,7 @@ MPK_DEV void cand32(const uint32_t (&v)[32], const float* cn_s, const float* sc_
                     int j0, float T, int* cnt, int* cand, int Q) {
     const uint32_t cn_a = smem_u32(cn_s + j0);
     const uint32_t sc_a = smem_u32(sc_s + j0);
+    uint32_t hits = 0;
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
         const float4 cc = lds_f4(cn_a + 16 * e);
@@ -81,11 +82,15 @@ MPK_DEV void cand32(const uint32_t (&v)[32], const float* cn_s, const float* sc_
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const float x = fmaf(__uint_as_float(v[4 * e + u]), s[u], cnv[u]);
-            if (x <= T) {
-                const int sl = atomicAdd(cnt, 1);
-                if (sl < Q) cand[sl] = j0 + 4 * e + u;
-            }
+            hits |= (x <= T ? 1u : 0u) << (4 * e + u);
         }
+    }
+    // append the (rare) hits after the chunk: one divergent loop instead of a branch per column
+    while (hits) {
+        const int b = __ffs(hits) - 1;
+        hits &= hits - 1;
+        const int sl = atomicAdd(cnt, 1);
+        if (sl < Q) cand[sl] = j0 + b;
     }
 }
 

@@ -71,6 +71,7 @@ struct kmeans_ctx {
     int* cand_cnt = nullptr;
     int* cand = nullptr;           // [cap][kCandQ]
     int* cand_left = nullptr;      // rows left for the full CUDA-core evaluation
+    unsigned long long* cand_key = nullptr;   // per row: min (value, column) key
     int dist_kernel = 0;
     AccLayout L{0, 0};
 
@@ -157,7 +158,7 @@ void free_all(kmeans_ctx* h) {
     if (h->tc) tc_plan_destroy(h->tc);
     if (h->fin) tc_plan_destroy(h->fin);
     void* fin_bufs[] = {h->fin_Xl, h->fin_Cl, h->fin_sx, h->fin_sc, h->fbc, h->fb_thr,
-                        h->cand_X, h->cand_sx, h->cand_cnt, h->cand, h->cand_left};
+                        h->cand_X, h->cand_sx, h->cand_cnt, h->cand, h->cand_left, h->cand_key};
     for (void* b : fin_bufs)
         if (b) cudaFree(b);
     void* bufs[] = {h->Xw, h->xl_alias ? nullptr : h->Xl, h->xn, h->sx, h->Cw, h->Cl, h->cn,
@@ -461,11 +462,12 @@ int final_assign(kmeans_ctx* h, const Problem& pf) {
             // candidate path (R2): gather the uncertified rows' operands, list their
             // candidate columns on the tensor cores, evaluate only those exactly in fp32
             if (nfb > h->cand_cap) {
-                void* old[] = {h->cand_X, h->cand_sx, h->cand_cnt, h->cand, h->cand_left};
+                void* old[] = {h->cand_X, h->cand_sx, h->cand_cnt, h->cand, h->cand_left, h->cand_key};
                 for (void* b : old)
                     if (b) cudaFree(b);
                 h->cand_X = h->cand_sx = nullptr;
                 h->cand_cnt = h->cand = h->cand_left = nullptr;
+                h->cand_key = nullptr;
                 const int64_t cap = std::min<int64_t>(n, (int64_t)nfb + nfb / 4 + 1024);
                 int rb = 0;
                 tc_plan_operands(plan, &rb);
@@ -474,6 +476,7 @@ int final_assign(kmeans_ctx* h, const Problem& pf) {
                 CK(cudaMalloc(&h->cand_cnt, (size_t)cap * 4));
                 CK(cudaMalloc(&h->cand, (size_t)cap * kCandQ * 4));
                 CK(cudaMalloc(&h->cand_left, (size_t)cap * 4));
+                CK(cudaMalloc(&h->cand_key, (size_t)cap * 8));
                 h->cand_cap = cap;
             }
             int rb = 0;
@@ -483,9 +486,19 @@ int final_assign(kmeans_ctx* h, const Problem& pf) {
             CK(cudaMemsetAsync(h->cand_cnt, 0, (size_t)nfb * 4, s));
             CK(launch_cand_tc(plan, h->cand_X, nfb, fguard, h->cand_sx, (const float*)h->cn,
                               (const float*)fx_sc, h->fb_thr, h->cand_cnt, h->cand, kCandQ, s));
+            if (getenv("MPK_CAND_STATS")) {   // debug: candidate count distribution
+                std::vector<int> cc(nfb);
+                CK(cudaMemcpyAsync(cc.data(), h->cand_cnt, (size_t)nfb * 4, cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                long long tot = 0;
+                int mx = 0, over = 0;
+                for (int v : cc) { tot += v; mx = std::max(mx, v); over += v > kCandQ; }
+                fprintf(stderr, "[cand] rows %d candidates %lld mean %.2f max %d overflow %d\n", nfb,
+                        tot, (double)tot / nfb, mx, over);
+            }
             CK(launch_cand_exact((const float*)h->Xw, (const float*)h->Cw, (const float*)h->cn, d,
                                  h->perm, nfb, h->cand_cnt, h->cand, kCandQ, h->labels,
-                                 h->fbc + 1, h->cand_left, s));
+                                 h->fbc + 1, h->cand_left, h->cand_key, s));
             int nleft = 0;
             CK(cudaMemcpyAsync(&nleft, h->fbc + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));

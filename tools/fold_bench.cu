@@ -10,51 +10,60 @@
 using namespace mpk::tcdev;
 
 template <int MODE>
-__global__ void __launch_bounds__(256, 1) k(int iters, unsigned long long* out, float* sink) {
+__global__ void __launch_bounds__(512, 1) k(int iters, unsigned long long* out, float* sink) {
     __shared__ __align__(16) float cn_s[1024];
     for (int j = threadIdx.x; j < 1024; j += blockDim.x) cn_s[j] = 0.5f * j;
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    uint32_t va[32];
-    for (int e = 0; e < 32; ++e) va[e] = __float_as_uint(lane * 0.25f + e);
-    float cv[NCH], cs[NCH], c2[NCH];
+    uint32_t va[32], vb[32];
+    for (int e = 0; e < 32; ++e) { va[e] = __float_as_uint(lane * 0.25f + e); vb[e] = va[e] ^ 3; }
+    float cv[NCH], cs[NCH], c2[NCH], cv2[NCH], cs2_[NCH], c22[NCH];
     chains_init(cv, cs, c2);
-    uint64_t s2[NCH / 2];
-    for (int m = 0; m < NCH / 2; ++m) s2[m] = pack2(-1.f, -1.f);
+    chains_init(cv2, cs2_, c22);
+    uint64_t s2[NCH / 2], s22[NCH / 2];
+    for (int m = 0; m < NCH / 2; ++m) { s2[m] = pack2(-1.f, -1.f); s22[m] = s2[m]; }
     const unsigned long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
         const int j0 = (i * 32) & 1023;
-        if (MODE == 0) fold32_x2<false>(va, cn_s, cn_s, -2.f, j0, cv, s2);
-        else fold32<false, false>(va, cn_s, cn_s, -2.f, j0, cv, cs, c2);
-        va[0] ^= 1;   // keep the data live / varying
+        if (MODE == 0 || MODE == 2) fold32_x2<false>(va, cn_s, cn_s, -2.f, j0, cv, s2);
+        else if (MODE == 1) fold32<false, false>(va, cn_s, cn_s, -2.f, j0, cv, cs, c2);
+        else {   // MODE 3: two chunks interleaved into two independent chain sets
+            fold32_x2<false>(va, cn_s, cn_s, -2.f, j0, cv, s2);
+            fold32_x2<false>(vb, cn_s, cn_s, -2.f, (j0 + 32) & 1023, cv2, s22);
+            ++i;
+        }
+        va[0] ^= (uint32_t)i; vb[1] ^= (uint32_t)i; va[17] += 1u; vb[29] += 3u;   // keep the data live / varying
     }
     const unsigned long long t1 = clock64();
     float acc = 0.f;
-    for (int c = 0; c < NCH; ++c) acc += cv[c] + cs[c];
-    for (int m = 0; m < NCH / 2; ++m) acc += __uint_as_float((uint32_t)s2[m]);
-    sink[blockIdx.x * 256 + threadIdx.x] = acc;
+    for (int c = 0; c < NCH; ++c) acc += cv[c] + cs[c] + cv2[c];
+    for (int m = 0; m < NCH / 2; ++m) acc += __uint_as_float((uint32_t)s2[m]) + __uint_as_float((uint32_t)s22[m]);
+    sink[blockIdx.x * 512 + threadIdx.x] = acc;
     if (lane == 0) atomicAdd(out, t1 - t0);
 }
 
 template <int MODE>
-void run(const char* nm) {
+void run(const char* nm, int threads = 256) {
     unsigned long long* d;
     float* sink;
     cudaMalloc(&d, 8);
-    cudaMalloc(&sink, 148 * 256 * 4);
+    cudaMalloc(&sink, 148 * 512 * 4);
     cudaMemset(d, 0, 8);
     const int iters = 20000;
-    k<MODE><<<148, 256>>>(iters, d, sink);
+    k<MODE><<<148, threads>>>(iters, d, sink);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return; }
     unsigned long long c;
     cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
-    printf("%-28s %.1f cycles per 32-column chunk per warp (alu model 128, 2 warps/SMSP)\n", nm,
-           (double)c / (148.0 * 8) / iters);
+    const double per_warp = (double)c / (148.0 * (threads / 32)) / iters;
+    const double per_smsp_chunk = per_warp / ((threads / 32) / 4) / (MODE == 3 ? 2 : 1);
+    printf("%-36s %.1f cycles per chunk per SMSP (alu floor 128)\n", nm, per_smsp_chunk);
 }
 
 int main() {
-    run<0>("fold32_x2 (FFMA2)");
-    run<1>("fold32 (scalar)");
+    run<0>("fold32_x2, 2 warps/SMSP");
+    run<1>("fold32 scalar, 2 warps/SMSP");
+    run<2>("fold32_x2, 4 warps/SMSP", 512);
+    run<3>("fold32_x2 x2 interleaved, 2 warps/SMSP");
     return 0;
 }

@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
+#include "tc_common.cuh"
 
 template <int MODE>
 __global__ void __launch_bounds__(256, 1) k(int iters, unsigned long long* out, float* sink) {
@@ -46,6 +47,23 @@ __global__ void __launch_bounds__(256, 1) k(int iters, unsigned long long* out, 
                 uint64_t a2 = ((uint64_t)__float_as_uint(b) << 32) | __float_as_uint(a), d2;
                 asm volatile("fma.rn.f32x2 %0, %1, %2, %1;" : "=l"(d2) : "l"(a2), "l"(0xC0000000C0000000ull));
                 a = __uint_as_float((uint32_t)d2); b = __uint_as_float((uint32_t)(d2 >> 32));
+            } else if (MODE == 9) {   // 1 FFMA2 + 2 FMNMX (the fold's pipe mix without FSET)
+                uint64_t a2 = ((uint64_t)__float_as_uint(b) << 32) | __float_as_uint(a), d2;
+                asm volatile("fma.rn.f32x2 %0, %1, %2, %1;" : "=l"(d2) : "l"(a2), "l"(0xC0000000C0000000ull));
+                const float lo = __uint_as_float((uint32_t)d2), hi = __uint_as_float((uint32_t)(d2 >> 32));
+                a = fminf(a, lo);
+                b = fminf(b, hi);
+            } else if (MODE == 10) {  // 1 FFMA (imm) + 2 FMNMX
+                const float lo = fmaf(a, -2.0f, b);
+                a = fminf(a, lo);
+                b = fminf(b, lo + 1.0f);
+            } else if (MODE == 11) {  // the fold's chain update on two chains (chain_step_x2)
+                // per element pair: FFMA2 x, 2 FSET, 2 FMNMX, FFMA2 s
+                static_assert(true, "");
+                uint64_t acc2 = ((uint64_t)__float_as_uint(x + e) << 32) | __float_as_uint(x - e);
+                mpk::tcdev::chain_step_x2(acc2, 0x3F8000003F800000ull, 0xC0000000C0000000ull,
+                                          v[e & 7], v[(e + 1) & 7], *reinterpret_cast<uint64_t*>(&s[(e & 3) * 2]),
+                                          0xBF800000BF800000ull);
             } else if (MODE == 5) {   // SEL int
                 int ia = __float_as_int(a), ib = __float_as_int(b);
                 ia = (ia & 1) ? ib : ia;
@@ -89,5 +107,8 @@ int main() {
     run<6>("FSET + FMNMX + FADD");
     run<7>("FSET + FMNMX + FMNMX");
     run<8>("FFMA2 (per 2 fp32)");
+    run<9>("FFMA2 + 2 FMNMX");
+    run<10>("FFMA imm + FADD + 2 FMNMX");
+    run<11>("chain_step_x2 (2 columns)");
     return 0;
 }
