@@ -447,6 +447,62 @@ __global__ void final_sse_kernel(const W* __restrict__ X, int64_t n, int d,
     }
 }
 
+// fp32, d <= 32 * TQ: the same sums in the same order as final_sse_kernel<float>, with every
+// load of the RW rows issued before the arithmetic (the runtime-length column loop issued one
+// column step's loads at a time: four HBM round trips per row group at d = 128).
+template <int TQ>
+__global__ void final_sse_fast_kernel(const float* __restrict__ X, int64_t n, int d,
+                                      const float* __restrict__ C,
+                                      const int32_t* __restrict__ labels,
+                                      double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    constexpr int RW = 4;
+    double acc = 0.0;
+    for (int64_t i0 = warp * RW; i0 < n; i0 += nwarps * RW) {
+        int lab[RW];
+#pragma unroll
+        for (int r = 0; r < RW; ++r) lab[r] = (i0 + r < n) ? labels[i0 + r] : 0;
+        float xv[TQ][RW], cv[TQ][RW];
+#pragma unroll
+        for (int q = 0; q < TQ; ++q) {
+            const int t = lane + 32 * q;
+#pragma unroll
+            for (int r = 0; r < RW; ++r) {
+                const bool ok = i0 + r < n && t < d;
+                xv[q][r] = ok ? X[(i0 + r) * d + t] : 0.0f;
+                cv[q][r] = ok ? C[(int64_t)lab[r] * d + t] : 0.0f;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < TQ; ++q) {
+            if (lane + 32 * q >= d) break;
+            float s = 0.0f, comp = 0.0f;
+#pragma unroll
+            for (int r = 0; r < RW; ++r) {
+                const float df = xv[q][r] - cv[q][r];
+                const float p2 = df * df;
+                const float e2 = fmaf(df, df, -p2);
+                const float t = s + p2;
+                const float z = t - s;
+                comp += (s - (t - z)) + (p2 - z) + e2;
+                s = t;
+            }
+            acc += (double)s + (double)comp;
+        }
+    }
+    acc = warp_sum(acc);
+    __shared__ double red[8];
+    if (lane == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += red[w];
+        atomicAdd(out, a);
+    }
+}
+
 template <typename LT, typename W>
 cudaError_t simt_dispatch_acc(int dist, const Problem& p, const void* Xl, const void* xn,
                               const void* sx, const void* Cl, const void* cn, const void* sc,
@@ -556,6 +612,14 @@ cudaError_t launch_final_sse(int work, const void* Xw, int64_t n, int d, const v
     if (work == KMEANS_FP64)
         final_sse_kernel<double><<<grid, 256, 0, s>>>((const double*)Xw, n, d, (const double*)Cw,
                                                      labels, sse_out);
+    else if (d <= 32)
+        final_sse_fast_kernel<1><<<grid, 256, 0, s>>>((const float*)Xw, n, d, (const float*)Cw, labels, sse_out);
+    else if (d <= 64)
+        final_sse_fast_kernel<2><<<grid, 256, 0, s>>>((const float*)Xw, n, d, (const float*)Cw, labels, sse_out);
+    else if (d <= 128)
+        final_sse_fast_kernel<4><<<grid, 256, 0, s>>>((const float*)Xw, n, d, (const float*)Cw, labels, sse_out);
+    else if (d <= 256)
+        final_sse_fast_kernel<8><<<grid, 256, 0, s>>>((const float*)Xw, n, d, (const float*)Cw, labels, sse_out);
     else
         final_sse_kernel<float><<<grid, 256, 0, s>>>((const float*)Xw, n, d, (const float*)Cw,
                                                     labels, sse_out);
