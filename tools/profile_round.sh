@@ -14,7 +14,7 @@ if [ $rc -eq 0 ]; then
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${tag}_launches.csv \
       timeout 1200 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/${tag}_ncu_launch.log 2>&1
   echo "launch list rc=$?"
-  ncu --set full --import-source on --clock-control none -k regex:assign_pair_kernel --launch-skip 3 -c 1 \
+  ncu --set full --import-source on --clock-control none -k regex:assign_pair_kernel --launch-skip 4 -c 1 \
       -o gpurun_out/${tag}_pair_full timeout 900 python bench.py --steps 1 --warmup 3 --iters 2 --no-cpu-baseline --no-e2e \
       > gpurun_out/${tag}_ncu_full.log 2>&1
   echo "full capture rc=$?"
