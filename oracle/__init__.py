@@ -50,9 +50,10 @@ def _load():
             lib.oracle_normalize_stats.argtypes = [i32, i64, i32, P, P, P]
             lib.oracle_normalize_apply.argtypes = [i32, i64, i32, P, P, P, P]
             lib.oracle_fit.argtypes = [i64, i32, i32, i32, i32, i32, P, P, i32, dbl, P, P, P, P,
-                                       P, P, P, P, P, P]
-            lib.oracle_step.argtypes = [i64, i32, i32, i32, i32, i32, P, P, P, P, P, P, P, P]
-            lib.oracle_assign.argtypes = [i64, i32, i32, i32, i32, i32, P, P, P, P, P]
+                                       P, P, P, P, P, P, dbl, P]
+            lib.oracle_step.argtypes = [i64, i32, i32, i32, i32, i32, P, P, P, P, P, P, P, P,
+                                        dbl, P]
+            lib.oracle_assign.argtypes = [i64, i32, i32, i32, i32, i32, P, P, P, P, P, dbl, P]
             lib.oracle_prep.argtypes = [i64, i32, i32, i32, i32, P, P, P, P]
             lib.oracle_final.argtypes = [i64, i32, i32, i32, P, P, P, P]
             lib.oracle_num_threads.restype = i32
@@ -121,9 +122,12 @@ def apply_normalization(X, shift, scale, work="fp64"):
     return out
 
 
-def fit(X, C0, work="fp64", dist="fp64", norm="none", guard=False, max_iter=300, tol=1e-4):
+def fit(X, C0, work="fp64", dist="fp64", norm="none", guard=False, max_iter=300, tol=1e-4,
+        delta=None):
     """Full Lloyd run (O1..O9). Returns a dict with labels, centroids, sse, iters, shift,
-    scale and per-iteration traces (sse_t, changed_t, shift2_t, empty_t)."""
+    scale and per-iteration traces (sse_t, changed_t, shift2_t, empty_t). delta >= 1 runs Alg 5
+    (Alg 4's per-pair precision switch, O4m); n_low counts the triggered low-precision pairs
+    over all iterations (eta = n_low / (iters * n * k))."""
     lib = _load()
     X, C0 = _f64(X), _f64(C0)
     n, d = X.shape
@@ -135,19 +139,21 @@ def fit(X, C0, work="fp64", dist="fp64", norm="none", guard=False, max_iter=300,
     shift, scale = np.empty(d), np.empty(d)
     tr_sse, tr_ch = np.zeros(max_iter), np.zeros(max_iter, np.int64)
     tr_sh, tr_em = np.zeros(max_iter), np.zeros(max_iter, np.int32)
+    n_low = ct.c_int64()
     rc = lib.oracle_fit(n, d, k, _prec(work), _prec(dist), _flags(norm, guard), _p(X), _p(C0),
                         max_iter, tol, _p(labels), _p(cent), ct.byref(sse), ct.byref(iters),
-                        _p(shift), _p(scale), _p(tr_sse), _p(tr_ch), _p(tr_sh), _p(tr_em))
+                        _p(shift), _p(scale), _p(tr_sse), _p(tr_ch), _p(tr_sh), _p(tr_em),
+                        float(delta or 0.0), ct.byref(n_low))
     if rc != 0:
         raise ValueError(f"oracle_fit rc={rc}")
     it = iters.value
     return dict(labels=labels, centroids=cent, sse=sse.value, iters=it, shift=shift,
                 scale=scale, sse_t=tr_sse[:it], changed_t=tr_ch[:it], shift2_t=tr_sh[:it],
-                empty_t=tr_em[:it])
+                empty_t=tr_em[:it], n_low=n_low.value)
 
 
-def step(X, C, work="fp32", dist="fp16", guard=False):
-    """One teacher-forced step (O3..O7) on normalised X from centroids C."""
+def step(X, C, work="fp32", dist="fp16", guard=False, delta=None):
+    """One teacher-forced step (O3..O7) on normalised X from centroids C (delta: O4m)."""
     lib = _load()
     X, Cc = _f64(X), _f64(C)
     n, d = X.shape
@@ -157,24 +163,32 @@ def step(X, C, work="fp32", dist="fp16", guard=False):
     sums = np.empty((k, d))
     counts = np.empty(k, np.int64)
     cnext = np.empty((k, d))
+    n_low = ct.c_int64()
     rc = lib.oracle_step(n, d, k, _prec(work), _prec(dist), int(guard), _p(X), _p(Cc),
-                         _p(labels), _p(dmin), _p(d2), _p(sums), _p(counts), _p(cnext))
+                         _p(labels), _p(dmin), _p(d2), _p(sums), _p(counts), _p(cnext),
+                         float(delta or 0.0), ct.byref(n_low))
     if rc != 0:
         raise ValueError(f"oracle_step rc={rc}")
-    return dict(labels=labels, dmin=dmin, d2nd=d2, sums=sums, counts=counts, centroids=cnext)
+    return dict(labels=labels, dmin=dmin, d2nd=d2, sums=sums, counts=counts, centroids=cnext,
+                n_low=n_low.value)
 
 
-def assign(X, C, work="fp32", dist="fp16", guard=False):
-    """Low-precision assignment (O2..O5): labels, best and second-best expanded distance."""
+def assign(X, C, work="fp32", dist="fp16", guard=False, delta=None, return_n_low=False):
+    """Low-precision assignment (O2..O5; O4m with delta): labels, best and second-best expanded
+    distance (and the number of triggered low-precision pairs if return_n_low)."""
     lib = _load()
     X, Cc = _f64(X), _f64(C)
     n, d = X.shape
     labels = np.empty(n, np.int32)
     dmin, d2 = np.empty(n), np.empty(n)
+    n_low = ct.c_int64()
     rc = lib.oracle_assign(n, d, Cc.shape[0], _prec(work), _prec(dist), int(guard), _p(X),
-                           _p(Cc), _p(labels), _p(dmin), _p(d2))
+                           _p(Cc), _p(labels), _p(dmin), _p(d2), float(delta or 0.0),
+                           ct.byref(n_low))
     if rc != 0:
         raise ValueError(f"oracle_assign rc={rc}")
+    if return_n_low:
+        return labels, dmin, d2, n_low.value
     return labels, dmin, d2
 
 

@@ -171,27 +171,54 @@ static void prep_vector(int work, int dist, int guard, int d, const double* p, d
 /*   accumulation": every product of two fp16/bf16/E5M2/fp32 values is exact in fp64).       */
 /*   argmin: scan j = 0..k-1, strict '<' from best = +inf, label 0: lowest index on ties,     */
 /*   NaN never wins, an all-NaN/+inf row keeps label 0 (readings Z12, Z13).                  */
+/* O4m (Alg 4; used by Alg 5 step 3), when delta2 = delta^2  */
+/* is > 0: per pair, condition eq:prec-delta                              */
+/*     max(x^T x / c^T c, c^T c / x^T x) >= delta^2                                          */
+/* is evaluated without the division, as max(xn, cn_j) >= delta^2 * min(xn, cn_j) in fp64    */
+/* (reading R5; any NaN norm makes it false; xn = cn_j = 0 makes it true). If it holds, D_ij  */
+/* is the scaled low-precision formula above (Alg 4 lines 1-6; the scaling s = ||.||_inf is   */
+/* always on in this mode); otherwise D_ij = x^T x - 2 x^T c_j + c^T c with the dot product  */
+/* of the working-precision values (Alg 4 line 8), accumulated in fp64. *n_trig counts the   */
+/* triggered pairs (eq:xi-low-prec-ratio's numerator).                     */
 /* ---------------------------------------------------------------------------------------- */
-static void assign_point(int d, int k, const double* xl, double xn, double sx, const double* Cl,
-                         const double* cn, const double* sc, int32_t* label, double* dmin,
+static void assign_point(int d, int k, const double* x, const double* xl, double xn, double sx,
+                         const double* C, const double* Cl, const double* cn, const double* sc,
+                         double delta2, int64_t* n_trig, int32_t* label, double* dmin,
                          double* d2nd) {
     double best = INFINITY, second = INFINITY;
     int32_t lab = 0;
+    int64_t trig_count = 0;
     for (int j = 0; j < k; ++j) {
-        double dot = 0.0;
-        for (int t = 0; t < d; ++t) dot += xl[t] * Cl[(int64_t)j * d + t];
-        double D = xn - 2.0 * (sx * sc[j]) * dot + cn[j];
+        int trig = 1;
+        if (delta2 > 0.0) {
+            const double a = xn, b = cn[j];
+            const double mx = (a > b) ? a : b, mn = (a > b) ? b : a;
+            trig = mx >= delta2 * mn;
+        }
+        double D;
+        if (trig) {
+            double dot = 0.0;
+            for (int t = 0; t < d; ++t) dot += xl[t] * Cl[(int64_t)j * d + t];
+            D = xn - 2.0 * (sx * sc[j]) * dot + cn[j];
+            trig_count++;
+        } else {
+            double dot = 0.0;
+            for (int t = 0; t < d; ++t) dot += x[t] * C[(int64_t)j * d + t];
+            D = xn - 2.0 * dot + cn[j];
+        }
         if (D < best) { second = best; best = D; lab = j; }
         else if (D < second) second = D;
     }
     *label = lab;
     *dmin = best;
     if (d2nd) *d2nd = second;
+    if (n_trig) *n_trig = trig_count;
 }
 
 /* Handle-free state for one run. */
 typedef struct {
     int64_t n; int d, k, work, dist, guard;
+    double delta2;                /* Alg 4's delta^2; 0: every pair in low precision (Alg 3)  */
     double *X, *Xl, *xn, *sx;     /* normalised X (work), low operands, norms, scales */
     double *C, *Cl, *cn, *sc;     /* centroids (work), low operands, norms, scales   */
 } ostate_t;
@@ -207,12 +234,17 @@ static void prep_centroids(ostate_t* S) {
                     &S->sc[j], S->Cl + (int64_t)j * S->d);
 }
 
-static void assign_all(ostate_t* S, int32_t* labels, double* dmin, double* d2nd) {
-    int64_t n = S->n;
-#pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < n; ++i)
-        assign_point(S->d, S->k, S->Xl + i * S->d, S->xn[i], S->sx[i], S->Cl, S->cn, S->sc,
-                     &labels[i], &dmin[i], d2nd ? &d2nd[i] : NULL);
+static int64_t assign_all(ostate_t* S, int32_t* labels, double* dmin, double* d2nd) {
+    int64_t n = S->n, trig = 0;
+#pragma omp parallel for schedule(static) reduction(+ : trig)
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t t = 0;
+        assign_point(S->d, S->k, S->X + i * S->d, S->Xl + i * S->d, S->xn[i], S->sx[i], S->C,
+                     S->Cl, S->cn, S->sc, S->delta2, &t, &labels[i], &dmin[i],
+                     d2nd ? &d2nd[i] : NULL);
+        trig += t;
+    }
+    return trig;
 }
 
 /* O7: sums (compensated fp64 in index order), counts, means rounded to u; empty -> keep.     */
@@ -289,6 +321,7 @@ static double final_pass(ostate_t* S, int32_t* labels) {
 static int alloc_state(ostate_t* S, int64_t n, int d, int k, int work, int dist, int guard) {
     memset(S, 0, sizeof(*S));
     S->n = n; S->d = d; S->k = k; S->work = work; S->dist = dist; S->guard = guard;
+    S->delta2 = 0.0;
     S->X = (double*)malloc(sizeof(double) * n * d);
     S->Xl = (double*)malloc(sizeof(double) * n * d);
     S->xn = (double*)malloc(sizeof(double) * n);
@@ -302,6 +335,17 @@ static int alloc_state(ostate_t* S, int64_t n, int d, int k, int work, int dist,
 static void free_state(ostate_t* S) {
     free(S->X); free(S->Xl); free(S->xn); free(S->sx);
     free(S->C); free(S->Cl); free(S->cn); free(S->sc);
+}
+
+/* Alg 4 mode: delta >= 1 sets delta^2 and turns the infinity-norm scaling on (Alg 4 lines 1-5);
+   delta <= 0 leaves Alg 3 (every pair in low precision, scaling as the flags say). */
+static int set_delta(ostate_t* S, double delta) {
+    if (delta > 0.0) {
+        if (!(delta >= 1.0)) return -1;
+        S->delta2 = delta * delta;
+        S->guard = 1;
+    }
+    return 0;
 }
 
 static int check_args(int64_t n, int d, int k, int work, int dist, int flags) {
@@ -326,11 +370,13 @@ int oracle_fit(int64_t n, int d, int k, int work, int dist, int flags, const dou
                const double* C0_in, int max_iter, double tol, int32_t* labels_out,
                double* C_out, double* sse_out, int32_t* iters_out, double* shift_out,
                double* scale_out, double* tr_sse, int64_t* tr_changed, double* tr_shift2,
-               int32_t* tr_empty) {
+               int32_t* tr_empty, double delta, int64_t* n_trig_out) {
     if (check_args(n, d, k, work, dist, flags) != 0 || max_iter < 1 || k > n) return -1;
     int norm = flags & ONORM_MASK, guard = (flags & OGUARD) != 0;
     ostate_t S;
     if (alloc_state(&S, n, d, k, work, dist, guard) != 0) { free_state(&S); return -2; }
+    if (set_delta(&S, delta) != 0) { free_state(&S); return -1; }
+    int64_t n_trig = 0;
     double* shift = (double*)malloc(sizeof(double) * d);
     double* scale = (double*)malloc(sizeof(double) * d);
     oracle_normalize_stats(norm, n, d, X_in, shift, scale);
@@ -352,7 +398,7 @@ int oracle_fit(int64_t n, int d, int k, int work, int dist, int flags, const dou
     int it = 0;
     for (it = 1; it <= max_iter; ++it) {
         prep_centroids(&S);                               /* O3 */
-        assign_all(&S, lab, dmin, NULL);                  /* O4, O5 */
+        n_trig += assign_all(&S, lab, dmin, NULL);        /* O4 (O4m), O5 */
         nsum_t sse = {0, 0};                              /* O6 */
         int64_t changed = 0;
         for (int64_t i = 0; i < n; ++i) {
@@ -373,6 +419,7 @@ int oracle_fit(int64_t n, int d, int k, int work, int dist, int flags, const dou
     memcpy(C_out, S.C, sizeof(double) * k * d);
     *sse_out = sse_final;
     *iters_out = it;
+    if (n_trig_out) *n_trig_out = n_trig;
     free(lab); free(prev); free(dmin); free(shift); free(scale);
     free_state(&S);
     return 0;
@@ -383,15 +430,17 @@ int oracle_fit(int64_t n, int d, int k, int work, int dist, int flags, const dou
 /* the new centroids (empty clusters keep C_in).                                              */
 int oracle_step(int64_t n, int d, int k, int work, int dist, int guard, const double* X,
                 const double* C_in, int32_t* labels, double* dmin, double* d2nd, double* sums,
-                int64_t* counts, double* C_next) {
+                int64_t* counts, double* C_next, double delta, int64_t* n_trig) {
     if (check_args(n, d, k, work, dist, guard ? OGUARD : 0) != 0) return -1;
     ostate_t S;
     if (alloc_state(&S, n, d, k, work, dist, guard) != 0) { free_state(&S); return -2; }
+    if (set_delta(&S, delta) != 0) { free_state(&S); return -1; }
     memcpy(S.X, X, sizeof(double) * n * d);
     memcpy(S.C, C_in, sizeof(double) * k * d);
     prep_points(&S);
     prep_centroids(&S);
-    assign_all(&S, labels, dmin, d2nd);
+    const int64_t tr = assign_all(&S, labels, dmin, d2nd);
+    if (n_trig) *n_trig = tr;
     double shift2; int empty;
     update_centroids(&S, labels, sums, counts, &shift2, &empty);
     memcpy(C_next, S.C, sizeof(double) * k * d);
@@ -401,15 +450,18 @@ int oracle_step(int64_t n, int d, int k, int work, int dist, int guard, const do
 
 /* Low-precision assignment only (kmeans_assign's definition): labels and D_min per point.   */
 int oracle_assign(int64_t n, int d, int k, int work, int dist, int guard, const double* X,
-                  const double* C, int32_t* labels, double* dmin, double* d2nd) {
+                  const double* C, int32_t* labels, double* dmin, double* d2nd, double delta,
+                  int64_t* n_trig) {
     if (check_args(n, d, k, work, dist, guard ? OGUARD : 0) != 0) return -1;
     ostate_t S;
     if (alloc_state(&S, n, d, k, work, dist, guard) != 0) { free_state(&S); return -2; }
+    if (set_delta(&S, delta) != 0) { free_state(&S); return -1; }
     memcpy(S.X, X, sizeof(double) * n * d);
     memcpy(S.C, C, sizeof(double) * k * d);
     prep_points(&S);
     prep_centroids(&S);
-    assign_all(&S, labels, dmin, d2nd);
+    const int64_t tr = assign_all(&S, labels, dmin, d2nd);
+    if (n_trig) *n_trig = tr;
     free_state(&S);
     return 0;
 }
