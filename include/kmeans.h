@@ -99,6 +99,11 @@ typedef struct kmeans_stats {
                                             certify; those with at most 32 candidate columns
                                             are resolved by exact fp32 evaluation of the
                                             candidates only (R2)                 */
+    int64_t n_dist;                      /* distances formed by the last fit's loop
+                                            (iters * n * k) or by the last kmeans_assign     */
+    int64_t n_dist_low;                  /* of which in low precision: all of them unless
+                                            kmeans_set_delta is on (then eq:xi-low-prec-ratio's
+                                            eta = n_dist_low / n_dist)     */
 } kmeans_stats;
 
 /*
@@ -156,6 +161,16 @@ int kmeans_get_stats(kmeans_handle h, kmeans_stats* out);
 /* kmeans_set_stream — run all of the handle's work on this cudaStream_t (NULL = the handle's
  * own stream). The caller keeps ownership of the stream. */
 int kmeans_set_stream(kmeans_handle h, void* cuda_stream);
+
+/* kmeans_set_delta — Alg 4 / Alg 5: per point-centroid pair, the
+ * distance of the Lloyd loop (and of kmeans_assign) uses the low precision only when
+ * eq:prec-delta holds, max(x^T x / c^T c, c^T c / x^T x) >= delta^2 (evaluated division-free in
+ * fp64: max(xn, cn) >= delta^2 min(xn, cn)), with Alg 4's infinity-norm operand scaling, and the
+ * working precision otherwise. delta = 1 makes every pair low precision (Alg 3 with scaling);
+ * delta = 0 turns the switch off (the default: every pair low precision, scaling as created).
+ * Runs on CUDA cores (both dot products per pair). The number of low-precision pairs is in
+ * kmeans_stats.n_dist_low. Returns KMEANS_EINVAL unless delta == 0 or 1 <= delta < inf.      */
+int kmeans_set_delta(kmeans_handle h, double delta);
 
 /* kmeans_set_timing — 1 = record CUDA events around every kernel of the loop (per-kernel times
  * in kmeans_stats), 0 = only the prep / loop / final events (default). */

@@ -30,7 +30,8 @@ NORM = {"none": KMEANS_NORM_NONE, "minmax": KMEANS_NORM_MINMAX, "zscore": KMEANS
 DIST_KERNELS = {0: "simt_work", 1: "simt_low", 2: "tcgen05", 3: "smalld_fused"}
 EXPORTS = ["kmeans_create", "kmeans_fit", "kmeans_assign", "kmeans_set_centroids",
            "kmeans_get_centroids", "kmeans_get_transform", "kmeans_get_stats",
-           "kmeans_set_stream", "kmeans_set_timing", "kmeans_destroy", "kmeans_last_error",
+           "kmeans_set_stream", "kmeans_set_timing", "kmeans_set_delta", "kmeans_destroy",
+           "kmeans_last_error",
            "kmeans_cast", "kmeans_create_dist", "kmeans_nccl_unique_id", "kmeans_version"]
 
 
@@ -47,7 +48,8 @@ class kmeans_stats(ct.Structure):
                 ("changed_t", ct.c_int64 * KMEANS_MAX_TRACE),
                 ("empty_t", ct.c_int32 * KMEANS_MAX_TRACE),
                 ("n_kernel_launches", ct.c_int64), ("n_final_fallback", ct.c_int64),
-                ("n_final_uncertified", ct.c_int64)]
+                ("n_final_uncertified", ct.c_int64), ("n_dist", ct.c_int64),
+                ("n_dist_low", ct.c_int64)]
 
 
 def _load():
@@ -66,6 +68,7 @@ def _load():
         "kmeans_get_stats": (i32, [P, ct.POINTER(kmeans_stats)]),
         "kmeans_set_stream": (i32, [P, P]),
         "kmeans_set_timing": (i32, [P, i32]),
+        "kmeans_set_delta": (i32, [P, ct.c_double]),
         "kmeans_destroy": (i32, [P]),
         "kmeans_last_error": (ct.c_char_p, [P]),
         "kmeans_cast": (i32, [i32, i32, P, i64, P]),
@@ -182,6 +185,11 @@ def kmeans_set_timing(h, enable: bool):
     _check(_lib.kmeans_set_timing(h, int(bool(enable))), h)
 
 
+def kmeans_set_delta(h, delta: float):
+    """Alg 4 / Alg 5 per-pair precision switch (0 = off, else delta >= 1)."""
+    _check(_lib.kmeans_set_delta(h, float(delta)), h)
+
+
 def kmeans_destroy(h):
     return _lib.kmeans_destroy(h)
 
@@ -205,19 +213,23 @@ def stats_dict(st: kmeans_stats) -> dict:
                 sse_t=list(st.sse_t[:t]), shift2_t=list(st.shift2_t[:t]),
                 changed_t=list(st.changed_t[:t]), empty_t=list(st.empty_t[:t]),
                 n_kernel_launches=st.n_kernel_launches, n_final_fallback=st.n_final_fallback,
-                n_final_uncertified=st.n_final_uncertified)
+                n_final_uncertified=st.n_final_uncertified, n_dist=st.n_dist,
+                n_dist_low=st.n_dist_low,
+                eta=(st.n_dist_low / st.n_dist) if st.n_dist else None)
 
 
 class KMeans:
     """Convenience wrapper owning one handle."""
 
     def __init__(self, n, d, k, work="fp32", dist="fp16", norm="none", guard=False,
-                 force_simt=False):
+                 force_simt=False, delta=None):
         flags = NORM[norm] | (KMEANS_GUARD_SCALE if guard else 0) | \
             (KMEANS_FORCE_SIMT if force_simt else 0)
         self.n, self.d, self.k = int(n), int(d), int(k)
         self.work = work
         self.h = kmeans_create(n, d, k, work, dist, flags)
+        if delta is not None:
+            kmeans_set_delta(self.h, delta)
 
     def fit(self, X, C0, max_iter=300, tol=1e-4, labels=None, centroids=None):
         return kmeans_fit(self.h, X, C0, max_iter, tol, labels, centroids)

@@ -104,6 +104,14 @@ cudaError_t launch_smalld_fused(int work, int dist, const Problem& p, const void
                                 const void* Cl, const void* cn, const void* sc, int32_t* labels,
                                 double* acc, AccLayout L, cudaStream_t s);
 
+// K6m: Alg 4's per-pair precision switch with threshold delta (>= 1); n_low (device) gets the
+// number of triggered (low-precision) pairs added.
+cudaError_t launch_assign_mixed(int work, int dist, const Problem& p, double delta, const void* Xl,
+                                const void* Xw, const void* xn, const void* sx, const void* Cl,
+                                const void* Cw, const void* cn, const void* sc, int32_t* labels,
+                                double* acc_sse, double* acc_changed, unsigned long long* n_low,
+                                cudaStream_t s);
+
 // K4: tcgen05 distance + argmin (fp16 / bf16 / e5m2 operands).
 bool tc_supported(int dist, int d_pad, int k);
 int tc_dpad(int dist, int d);   // padded row length (elements) the tcgen05 kernel needs

@@ -146,6 +146,181 @@ assign_simt_kernel(Problem p, const LT* __restrict__ Xl, const W* __restrict__ x
 }
 
 // ------------------------------------------------------------------------------------------
+// K6m: Alg 4's per-pair precision switch (Alg 5 step 3). For each pair
+// the condition eq:prec-delta is evaluated division-free in fp64,
+//     max(xn_i, cn_j) >= delta^2 min(xn_i, cn_j)           (reading R5, same as oracle O4m),
+// and the distance is the scaled low-precision value when it holds (Alg 4 lines 1-6: the dot of
+// the stored low operands, fp32 accumulation, v = fma(-2 s_i s_j, dot, cn_j)) and the
+// working-precision value otherwise (line 8: the dot of the working operands accumulated in
+// the working precision, v = fma(-2, dot, cn_j)). Both dot products are formed for every pair
+// (CUDA cores; the tensor-core variant is future work); triggered pairs are
+// counted (eq:xi-low-prec-ratio). Same argmin / SSE / changed bookkeeping as K6.
+// ------------------------------------------------------------------------------------------
+constexpr int MBK = 16;
+
+template <typename LT, typename W>
+__global__ void __launch_bounds__(NT)
+assign_mixed_kernel(Problem p, double delta2, const LT* __restrict__ Xl,
+                    const W* __restrict__ Xw, const W* __restrict__ xn,
+                    const W* __restrict__ sx, const LT* __restrict__ Cl,
+                    const W* __restrict__ Cw, const W* __restrict__ cn,
+                    const W* __restrict__ sc, int32_t* __restrict__ labels, double* acc_sse,
+                    double* acc_changed, unsigned long long* n_low) {
+    __shared__ float Xs[MBK][BM];
+    __shared__ float Cs[MBK][BN];
+    __shared__ W Xws[MBK][BM];
+    __shared__ W Cws[MBK][BN];
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;
+    const int64_t row0 = (int64_t)blockIdx.x * BM;
+
+    W bestv[4];
+    int bestj[4];
+    W srow[4], xrow[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        bestv[r] = (W)INFINITY;
+        bestj[r] = 0;
+        const int64_t row = row0 + ty * 4 + r;
+        srow[r] = (sx && row < p.n) ? sx[row] : (W)1;
+        xrow[r] = row < p.n ? xn[row] : (W)0;
+    }
+    unsigned long long trig_count = 0;
+
+    for (int n0 = 0; n0 < p.k; n0 += BN) {
+        float acc[4][4];
+        W accw[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { acc[r][c] = 0.0f; accw[r][c] = (W)0; }
+        for (int k0 = 0; k0 < p.d; k0 += MBK) {
+#pragma unroll
+            for (int e = 0; e < (BM * MBK) / NT; ++e) {
+                const int idx = tid + e * NT;
+                const int r = idx / MBK, kk = idx % MBK;
+                const int64_t row = row0 + r;
+                const int col = k0 + kk;
+                float v = 0.0f;
+                W vw = (W)0;
+                if (row < p.n && col < p.d) {
+                    v = (float)widen(Xl[row * p.d_pad + col]);
+                    vw = Xw[row * p.d + col];
+                }
+                Xs[kk][r] = v;
+                Xws[kk][r] = vw;
+                const int cj = n0 + r;
+                float w = 0.0f;
+                W ww = (W)0;
+                if (cj < p.k && col < p.d) {
+                    w = (float)widen(Cl[(int64_t)cj * p.d_pad + col]);
+                    ww = Cw[(int64_t)cj * p.d + col];
+                }
+                Cs[kk][r] = w;
+                Cws[kk][r] = ww;
+            }
+            __syncthreads();
+#pragma unroll 4
+            for (int kk = 0; kk < MBK; ++kk) {
+                float a[4], b[4];
+                W aw[4], bw[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) { a[r] = Xs[kk][ty * 4 + r]; aw[r] = Xws[kk][ty * 4 + r]; }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { b[c] = Cs[kk][tx * 4 + c]; bw[c] = Cws[kk][tx * 4 + c]; }
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        acc[r][c] = fmaf(a[r], b[c], acc[r][c]);
+                        accw[r][c] = fma(aw[r], bw[c], accw[r][c]);
+                    }
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int j = n0 + tx * 4 + c;
+            if (j < p.k) {
+                const W cnj = cn[j];
+                const W scj = sc ? sc[j] : (W)1;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    if (row0 + ty * 4 + r >= p.n) continue;
+                    const double a = (double)xrow[r], b = (double)cnj;
+                    const double mx = (a > b) ? a : b, mn = (a > b) ? b : a;
+                    const bool trig = mx >= delta2 * mn;
+                    W v;
+                    if (trig) {
+                        v = fma((W)-2 * (srow[r] * scj), (W)acc[r][c], cnj);
+                        ++trig_count;
+                    } else {
+                        v = fma((W)-2, accw[r][c], cnj);
+                    }
+                    if (v < bestv[r]) { bestv[r] = v; bestj[r] = j; }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+            const W v2 = __shfl_xor_sync(0xffffffffu, bestv[r], o);
+            const int j2 = __shfl_xor_sync(0xffffffffu, bestj[r], o);
+            argmin_merge(bestv[r], bestj[r], v2, j2);
+        }
+    }
+    double my_sse = 0.0, my_changed = 0.0;
+    if (tx == 0) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int64_t row = row0 + ty * 4 + r;
+            if (row < p.n) {
+                if (acc_changed && labels[row] != bestj[r]) my_changed += 1.0;
+                labels[row] = bestj[r];
+                if (acc_sse) {
+                    const double md = (double)xn[row] + (double)bestv[r];
+                    my_sse += md > 0.0 ? md : 0.0;
+                }
+            }
+        }
+    }
+    my_sse = warp_sum(my_sse);
+    my_changed = warp_sum(my_changed);
+    trig_count = warp_sum(trig_count);
+    __shared__ double red[2][NT / 32];
+    __shared__ unsigned long long redt[NT / 32];
+    if ((tid & 31) == 0) {
+        red[0][tid >> 5] = my_sse;
+        red[1][tid >> 5] = my_changed;
+        redt[tid >> 5] = trig_count;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double a = 0, b = 0;
+        unsigned long long t = 0;
+        for (int w = 0; w < NT / 32; ++w) { a += red[0][w]; b += red[1][w]; t += redt[w]; }
+        if (acc_sse) atomicAdd(acc_sse, a);
+        if (acc_changed && b != 0.0) atomicAdd(acc_changed, b);
+        if (n_low && t) atomicAdd(n_low, t);
+    }
+}
+
+template <typename LT, typename W>
+static cudaError_t mixed_launch(const Problem& p, double delta2, const void* Xl, const void* Xw,
+                                const void* xn, const void* sx, const void* Cl, const void* Cw,
+                                const void* cn, const void* sc, int32_t* labels,
+                                double* acc_sse, double* acc_changed, unsigned long long* n_low,
+                                cudaStream_t s) {
+    const int64_t blocks = (p.n + BM - 1) / BM;
+    assign_mixed_kernel<LT, W><<<(unsigned)blocks, NT, 0, s>>>(
+        p, delta2, (const LT*)Xl, (const W*)Xw, (const W*)xn, (const W*)sx, (const LT*)Cl,
+        (const W*)Cw, (const W*)cn, (const W*)sc, labels, acc_sse, acc_changed, n_low);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
 // K6b: register-tiled (8 x 8 per thread, 128 x 128 per block) CUDA-core variant for fp32
 // accumulation — the fp32 working mode and the final pass's CUDA-core rows. Same arithmetic as
 // K6: products summed in order t = 0..d-1 by fp32 FMA, v = fma(-2 s_i s_j, dot, ||c_j||^2),
@@ -624,6 +799,33 @@ cudaError_t launch_final_sse(int work, const void* Xw, int64_t n, int d, const v
         final_sse_kernel<float><<<grid, 256, 0, s>>>((const float*)Xw, n, d, (const float*)Cw,
                                                     labels, sse_out);
     return cudaGetLastError();
+}
+
+cudaError_t launch_assign_mixed(int work, int dist, const Problem& p, double delta, const void* Xl,
+                                const void* Xw, const void* xn, const void* sx, const void* Cl,
+                                const void* Cw, const void* cn, const void* sc, int32_t* labels,
+                                double* acc_sse, double* acc_changed, unsigned long long* n_low,
+                                cudaStream_t s) {
+    launches_add(1);
+    if (p.n <= 0) return cudaSuccess;
+    const double delta2 = delta * delta;
+    if (work == KMEANS_FP64) {
+        switch (dist) {
+            case KMEANS_FP64: return mixed_launch<double, double>(p, delta2, Xl, Xw, xn, sx, Cl, Cw, cn, sc, labels, acc_sse, acc_changed, n_low, s);
+            case KMEANS_FP32: return mixed_launch<float, double>(p, delta2, Xl, Xw, xn, sx, Cl, Cw, cn, sc, labels, acc_sse, acc_changed, n_low, s);
+            case KMEANS_FP16: return mixed_launch<__half, double>(p, delta2, Xl, Xw, xn, sx, Cl, Cw, cn, sc, labels, acc_sse, acc_changed, n_low, s);
+            case KMEANS_BF16: return mixed_launch<__nv_bfloat16, double>(p, delta2, Xl, Xw, xn, sx, Cl, Cw, cn, sc, labels, acc_sse, acc_changed, n_low, s);
+            case KMEANS_E5M2: return mixed_launch<e5m2_t, double>(p, delta2, Xl, Xw, xn, sx, Cl, Cw, cn, sc, labels, acc_sse, acc_changed, n_low, s);
+        }
+    } else {
+        switch (dist) {
+            case KMEANS_FP32: return mixed_launch<float, float>(p, delta2, Xl, Xw, xn, sx, Cl, Cw, cn, sc, labels, acc_sse, acc_changed, n_low, s);
+            case KMEANS_FP16: return mixed_launch<__half, float>(p, delta2, Xl, Xw, xn, sx, Cl, Cw, cn, sc, labels, acc_sse, acc_changed, n_low, s);
+            case KMEANS_BF16: return mixed_launch<__nv_bfloat16, float>(p, delta2, Xl, Xw, xn, sx, Cl, Cw, cn, sc, labels, acc_sse, acc_changed, n_low, s);
+            case KMEANS_E5M2: return mixed_launch<e5m2_t, float>(p, delta2, Xl, Xw, xn, sx, Cl, Cw, cn, sc, labels, acc_sse, acc_changed, n_low, s);
+        }
+    }
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace mpk

@@ -63,6 +63,11 @@ struct kmeans_ctx {
     int* fbc = nullptr;            // [0] uncertified rows, [1] rows left for the full evaluation
     int64_t last_fallback = 0;     // rows re-evaluated on CUDA cores in the last final pass
     int64_t last_uncertified = 0;  // rows the certified filter left open in the last final pass
+    // Alg 4 / Alg 5 per-pair precision switch (kmeans_set_delta): 0 = off
+    double delta = 0.0;
+    int guard_user = 0;            // the create-time guard flag (delta > 0 forces the scaling)
+    unsigned long long* n_low_dev = nullptr;   // triggered low-precision pairs, this fit
+    int64_t last_n_low = 0, last_n_dist = 0;
     // final-pass candidate path (grown to the uncertified row count on demand)
     int64_t cand_cap = 0;
     float* fb_thr = nullptr;       // per uncertified row: threshold T (size n)
@@ -158,7 +163,8 @@ void free_all(kmeans_ctx* h) {
     if (h->tc) tc_plan_destroy(h->tc);
     if (h->fin) tc_plan_destroy(h->fin);
     void* fin_bufs[] = {h->fin_Xl, h->fin_Cl, h->fin_sx, h->fin_sc, h->fbc, h->fb_thr,
-                        h->cand_X, h->cand_sx, h->cand_cnt, h->cand, h->cand_left, h->cand_key};
+                        h->cand_X, h->cand_sx, h->cand_cnt, h->cand, h->cand_left, h->cand_key,
+                        h->n_low_dev};
     for (void* b : fin_bufs)
         if (b) cudaFree(b);
     void* bufs[] = {h->Xw, h->xl_alias ? nullptr : h->Xl, h->xn, h->sx, h->Cw, h->Cl, h->cn,
@@ -273,6 +279,8 @@ int create_impl(int64_t n, int32_t d, int32_t k, int work, int dist, int flags,
     CA(dalloc(&h->census, 4 * sizeof(unsigned long long)));
     CA(dalloc(&h->sse_dev, 4 * sizeof(double)));
     CA(dalloc(&h->fbc, 4 * sizeof(int)));
+    CA(dalloc(&h->n_low_dev, sizeof(unsigned long long)));
+    h->guard_user = h->guard;
     if (h->dist_kernel == DK_TCGEN05) {
         std::string e;
         h->tc = tc_plan_create(dist, n, d, h->d_pad, k, h->Xl, h->Cl, &e);
@@ -361,7 +369,11 @@ struct EventPool {
 // Distance + argmin for the current centroids on h->n rows (loop iteration or assign).
 int run_assign(kmeans_ctx* h, int64_t rows, double* acc_sse, double* acc_changed) {
     Problem p{rows, h->d, h->k, h->d_pad, h->guard};
-    if (h->dist_kernel == DK_TCGEN05) {
+    if (h->delta > 0.0) {   // Alg 4: per-pair precision switch (both dot products per pair)
+        CK(launch_assign_mixed(h->work, h->dist, p, h->delta, h->Xl, h->Xw, h->xn, h->sx, h->Cl,
+                               h->Cw, h->cn, h->sc, h->labels, acc_sse, acc_changed,
+                               h->n_low_dev, h->stream));
+    } else if (h->dist_kernel == DK_TCGEN05) {
         CK(launch_assign_tc(h->tc, p, (const float*)h->xn, h->guard ? (const float*)h->sx : nullptr,
                             (const float*)h->cn, h->guard ? (const float*)h->sc : nullptr,
                             h->labels, acc_sse, acc_changed, h->stream));
@@ -548,6 +560,7 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
     // ---- A2: point prep (norms, guard scales, low operands), fused with the normalisation
     // on the fast path --------------------------------------------------------------------
     CK(cudaMemsetAsync(h->census, 0, 4 * sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(h->n_low_dev, 0, sizeof(unsigned long long), s));
     if (prep_fast_ok(h->work, d)) {
         CK(launch_prep_fast(h->dist, Xsrc, n, d, h->d_pad, h->guard, h->xn, h->sx, h->Xl,
                             h->census, norm ? h->Xw : nullptr, norm ? h->shift : nullptr,
@@ -576,7 +589,7 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
         CK(cudaMemsetAsync(h->acc, 0, sizeof(double) * h->L.total(), s));
         if (int rc = prep_centroids(h)) return rc;                         // A3
         if (timing) CK(cudaEventRecord(t0, s));
-        if (h->dist_kernel == DK_SMALLD) {                                  // A4 + A5 fused
+        if (h->dist_kernel == DK_SMALLD && h->delta <= 0.0) {              // A4 + A5 fused
             Problem p{n, d, k, h->d_pad, h->guard};
             CK(launch_smalld_fused(h->work, h->dist, p, h->Xw, h->Cl, h->cn,
                                    h->guard ? h->sc : nullptr, h->labels, h->acc, h->L, s));
@@ -630,8 +643,9 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
                                                       : cudaMemcpyDeviceToHost;
         CK(cudaMemcpyAsync(cent_out, h->Cw, (size_t)k * d * h->wsize, kind, s));
     }
-    unsigned long long census_h[4];
+    unsigned long long census_h[4], n_low_h = 0;
     CK(cudaMemcpyAsync(census_h, h->census, sizeof(census_h), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&n_low_h, h->n_low_dev, sizeof(n_low_h), cudaMemcpyDeviceToHost, s));
     int tl = std::min(it, KMEANS_MAX_TRACE - 1);
     std::vector<IterRec> tr(tl);
     if (tl > 0) CK(cudaMemcpyAsync(tr.data(), h->trace, sizeof(IterRec) * tl,
@@ -670,6 +684,12 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
     st.n_kernel_launches = launches_read() - launches0;
     st.n_final_fallback = h->last_fallback;
     st.n_final_uncertified = h->last_uncertified;
+    // distances formed in the loop on this rank: every iteration computes all n k pairs;
+    // with delta > 0, n_dist_low of them were triggered to low precision (eta)
+    h->last_n_dist = (int64_t)it * n * k;
+    h->last_n_low = h->delta > 0.0 ? (int64_t)n_low_h : h->last_n_dist;
+    st.n_dist_low = h->last_n_low;
+    st.n_dist = h->last_n_dist;
     int warn = 0;
     if (st.n_nonfinite > 0) warn |= KMEANS_WARN_NONFINITE;
     if (any_empty) warn |= KMEANS_WARN_EMPTY;
@@ -722,6 +742,7 @@ int kmeans_assign(kmeans_handle h, const void* X, int64_t m, int32_t* labels, do
     double total = 0.0;
     const bool lab_dev = is_device_ptr(labels);
     if (int rc = prep_centroids(h)) return rc;
+    CK(cudaMemsetAsync(h->n_low_dev, 0, sizeof(unsigned long long), s));
     for (int64_t r0 = 0; r0 < m; r0 += h->n) {
         int64_t rows = std::min<int64_t>(h->n, m - r0);
         const char* src = (const char*)X + (size_t)r0 * h->d * h->wsize;
@@ -739,7 +760,7 @@ int kmeans_assign(kmeans_handle h, const void* X, int64_t m, int32_t* labels, do
                            h->Xl, nullptr, s));
         }
         CK(cudaMemsetAsync(h->sse_dev, 0, sizeof(double), s));
-        if (h->dist_kernel == DK_SMALLD) {
+        if (h->dist_kernel == DK_SMALLD && h->delta <= 0.0) {
             Problem p{rows, h->d, h->k, h->d_pad, h->guard};
             CK(launch_assign_simt(h->work, h->dist, p, h->Xl, h->xn, h->guard ? h->sx : nullptr,
                                   h->Cl, h->cn, h->guard ? h->sc : nullptr, h->labels,
@@ -755,6 +776,13 @@ int kmeans_assign(kmeans_handle h, const void* X, int64_t m, int32_t* labels, do
         total += part;
     }
     if (sse) *sse = total;
+    // distance counts of this assign (kmeans_stats.n_dist / n_dist_low)
+    unsigned long long n_low_h = 0;
+    CK(cudaMemcpy(&n_low_h, h->n_low_dev, sizeof(n_low_h), cudaMemcpyDeviceToHost));
+    h->last_n_dist = m * (int64_t)h->k;
+    h->last_n_low = h->delta > 0.0 ? (int64_t)n_low_h : h->last_n_dist;
+    h->stats.n_dist = h->last_n_dist;
+    h->stats.n_dist_low = h->last_n_low;
     return KMEANS_OK;
 }
 
@@ -813,6 +841,16 @@ int kmeans_set_stream(kmeans_handle h, void* stream) {
 int kmeans_set_timing(kmeans_handle h, int enable) {
     if (!h) return KMEANS_EINVAL;
     h->timing = enable;
+    return KMEANS_OK;
+}
+
+int kmeans_set_delta(kmeans_handle h, double delta) {
+    if (!h) return KMEANS_EINVAL;
+    if (!(delta == 0.0 || (delta >= 1.0 && std::isfinite(delta))))
+        return fail(h, KMEANS_EINVAL, "delta must be 0 (off) or a finite value >= 1");
+    h->delta = delta;
+    // Alg 4 lines 1-5: the triggered pairs use the infinity-norm scaled operands
+    h->guard = delta > 0.0 ? 1 : h->guard_user;
     return KMEANS_OK;
 }
 
