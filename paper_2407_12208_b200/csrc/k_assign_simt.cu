@@ -18,6 +18,8 @@
 #include "common.cuh"
 #include "internal.h"
 
+#include <stdlib.h>
+
 namespace mpk {
 
 namespace {
@@ -447,6 +449,242 @@ assign_simt_big_kernel(Problem p, const LT* __restrict__ Xl, const W* __restrict
 }
 
 // ------------------------------------------------------------------------------------------
+// K6m-b: Alg 4's per-pair precision switch for fp32 work on K6b's 128 x 128 tiles (8 x 8 per
+// thread). Per centroid tile, the rows' and columns' norm ranges classify the tile in fp64
+// (monotone, so the classification agrees with every per-pair decision):
+//   no pair triggered   <=  xmax < d2 cmin  and  cmax < d2 xmin
+//   every pair triggered <= xmin >= d2 cmax  or   cmin >= d2 xmax
+// and only the dot products a tile needs are formed (z-scored data at delta = 2 is almost
+// entirely "no pair triggered": one fp32 GEMM instead of two). A mixed tile runs the low
+// GEMM (triggered pairs) and then the working GEMM (the others); the argmin merges by (value,
+// index), so the result equals K6m's ascending-j scan. Same arithmetic per value as K6m:
+// dot products accumulated t = 0..d-1 by fp32 FMA, v = fma(-2 s_i s_j, dot_l, cn_j) or
+// fma(-2, dot_w, cn_j).
+// ------------------------------------------------------------------------------------------
+template <typename LT, bool LOWP>
+MPK_DEV void mixed_tile_gemm(const Problem& p, const void* __restrict__ Xsrc,
+                             const void* __restrict__ Csrc, int64_t row0, int n0, int tid,
+                             int tx, int ty, const int64_t (&arow)[8], float (&As)[B2K][B2M + 4],
+                             float (&Bs)[B2K][B2N + 4], float (&acc)[8][8]) {
+    const int stride = LOWP ? p.d_pad : p.d;
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[r][c] = 0.0f;
+    for (int k0 = 0; k0 < p.d; k0 += B2K) {
+        const int kk = tid & 15;
+        const int col = k0 + kk;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int r = (tid >> 4) + 16 * e;
+            float a = 0.0f, b = 0.0f;
+            if (arow[e] >= 0 && col < p.d) {
+                a = LOWP ? (float)widen(((const LT*)Xsrc)[arow[e] * stride + col])
+                         : ((const float*)Xsrc)[arow[e] * stride + col];
+            }
+            const int cj = n0 + r;
+            if (cj < p.k && col < p.d) {
+                b = LOWP ? (float)widen(((const LT*)Csrc)[(int64_t)cj * stride + col])
+                         : ((const float*)Csrc)[(int64_t)cj * stride + col];
+            }
+            As[kk][r] = a;
+            Bs[kk][r] = b;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < B2K; ++q) {
+            const float4 a0 = *reinterpret_cast<const float4*>(&As[q][ty * 8]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&As[q][ty * 8 + 4]);
+            const float4 b0 = *reinterpret_cast<const float4*>(&Bs[q][tx * 8]);
+            const float4 b1 = *reinterpret_cast<const float4*>(&Bs[q][tx * 8 + 4]);
+            const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) acc[r][c] = fmaf(a[r], b[c], acc[r][c]);
+        }
+        __syncthreads();
+    }
+}
+
+#ifndef MPK_MIXB_MINB
+#define MPK_MIXB_MINB 2
+#endif
+template <typename LT>
+__global__ void __launch_bounds__(B2T, MPK_MIXB_MINB)
+assign_mixed_big_kernel(Problem p, double delta2, const LT* __restrict__ Xl,
+                        const float* __restrict__ Xw, const float* __restrict__ xn,
+                        const float* __restrict__ sx, const LT* __restrict__ Cl,
+                        const float* __restrict__ Cw, const float* __restrict__ cn,
+                        const float* __restrict__ sc, int32_t* __restrict__ labels,
+                        double* acc_sse, double* acc_changed, unsigned long long* n_low) {
+    __shared__ __align__(16) float As[B2K][B2M + 4];
+    __shared__ __align__(16) float Bs[B2K][B2N + 4];
+    __shared__ float red_f[4][B2T / 32];
+    __shared__ int red_nan[B2T / 32];
+    __shared__ float tile_rng[6];   // xmin, xmax, cmin, cmax, row-NaN, col-NaN
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, wid = tid >> 5;
+    const int tx = tid & 15, ty = tid >> 4;
+    const int64_t row0 = (int64_t)blockIdx.x * B2M;
+
+    float bestv[8], srow[8], xrow[8];
+    int bestj[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const int64_t row = row0 + ty * 8 + r;
+        bestv[r] = INFINITY;
+        bestj[r] = 0;
+        srow[r] = (sx && row < p.n) ? sx[row] : 1.0f;
+        xrow[r] = row < p.n ? xn[row] : 0.0f;
+    }
+    int64_t arow[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int64_t li = row0 + (tid >> 4) + 16 * e;
+        arow[e] = li < p.n ? li : -1;
+    }
+    // row norm range of this block (thread t < 128 owns row t)
+    {
+        float lo = INFINITY, hi = -INFINITY;
+        int nan = 0;
+        if (tid < B2M && row0 + tid < p.n) {
+            const float v = xn[row0 + tid];
+            if (isnan(v)) nan = 1;
+            else { lo = v; hi = v; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+            nan |= __shfl_xor_sync(0xffffffffu, nan, o);
+        }
+        if (lane == 0) { red_f[0][wid] = lo; red_f[1][wid] = hi; red_nan[wid] = nan; }
+        __syncthreads();
+        if (tid == 0) {
+            float a = INFINITY, b = -INFINITY;
+            int c = 0;
+            for (int w = 0; w < B2T / 32; ++w) { a = fminf(a, red_f[0][w]); b = fmaxf(b, red_f[1][w]); c |= red_nan[w]; }
+            tile_rng[0] = a; tile_rng[1] = b; tile_rng[4] = (float)c;
+        }
+        __syncthreads();
+    }
+    const double xmin = tile_rng[0], xmax = tile_rng[1];
+    const bool row_nan = tile_rng[4] != 0.0f;
+    unsigned long long trig_count = 0;
+    float acc[8][8];
+
+    for (int n0 = 0; n0 < p.k; n0 += B2N) {
+        // column norm range of this centroid tile
+        {
+            float lo = INFINITY, hi = -INFINITY;
+            int nan = 0;
+            if (tid < B2N && n0 + tid < p.k) {
+                const float v = cn[n0 + tid];
+                if (isnan(v)) nan = 1;
+                else { lo = v; hi = v; }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+                hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+                nan |= __shfl_xor_sync(0xffffffffu, nan, o);
+            }
+            if (lane == 0) { red_f[2][wid] = lo; red_f[3][wid] = hi; red_nan[wid] = nan; }
+            __syncthreads();
+            if (tid == 0) {
+                float a = INFINITY, b = -INFINITY;
+                int c = 0;
+                for (int w = 0; w < B2T / 32; ++w) { a = fminf(a, red_f[2][w]); b = fmaxf(b, red_f[3][w]); c |= red_nan[w]; }
+                tile_rng[2] = a; tile_rng[3] = b; tile_rng[5] = (float)c;
+            }
+            __syncthreads();
+        }
+        const double cmin = tile_rng[2], cmax = tile_rng[3];
+        const bool any_nan = row_nan || tile_rng[5] != 0.0f;
+        const bool none_trig = !any_nan && xmax < delta2 * cmin && cmax < delta2 * xmin;
+        const bool all_trig = !any_nan && (xmin >= delta2 * cmax || cmin >= delta2 * xmax);
+        __syncthreads();   // tile_rng is rewritten by the next tile
+        for (int phase = 0; phase < 2; ++phase) {
+            const bool low = phase == 0;
+            if (low && none_trig) continue;
+            if (!low && all_trig) continue;
+            if (low) mixed_tile_gemm<LT, true>(p, Xl, Cl, row0, n0, tid, tx, ty, arow, As, Bs, acc);
+            else mixed_tile_gemm<LT, false>(p, Xw, Cw, row0, n0, tid, tx, ty, arow, As, Bs, acc);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const int j = n0 + tx * 8 + c;
+                if (j >= p.k) continue;
+                const float cnj = cn[j];
+                const float scj = sc ? sc[j] : 1.0f;
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    if (row0 + ty * 8 + r >= p.n) continue;
+                    bool trig;
+                    if (all_trig) trig = true;
+                    else if (none_trig) trig = false;
+                    else {
+                        const double a = (double)xrow[r], b = (double)cnj;
+                        const double mx = (a > b) ? a : b, mn = (a > b) ? b : a;
+                        trig = mx >= delta2 * mn;
+                    }
+                    if (trig != low) continue;
+                    float v;
+                    if (low) {
+                        v = fmaf(-2.0f * (srow[r] * scj), acc[r][c], cnj);
+                        ++trig_count;
+                    } else {
+                        v = fmaf(-2.0f, acc[r][c], cnj);
+                    }
+                    argmin_merge(bestv[r], bestj[r], v, j);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+            const float v2 = __shfl_xor_sync(0xffffffffu, bestv[r], o);
+            const int j2 = __shfl_xor_sync(0xffffffffu, bestj[r], o);
+            argmin_merge(bestv[r], bestj[r], v2, j2);
+        }
+    }
+    double my_sse = 0.0, my_changed = 0.0;
+    if (tx == 0) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int64_t row = row0 + ty * 8 + r;
+            if (row < p.n) {
+                // an all-NaN/+inf row keeps label 0 (bestj stays 0)
+                if (acc_changed && labels[row] != bestj[r]) my_changed += 1.0;
+                labels[row] = bestj[r];
+                if (acc_sse) {
+                    const double md = (double)xn[row] + (double)bestv[r];
+                    my_sse += md > 0.0 ? md : 0.0;
+                }
+            }
+        }
+    }
+    my_sse = warp_sum(my_sse);
+    my_changed = warp_sum(my_changed);
+    trig_count = warp_sum(trig_count);
+    __shared__ double red[2][B2T / 32];
+    __shared__ unsigned long long redt[B2T / 32];
+    if (lane == 0) { red[0][wid] = my_sse; red[1][wid] = my_changed; redt[wid] = trig_count; }
+    __syncthreads();
+    if (tid == 0) {
+        double a = 0, b = 0;
+        unsigned long long t = 0;
+        for (int w = 0; w < B2T / 32; ++w) { a += red[0][w]; b += red[1][w]; t += redt[w]; }
+        if (acc_sse) atomicAdd(acc_sse, a);
+        if (acc_changed && b != 0.0) atomicAdd(acc_changed, b);
+        if (n_low && t) atomicAdd(n_low, t);
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 // K5 small-d fused assign + update.
 // ------------------------------------------------------------------------------------------
 constexpr int SD_D = 4, SD_K = 8, SD_T = 256;
@@ -817,6 +1055,17 @@ cudaError_t launch_assign_mixed(int work, int dist, const Problem& p, double del
             case KMEANS_BF16: return mixed_launch<__nv_bfloat16, double>(p, delta2, Xl, Xw, xn, sx, Cl, Cw, cn, sc, labels, acc_sse, acc_changed, n_low, s);
             case KMEANS_E5M2: return mixed_launch<e5m2_t, double>(p, delta2, Xl, Xw, xn, sx, Cl, Cw, cn, sc, labels, acc_sse, acc_changed, n_low, s);
         }
+    } else if (getenv("MPK_MIXED_SMALL") == nullptr) {
+        // fp32 work: K6b-sized tiles, per-tile classification (K6m-b)
+        const int64_t blocks = (p.n + B2M - 1) / B2M;
+#define MIXB(LT) assign_mixed_big_kernel<LT><<<(unsigned)blocks, B2T, 0, s>>>(p, delta2, (const LT*)Xl, (const float*)Xw, (const float*)xn, (const float*)sx, (const LT*)Cl, (const float*)Cw, (const float*)cn, (const float*)sc, labels, acc_sse, acc_changed, n_low)
+        switch (dist) {
+            case KMEANS_FP32: MIXB(float); return cudaGetLastError();
+            case KMEANS_FP16: MIXB(__half); return cudaGetLastError();
+            case KMEANS_BF16: MIXB(__nv_bfloat16); return cudaGetLastError();
+            case KMEANS_E5M2: MIXB(e5m2_t); return cudaGetLastError();
+        }
+#undef MIXB
     } else {
         switch (dist) {
             case KMEANS_FP32: return mixed_launch<float, float>(p, delta2, Xl, Xw, xn, sx, Cl, Cw, cn, sc, labels, acc_sse, acc_changed, n_low, s);

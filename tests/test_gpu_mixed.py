@@ -113,3 +113,22 @@ def test_set_delta_rejects_values_below_one():
         mpk.kmeans_set_delta(km.h, float("inf"))
     mpk.kmeans_set_delta(km.h, 0.0)
     km.close()
+
+
+@pytest.mark.parametrize("dist", ["fp16", "bf16"])
+def test_mixed_tile_classes(dist):
+    """Rows sorted by norm and several centroid tiles (k = 300): the fp32 kernel sees tiles in
+    which no pair, every pair and some pairs trigger (its per-tile shortcut); trigger counts stay
+    exact and labels admissible."""
+    n, d, k, delta = 4099, 40, 300, 1.5
+    Xn, _ = _spread(n, d, 8, "fp32", seed=7)
+    order = np.argsort((Xn.astype(np.float64) ** 2).sum(1))
+    Xn = np.ascontiguousarray(Xn[order])
+    C = synth.init_rows(Xn, k, 3)
+    C = np.ascontiguousarray(C[np.argsort((C.astype(np.float64) ** 2).sum(1))])
+    lab, st = _gpu_assign(Xn, C, "fp32", dist, delta=delta)
+    ref_lab, _, _, ref_low = oracle.assign(Xn, C, "fp32", dist, delta=delta, return_n_low=True)
+    D, B, n_trig = _mixed_reference(Xn, C, "fp32", dist, delta)
+    assert 0 < ref_low < n * k
+    assert st["n_dist_low"] == ref_low
+    assert check_labels_admissible(lab, ref_lab, D, B) <= 2e-3
