@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-simt", action="store_true")
+    ap.add_argument("--delta", type=float, default=None,
+                    help="Alg 4/5 per-pair precision switch (kmeans_set_delta); not the default "
+                         "workload: reports eta and the CUDA-core mixed kernel's roofline")
     return ap.parse_args()
 
 
@@ -211,6 +214,8 @@ def main():
         h = mpk.kmeans_create(n_local, d, k, cfg.work, dist, flags)
     stream = torch.cuda.Stream()
     mpk.kmeans_set_stream(h, stream.cuda_stream)
+    if args.delta is not None:
+        mpk.kmeans_set_delta(h, args.delta)
 
     def step():
         return mpk.kmeans_fit(h, Xd, Cd, args.iters, -1.0, labels, cent)
@@ -246,9 +251,9 @@ def main():
 
     # ---- roofline of the dominant kernel (distance + argmin) ------------------------------
     peaks, peak_src = load_peaks()
-    kern = st["dist_kernel"]
+    kern = st["dist_kernel"] if args.delta is None else "mixed_cuda_core"
     t_launch_ms = t_dist / (args.steps * args.iters)
-    flops = 2.0 * n_local * k * d
+    flops = 2.0 * n_local * k * d       # one dot product per pair (low or working precision)
     if kern == "tcgen05":
         ratio = 2.0 if dist == "e5m2" else 1.0
         peak = peaks["bf16_tflops"] * ratio
@@ -295,7 +300,7 @@ def main():
                                          + 8), "steps": e_steps}
 
     cb = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.delta is None:
         cb = cpu_baseline(cfg, dist, norm, guard)
 
     mpk.kmeans_destroy(h)
@@ -317,6 +322,7 @@ def main():
                     "dist": st["t_dist_ms"], "update": st["t_update_ms"],
                     "allreduce": st["t_allreduce_ms"], "finalize": st["t_finalize_ms"]},
                 "dist_kernel": kern, "last_sse": sse,
+                **({"delta": args.delta, "eta": st["eta"]} if args.delta is not None else {}),
                 "final_pass_cuda_core_rows": st["n_final_fallback"],
                 "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk.summary()}
