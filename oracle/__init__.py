@@ -57,6 +57,7 @@ def _load():
             lib.oracle_prep.argtypes = [i64, i32, i32, i32, i32, P, P, P, P]
             lib.oracle_final.argtypes = [i64, i32, i32, i32, P, P, P, P]
             lib.oracle_num_threads.restype = i32
+            lib.oracle_seed_d2.argtypes = [i64, i32, i32, i32, i32, i32, P, P, P, P, P]
             _lib = lib
     return _lib
 
@@ -211,3 +212,23 @@ def final(X, C, work="fp32"):
     lib.oracle_final(X.shape[0], X.shape[1], Cc.shape[0], _prec(work), _p(X), _p(Cc),
                      _p(labels), ct.byref(sse))
     return labels, sse.value
+
+
+def seed_d2(X, k, u, work="fp32", dist="fp16", norm="none", guard=False, return_d2=False):
+    """O10: D^2 seeding (Alg 1) in the low precision with the caller's uniforms u[k] (reading
+    R6). Returns (indices int64[k], warn) — or (indices, warn, final D2) with return_d2."""
+    lib = _load()
+    X = _f64(X)
+    n, d = X.shape
+    uu = _f64(u)
+    assert uu.shape == (k,)
+    idx = np.empty(k, np.int64)
+    d2 = np.empty(n) if return_d2 else None
+    warn = ct.c_int()
+    rc = lib.oracle_seed_d2(n, d, k, _prec(work), _prec(dist), _flags(norm, guard), _p(X),
+                            _p(uu), _p(idx), _p(d2) if return_d2 else None, ct.byref(warn))
+    if rc != 0:
+        raise ValueError(f"oracle_seed_d2 rc={rc}")
+    if return_d2:
+        return idx, warn.value, d2
+    return idx, warn.value
