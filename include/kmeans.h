@@ -71,7 +71,9 @@ enum kmeans_status {
     KMEANS_WARN_NONFINITE = 1,       /* a low-precision cast produced +-inf / NaN (overflow)  */
     KMEANS_WARN_EMPTY = 2,           /* some cluster was empty in some iteration (kept)       */
     KMEANS_WARN_MAXITER = 4,         /* tol >= 0 and max_iter reached without convergence     */
-    KMEANS_WARN_UNDERFLOW = 8        /* a nonzero value rounded to zero or a subnormal in u_l  */
+    KMEANS_WARN_UNDERFLOW = 8,       /* a nonzero value rounded to zero or a subnormal in u_l  */
+    KMEANS_WARN_SEED_UNIFORM = 16    /* kmeans_seed_d2: a round had sum D^2 = 0 or non-finite
+                                        and drew uniformly                        */
 };
 
 /* Per-fit observability (filled by kmeans_get_stats after kmeans_fit). */
@@ -161,6 +163,17 @@ int kmeans_get_stats(kmeans_handle h, kmeans_stats* out);
 /* kmeans_set_stream — run all of the handle's work on this cudaStream_t (NULL = the handle's
  * own stream). The caller keeps ownership of the stream. */
 int kmeans_set_stream(kmeans_handle h, void* cuda_stream);
+
+/* kmeans_seed_d2 — seeding by D^2 weighting (Alg 1) with the distances of
+ * Alg 3 step 1 in the low precision, on the handle's n rows of X (same
+ * normalisation and operands as kmeans_fit; X host or device, work dtype, n x d). u: k uniforms
+ * in [0, 1) (host), the method's random draws. indices (host, int64[k], out): the chosen rows,
+ * distinct. The draw is the deterministic rule of DESIGN.md reading R6 (first index
+ * floor(u_0 n); then the first index whose running sum of D^2 weights, in a fixed blocked order,
+ * exceeds u_j * sum; D^2 from the stored low operands with the dot in fp64). Pass the rows
+ * X[indices] as C0 to kmeans_fit for Alg 3 / Alg 5 end to end. Single-GPU handles only.
+ * Returns 0, KMEANS_WARN_SEED_UNIFORM, or an error (u outside [0, 1): KMEANS_EINVAL).        */
+int kmeans_seed_d2(kmeans_handle h, const void* X, const double* u, int64_t* indices);
 
 /* kmeans_set_delta — Alg 4 / Alg 5: per point-centroid pair, the
  * distance of the Lloyd loop (and of kmeans_assign) uses the low precision only when

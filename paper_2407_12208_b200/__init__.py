@@ -22,6 +22,7 @@ KMEANS_FORCE_SIMT = 0x200
 KMEANS_OK, KMEANS_EINVAL, KMEANS_ENOMEM, KMEANS_ECUDA, KMEANS_ENCCL, KMEANS_ENODEV = \
     0, -1, -2, -3, -4, -5
 KMEANS_WARN_NONFINITE, KMEANS_WARN_EMPTY, KMEANS_WARN_MAXITER, KMEANS_WARN_UNDERFLOW = 1, 2, 4, 8
+KMEANS_WARN_SEED_UNIFORM = 16
 KMEANS_MAX_TRACE = 1024
 
 PREC = {"fp64": KMEANS_FP64, "fp32": KMEANS_FP32, "fp16": KMEANS_FP16, "bf16": KMEANS_BF16,
@@ -30,7 +31,8 @@ NORM = {"none": KMEANS_NORM_NONE, "minmax": KMEANS_NORM_MINMAX, "zscore": KMEANS
 DIST_KERNELS = {0: "simt_work", 1: "simt_low", 2: "tcgen05", 3: "smalld_fused"}
 EXPORTS = ["kmeans_create", "kmeans_fit", "kmeans_assign", "kmeans_set_centroids",
            "kmeans_get_centroids", "kmeans_get_transform", "kmeans_get_stats",
-           "kmeans_set_stream", "kmeans_set_timing", "kmeans_set_delta", "kmeans_destroy",
+           "kmeans_set_stream", "kmeans_set_timing", "kmeans_set_delta", "kmeans_seed_d2",
+           "kmeans_destroy",
            "kmeans_last_error",
            "kmeans_cast", "kmeans_create_dist", "kmeans_nccl_unique_id", "kmeans_version"]
 
@@ -69,6 +71,7 @@ def _load():
         "kmeans_set_stream": (i32, [P, P]),
         "kmeans_set_timing": (i32, [P, i32]),
         "kmeans_set_delta": (i32, [P, ct.c_double]),
+        "kmeans_seed_d2": (i32, [P, P, P, P]),
         "kmeans_destroy": (i32, [P]),
         "kmeans_last_error": (ct.c_char_p, [P]),
         "kmeans_cast": (i32, [i32, i32, P, i64, P]),
@@ -185,6 +188,17 @@ def kmeans_set_timing(h, enable: bool):
     _check(_lib.kmeans_set_timing(h, int(bool(enable))), h)
 
 
+def kmeans_seed_d2(h, X, u):
+    """Alg 1 D^2 seeding in the low precision (R6): returns (indices int64[k], rc)."""
+    import numpy as np
+    uu = np.ascontiguousarray(np.asarray(u, dtype=np.float64))   # exactly k values
+    idx = np.empty(uu.shape[0], np.int64)
+    rc = _lib.kmeans_seed_d2(h, _ptr(X), uu.ctypes.data_as(ct.c_void_p),
+                             idx.ctypes.data_as(ct.c_void_p))
+    _check(rc, h)
+    return idx, rc
+
+
 def kmeans_set_delta(h, delta: float):
     """Alg 4 / Alg 5 per-pair precision switch (0 = off, else delta >= 1)."""
     _check(_lib.kmeans_set_delta(h, float(delta)), h)
@@ -236,6 +250,12 @@ class KMeans:
 
     def assign(self, X, labels, m=None):
         return kmeans_assign(self.h, X, X.shape[0] if m is None else m, labels)
+
+    def seed(self, X, u):
+        """Alg 1 D^2 seeding with the k uniforms u (returns int64 row indices)."""
+        if len(u) != self.k:
+            raise ValueError(f"need exactly k = {self.k} uniforms")
+        return kmeans_seed_d2(self.h, X, u)[0]
 
     def stats(self) -> dict:
         return stats_dict(kmeans_get_stats(self.h))

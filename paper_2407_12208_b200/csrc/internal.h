@@ -112,6 +112,14 @@ cudaError_t launch_assign_mixed(int work, int dist, const Problem& p, double del
                                 double* acc_sse, double* acc_changed, unsigned long long* n_low,
                                 cudaStream_t s);
 
+// K11: D^2 seeding rounds (Alg 1 in the low precision, R6): idx[0] set by the
+// caller; fills idx[1..k-1]; D2 (n) and ps (seed_blocks(n)) are scratch; *warn |= 1 on a
+// degenerate round (uniform fallback).
+int64_t seed_blocks(int64_t n);
+cudaError_t launch_seed_d2(int work, int dist, const void* Xl, int64_t n, int d, int d_pad,
+                           const void* xn, const void* sx, int guard, int k, const double* u,
+                           int64_t* idx, double* D2, double* ps, int* warn, cudaStream_t s);
+
 // K4: tcgen05 distance + argmin (fp16 / bf16 / e5m2 operands).
 bool tc_supported(int dist, int d_pad, int k);
 int tc_dpad(int dist, int d);   // padded row length (elements) the tcgen05 kernel needs

@@ -532,6 +532,33 @@ int final_assign(kmeans_ctx* h, const Problem& pf) {
     return 0;
 }
 
+// A1 + A2 for the handle's n rows of X: normalisation statistics and transform (O1), norms,
+// guard scales and low-precision operands (O2). A device X is read in place by the statistics
+// and the (out-of-place) normalisation, so it is never copied; a host X is staged into Xw first
+// (that copy is needed anyway). Resets the operand census.
+int prepare_points(kmeans_ctx* h, const void* X) {
+    cudaStream_t s = h->stream;
+    const int64_t n = h->n;
+    const int d = h->d;
+    const bool norm = h->norm != KMEANS_NORM_NONE;
+    const void* Xsrc = h->Xw;
+    if (norm && is_device_ptr(X)) Xsrc = X;
+    else if (int rc = stage_rows(h, X, n, h->Xw)) return rc;
+    if (norm)
+        if (int rc = normalise_stats(h, Xsrc, n)) return rc;
+    CK(cudaMemsetAsync(h->census, 0, 4 * sizeof(unsigned long long), s));
+    if (prep_fast_ok(h->work, d)) {
+        CK(launch_prep_fast(h->dist, Xsrc, n, d, h->d_pad, h->guard, h->xn, h->sx, h->Xl,
+                            h->census, norm ? h->Xw : nullptr, norm ? h->shift : nullptr,
+                            norm ? h->scale : nullptr, s));
+    } else {
+        if (norm) CK(launch_norm_apply(h->work, h->Xw, n, d, h->shift, h->scale, s, Xsrc));
+        CK(launch_prep(h->work, h->dist, h->Xw, n, d, h->d_pad, h->guard, h->xn, h->sx, h->Xl,
+                       h->census, s));
+    }
+    return 0;
+}
+
 int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, double tol,
              int32_t* labels_out, void* cent_out, double* sse_out, int32_t* iters_out) {
     if (!X || !C0) return fail(h, KMEANS_EINVAL, "X and C0 are required");
@@ -545,31 +572,12 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
     const int d = h->d, k = h->k;
 
     CK(cudaEventRecord(e0, s));
-    // ---- A1: stage + normalise X and C0 -------------------------------------------------
-    // A device X is read in place by the statistics and the (out-of-place) normalisation, so it
-    // is never copied; a host X is staged into Xw first (that copy is needed anyway).
-    const bool norm = h->norm != KMEANS_NORM_NONE;
-    const void* Xsrc = h->Xw;
-    if (norm && is_device_ptr(X)) Xsrc = X;
-    else if (int rc = stage_rows(h, X, n, h->Xw)) return rc;
+    // ---- A1 + A2: normalise X, point prep; normalise C0 ----------------------------------
+    if (int rc = prepare_points(h, X)) return rc;
     if (int rc = stage_rows(h, C0, k, h->Cw)) return rc;
-    if (norm) {
-        if (int rc = normalise_stats(h, Xsrc, n)) return rc;
+    if (h->norm != KMEANS_NORM_NONE)
         CK(launch_norm_apply(h->work, h->Cw, k, d, h->shift, h->scale, s));
-    }
-    // ---- A2: point prep (norms, guard scales, low operands), fused with the normalisation
-    // on the fast path --------------------------------------------------------------------
-    CK(cudaMemsetAsync(h->census, 0, 4 * sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(h->n_low_dev, 0, sizeof(unsigned long long), s));
-    if (prep_fast_ok(h->work, d)) {
-        CK(launch_prep_fast(h->dist, Xsrc, n, d, h->d_pad, h->guard, h->xn, h->sx, h->Xl,
-                            h->census, norm ? h->Xw : nullptr, norm ? h->shift : nullptr,
-                            norm ? h->scale : nullptr, s));
-    } else {
-        if (norm) CK(launch_norm_apply(h->work, h->Xw, n, d, h->shift, h->scale, s, Xsrc));
-        CK(launch_prep(h->work, h->dist, h->Xw, n, d, h->d_pad, h->guard, h->xn, h->sx, h->Xl,
-                       h->census, s));
-    }
     CK(cudaMemsetAsync(h->labels, 0xff, (size_t)n * sizeof(int32_t), s));   // labels_prev = -1
     CK(cudaMemsetAsync(h->trace, 0, sizeof(IterRec) * KMEANS_MAX_TRACE, s));
     CK(cudaEventRecord(e1, s));
@@ -842,6 +850,50 @@ int kmeans_set_timing(kmeans_handle h, int enable) {
     if (!h) return KMEANS_EINVAL;
     h->timing = enable;
     return KMEANS_OK;
+}
+
+int kmeans_seed_d2(kmeans_handle h, const void* X, const double* u, int64_t* indices) {
+    if (!h) return KMEANS_EINVAL;
+    if (!X || !u || !indices) return fail(h, KMEANS_EINVAL, "X, u and indices are required");
+    if (h->comm) return fail(h, KMEANS_EINVAL, "kmeans_seed_d2 runs on single-GPU handles");
+    CK(cudaSetDevice(h->device));
+    cudaStream_t s = h->stream;
+    const int64_t n = h->n;
+    const int k = h->k;
+    for (int j = 0; j < k; ++j)
+        if (!(u[j] >= 0.0 && u[j] < 1.0))
+            return fail(h, KMEANS_EINVAL, "the uniforms u must lie in [0, 1)");
+    if (int rc = prepare_points(h, X)) return rc;
+    // scratch: D2 (n), block sums, u, indices, warning flag
+    double* D2 = nullptr;
+    double* ps = nullptr;
+    double* u_dev = nullptr;
+    int64_t* idx_dev = nullptr;
+    int* warn_dev = nullptr;
+    const int64_t nb = seed_blocks(n);
+    CK(cudaMallocAsync((void**)&D2, (size_t)n * sizeof(double), s));
+    CK(cudaMallocAsync((void**)&ps, (size_t)nb * sizeof(double), s));
+    CK(cudaMallocAsync((void**)&u_dev, (size_t)k * sizeof(double), s));
+    CK(cudaMallocAsync((void**)&idx_dev, (size_t)k * sizeof(int64_t), s));
+    CK(cudaMallocAsync((void**)&warn_dev, sizeof(int), s));
+    CK(cudaMemcpyAsync(u_dev, u, (size_t)k * sizeof(double), cudaMemcpyHostToDevice, s));
+    int64_t first = (int64_t)(u[0] * (double)n);   // Alg 1 line 1 (reading R6)
+    if (first > n - 1) first = n - 1;
+    CK(cudaMemcpyAsync(idx_dev, &first, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(warn_dev, 0, sizeof(int), s));
+    CK(launch_seed_d2(h->work, h->dist, h->Xl, n, h->d, h->d_pad, h->xn, h->sx, h->guard, k,
+                      u_dev, idx_dev, D2, ps, warn_dev, s));
+    int warn = 0;
+    CK(cudaMemcpyAsync(indices, idx_dev, (size_t)k * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&warn, warn_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    cudaFreeAsync(D2, s);
+    cudaFreeAsync(ps, s);
+    cudaFreeAsync(u_dev, s);
+    cudaFreeAsync(idx_dev, s);
+    cudaFreeAsync(warn_dev, s);
+    CK(cudaStreamSynchronize(s));
+    return warn ? KMEANS_WARN_SEED_UNIFORM : KMEANS_OK;
 }
 
 int kmeans_set_delta(kmeans_handle h, double delta) {
