@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-simt", action="store_true")
+    ap.add_argument("--seed-d2", action="store_true",
+                    help="time D^2 seeding (kmeans_seed_d2, Alg 1 in u_l) instead of the fit; "
+                         "value = seeding rounds/s, roofline against HBM")
     ap.add_argument("--delta", type=float, default=None,
                     help="Alg 4/5 per-pair precision switch (kmeans_set_delta); not the default "
                          "workload: reports eta and the CUDA-core mixed kernel's roofline")
@@ -162,6 +165,42 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_seed_bench(args, mpk, h, Xd, n, d, k, cfg, dist, stream, torch):
+    """D^2 seeding (Alg 1 in u_l): K steps of a full k-centre seeding of the config's X."""
+    import numpy as np
+    rng = np.random.default_rng(0)
+    u = rng.random(k)
+    for _ in range(max(3, args.warmup)):
+        mpk.kmeans_seed_d2(h, Xd, u)
+    torch.cuda.synchronize()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            mpk.kmeans_seed_d2(h, Xd, u)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    rounds = (k - 1) * args.steps
+    es = {"fp16": 2, "bf16": 2, "e5m2": 1, "fp32": 4, "fp64": 8}[dist]
+    d_pad = ((d * es + 127) // 128) * 128 // es if d * es > 64 else d
+    bytes_per_round = n * d_pad * es + 16 * n       # X~ read, D2 read + write
+    peaks, src = load_peaks()
+    achieved = bytes_per_round * rounds / (ms / 1e3) / 1e9
+    line = {"metric": "D^2 seeding rounds/s (Alg 1 in u_l)", "value": rounds / (ms / 1e3),
+            "unit": "rounds/s", "n_gpus": 1, "steps": args.steps, "warmup": max(3, args.warmup),
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": dist, "data": "synthetic (seeded Gaussian blobs)",
+            "config": {"workload": args.config, "n": n, "d": d, "k": k, "dist": dist,
+                       "norm": cfg.norms[0], "rounds_per_step": k - 1},
+            "roofline": {"kernel": "seed_update_kernel + seed_pick_kernel", "bound": "hbm",
+                         "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                         "algorithmic_per_round": f"n*d_pad*s_l + 16n = {bytes_per_round:.4e} B"},
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
 def traffic_from_profiles(workload, dist):
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
@@ -219,6 +258,13 @@ def main():
 
     def step():
         return mpk.kmeans_fit(h, Xd, Cd, args.iters, -1.0, labels, cent)
+
+    if args.seed_d2:
+        if world > 1:
+            raise SystemExit("--seed-d2 runs on one GPU (kmeans_seed_d2 is single-GPU)")
+        run_seed_bench(args, mpk, h, Xd, n_local, d, k, cfg, dist, stream, torch)
+        mpk.kmeans_destroy(h)
+        return
 
     for _ in range(max(3, args.warmup)):
         step()
