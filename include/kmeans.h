@@ -106,6 +106,13 @@ typedef struct kmeans_stats {
     int64_t n_dist_low;                  /* of which in low precision: all of them unless
                                             kmeans_set_delta is on (then eq:xi-low-prec-ratio's
                                             eta = n_dist_low / n_dist)     */
+    double u_bound_t[KMEANS_MAX_TRACE];  /* Thm 5.3 (eq:center-update-prec):
+                                            min over the clusters that moved in iteration t of
+                                            |c^-mu^|^T|c^-mu^| / (2 |c^-mu^|^T |mu^|), the
+                                            largest unit roundoff of the centre update that
+                                            still cannot stall the iteration (+inf: none moved)*/
+    int32_t n_update_prec_short;         /* iterations with u_bound_t below the working
+                                            precision's unit roundoff (2^-24 / 2^-53)          */
 } kmeans_stats;
 
 /*

@@ -50,7 +50,7 @@ def _load():
             lib.oracle_normalize_stats.argtypes = [i32, i64, i32, P, P, P]
             lib.oracle_normalize_apply.argtypes = [i32, i64, i32, P, P, P, P]
             lib.oracle_fit.argtypes = [i64, i32, i32, i32, i32, i32, P, P, i32, dbl, P, P, P, P,
-                                       P, P, P, P, P, P, dbl, P]
+                                       P, P, P, P, P, P, dbl, P, P]
             lib.oracle_step.argtypes = [i64, i32, i32, i32, i32, i32, P, P, P, P, P, P, P, P,
                                         dbl, P]
             lib.oracle_assign.argtypes = [i64, i32, i32, i32, i32, i32, P, P, P, P, P, dbl, P]
@@ -141,16 +141,17 @@ def fit(X, C0, work="fp64", dist="fp64", norm="none", guard=False, max_iter=300,
     tr_sse, tr_ch = np.zeros(max_iter), np.zeros(max_iter, np.int64)
     tr_sh, tr_em = np.zeros(max_iter), np.zeros(max_iter, np.int32)
     n_low = ct.c_int64()
+    tr_ub = np.zeros(max_iter)
     rc = lib.oracle_fit(n, d, k, _prec(work), _prec(dist), _flags(norm, guard), _p(X), _p(C0),
                         max_iter, tol, _p(labels), _p(cent), ct.byref(sse), ct.byref(iters),
                         _p(shift), _p(scale), _p(tr_sse), _p(tr_ch), _p(tr_sh), _p(tr_em),
-                        float(delta or 0.0), ct.byref(n_low))
+                        float(delta or 0.0), ct.byref(n_low), _p(tr_ub))
     if rc != 0:
         raise ValueError(f"oracle_fit rc={rc}")
     it = iters.value
     return dict(labels=labels, centroids=cent, sse=sse.value, iters=it, shift=shift,
                 scale=scale, sse_t=tr_sse[:it], changed_t=tr_ch[:it], shift2_t=tr_sh[:it],
-                empty_t=tr_em[:it], n_low=n_low.value)
+                empty_t=tr_em[:it], n_low=n_low.value, u_bound_t=tr_ub[:it])
 
 
 def step(X, C, work="fp32", dist="fp16", guard=False, delta=None):

@@ -30,6 +30,7 @@
  *                             SSE by eq:dist-eval-alternative PAPER.md:189-192
  *   O4m Alg 4 / Alg 5         per-pair precision switch eq:prec-delta PAPER.md:613-645, 684-699
  *   O10 seeding               Alg 1 (D^2 weighting) PAPER.md:150-161 in u_l (Alg 3 step 1)
+ *   O11 update precision      Thm 5.3 eq:center-update-prec PAPER.md:487-493
  *
  * Parity pins live in tests/test_oracle_*.py; nothing here is "parity unpinned".
  */
@@ -250,6 +251,26 @@ static int64_t assign_all(ostate_t* S, int32_t* labels, double* dmin, double* d2
 }
 
 /* O7: sums (compensated fp64 in index order), counts, means rounded to u; empty -> keep.     */
+/* O11: Thm 5.3 (eq:center-update-prec) for one update: over the clusters   */
+/* whose centre moved, min of |c^ - mu^|^T |c^ - mu^| / (2 |c^ - mu^|^T |mu^|) with c^ the     */
+/* previous and mu^ the new (computed) centre; +inf when no centre moved.                      */
+static double center_update_bound(int k, int d, const double* Cprev, const double* Cnew) {
+    double best = INFINITY;
+    for (int j = 0; j < k; ++j) {
+        double num = 0.0, den = 0.0;
+        for (int t = 0; t < d; ++t) {
+            double df = Cprev[(int64_t)j * d + t] - Cnew[(int64_t)j * d + t];
+            num += df * df;
+            den += fabs(df) * fabs(Cnew[(int64_t)j * d + t]);
+        }
+        if (num > 0.0 && den > 0.0) {
+            double b = num / (2.0 * den);
+            if (b < best) best = b;
+        }
+    }
+    return best;
+}
+
 static void update_centroids(ostate_t* S, const int32_t* labels, double* sums_out,
                              int64_t* counts_out, double* shift2, int* n_empty) {
     int d = S->d, k = S->k;
@@ -372,7 +393,7 @@ int oracle_fit(int64_t n, int d, int k, int work, int dist, int flags, const dou
                const double* C0_in, int max_iter, double tol, int32_t* labels_out,
                double* C_out, double* sse_out, int32_t* iters_out, double* shift_out,
                double* scale_out, double* tr_sse, int64_t* tr_changed, double* tr_shift2,
-               int32_t* tr_empty, double delta, int64_t* n_trig_out) {
+               int32_t* tr_empty, double delta, int64_t* n_trig_out, double* tr_ubound) {
     if (check_args(n, d, k, work, dist, flags) != 0 || max_iter < 1 || k > n) return -1;
     int norm = flags & ONORM_MASK, guard = (flags & OGUARD) != 0;
     ostate_t S;
@@ -409,7 +430,13 @@ int oracle_fit(int64_t n, int d, int k, int work, int dist, int flags, const dou
             prev[i] = lab[i];
         }
         double shift2; int empty;
+        double* Cprev = tr_ubound ? (double*)malloc(sizeof(double) * k * d) : NULL;
+        if (Cprev) memcpy(Cprev, S.C, sizeof(double) * k * d);
         update_centroids(&S, lab, NULL, NULL, &shift2, &empty);   /* O7 */
+        if (Cprev) {
+            tr_ubound[it - 1] = center_update_bound(k, d, Cprev, S.C);   /* O11 */
+            free(Cprev);
+        }
         if (tr_sse) tr_sse[it - 1] = nsum_get(&sse);
         if (tr_changed) tr_changed[it - 1] = changed;
         if (tr_shift2) tr_shift2[it - 1] = shift2;

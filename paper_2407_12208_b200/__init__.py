@@ -51,7 +51,8 @@ class kmeans_stats(ct.Structure):
                 ("empty_t", ct.c_int32 * KMEANS_MAX_TRACE),
                 ("n_kernel_launches", ct.c_int64), ("n_final_fallback", ct.c_int64),
                 ("n_final_uncertified", ct.c_int64), ("n_dist", ct.c_int64),
-                ("n_dist_low", ct.c_int64)]
+                ("n_dist_low", ct.c_int64), ("u_bound_t", ct.c_double * KMEANS_MAX_TRACE),
+                ("n_update_prec_short", ct.c_int32)]
 
 
 def _load():
@@ -226,6 +227,7 @@ def stats_dict(st: kmeans_stats) -> dict:
                 t_finalize_ms=st.t_finalize_ms, t_allreduce_ms=st.t_allreduce_ms,
                 sse_t=list(st.sse_t[:t]), shift2_t=list(st.shift2_t[:t]),
                 changed_t=list(st.changed_t[:t]), empty_t=list(st.empty_t[:t]),
+                u_bound_t=list(st.u_bound_t[:t]), n_update_prec_short=st.n_update_prec_short,
                 n_kernel_launches=st.n_kernel_launches, n_final_fallback=st.n_final_fallback,
                 n_final_uncertified=st.n_final_uncertified, n_dist=st.n_dist,
                 n_dist_low=st.n_dist_low,

@@ -36,6 +36,10 @@ struct IterRec {
     double shift2;
     double changed;
     double empty;
+    // Thm 5.3 (eq:center-update-prec): max over clusters that moved of
+    // 2 |c^ - mu^|^T |mu^| / |c^ - mu^|^T |c^ - mu^|; the bound on the update's unit roundoff
+    // is its reciprocal (0 = no cluster moved: no constraint)
+    double ub_inv;
 };
 
 // Device-side problem description passed to kernels by value.
@@ -159,10 +163,17 @@ cudaError_t launch_cand_exact(const float* Xw, const float* Cw, const float* cn,
                               int cand_q, int32_t* labels, int* left_count, int* left_rows,
                               unsigned long long* keys, cudaStream_t s);
 
-// K7: update = bucket by label (count, scan, scatter) + segmented fp64 sums.
+// K7: update = stable bucket sort by label (block counts, scan, scatter) + segmented fp64 sums
+// with an ordered reduction of the chunk-boundary partials: bit-reproducible for k <= 12288.
+struct UpdateScratch {
+    int* cb = nullptr;          // per-(label, 4096-row block) counts / offsets
+    double* part = nullptr;     // piece sums of clusters longer than one segsum piece (d each)
+    int* mpo = nullptr;         // k + 1 first-slot offsets into part
+};
+size_t update_scratch_bytes(int64_t n, int d, int k, size_t* cb, size_t* part, size_t* mpo);
 cudaError_t launch_update(int work, const void* Xw, int64_t n, int d, int k,
                           const int32_t* labels, int* cnt, int* offs, int* cursor, int* perm,
-                          double* acc, AccLayout L, cudaStream_t s);
+                          double* acc, AccLayout L, const UpdateScratch& us, cudaStream_t s);
 
 // K8: finalize: C = round_u(sum / count) (empty -> keep), shift^2, empty count, trace record.
 cudaError_t launch_finalize(int work, int64_t k, int d, const double* acc, AccLayout L,

@@ -1,13 +1,19 @@
 // k_update.cu — K7 centroid update and K8 finalize (eq:center, in the working
 // precision u: Alg 3 step 4).
 //
-// K7 is a bucket-by-label update that needs no floating-point atomics on the hot rows:
-//   U1 count   : block-privatised int histogram of the labels (smem) -> global counts
+// K7 is a stable bucket-by-label update with no floating-point atomics, so the new centres are
+// bit-for-bit the same on every run (k <= kHistMax; above it U1/U3 fall back to atomic slot
+// claims and the order inside a cluster may vary):
+//   U1 count   : per-8192-row-block label histograms (smem) -> CB, then a per-label scan over the
+//                blocks (the block offsets inside the cluster's bucket, and the counts)
 //   U2 scan    : exclusive prefix sum of the k counts -> bucket offsets (one block)
-//   U3 scatter : warp-aggregated (__match_any_sync) slot claims -> perm[] = rows grouped by label
-//   U4 segsum  : each warp streams a contiguous chunk of perm[], lanes over columns, summing the
-//                gathered rows in fp64 registers; a flush (one fp64 atomic per column) happens
-//                only where the label changes inside the chunk (~1-2 per chunk).
+//   U3 scatter : stable in-block ranks (__match_any_sync, warps in row order) -> perm[] = rows
+//                grouped by label, in increasing row index inside each label
+//   U4 segsum  : each bucket is cut into pieces of P rows from its start; warps stream the pieces
+//                starting in their chunk of perm[], lanes over columns, summing the gathered
+//                rows in fp64 registers; one-piece clusters are stored directly, longer ones
+//                per piece, and U4b adds a cluster's pieces in a fixed order. A cluster's sum
+//                then depends on its members only (same members -> bit-identical centre).
 // Sums are therefore accumulated in fp64 (at least the working precision u; DESIGN.md reading
 // on update precision) and the mean is rounded once to u in K8. X is read exactly once, in
 // whole rows (coalesced 16-byte vector loads), so U4 is HBM-bound.
@@ -44,66 +50,192 @@ __global__ void count_kernel(const int32_t* __restrict__ labels, int64_t n, int 
 }
 
 // Single-block exclusive scan of k counts (k arbitrary): chunked by 1024 with a running carry.
-__global__ void scan_kernel(const int* __restrict__ cnt, int k, int* __restrict__ offs,
-                            int* __restrict__ cursor, double* __restrict__ acc_counts) {
-    __shared__ int sh[1024];
-    __shared__ int carry;
-    if (threadIdx.x == 0) carry = 0;
+// A second scan over the same chunks gives mpo[j], the first partial-sum slot of cluster j when
+// it spans several segsum pieces of P rows (ceil(cnt_j / P) >= 2 slots; else 0 slots).
+__global__ void scan_kernel(const int* __restrict__ cnt, int k, int64_t P, int* __restrict__ offs,
+                            int* __restrict__ cursor, int* __restrict__ mpo,
+                            double* __restrict__ acc_counts) {
+    __shared__ int sh[1024], sh2[1024];
+    __shared__ int carry, carry2;
+    if (threadIdx.x == 0) carry = carry2 = 0;
     __syncthreads();
     for (int base = 0; base < k; base += 1024) {
         int j = base + threadIdx.x;
         int v = j < k ? cnt[j] : 0;
+        const int np = (int)((v + P - 1) / P);
+        int v2 = np >= 2 ? np : 0;
         sh[threadIdx.x] = v;
+        sh2[threadIdx.x] = v2;
         __syncthreads();
         for (int o = 1; o < 1024; o <<= 1) {
             int t = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
+            int t2 = threadIdx.x >= o ? sh2[threadIdx.x - o] : 0;
             __syncthreads();
             sh[threadIdx.x] += t;
+            sh2[threadIdx.x] += t2;
             __syncthreads();
         }
         if (j < k) {
             int ex = carry + sh[threadIdx.x] - v;
             offs[j] = ex;
             cursor[j] = ex;
+            mpo[j] = carry2 + sh2[threadIdx.x] - v2;
             acc_counts[j] = (double)v;
         }
         __syncthreads();
-        if (threadIdx.x == 1023) carry += sh[1023];
+        if (threadIdx.x == 1023) { carry += sh[1023]; carry2 += sh2[1023]; }
         __syncthreads();
     }
-    if (threadIdx.x == 0) offs[k] = carry;
+    if (threadIdx.x == 0) { offs[k] = carry; mpo[k] = carry2; }
 }
 
-// U3 (k <= kHistMax): block-aggregated slot claims. Each block ranks its rows per label in a
-// shared-memory histogram (integer smem atomics), reserves one contiguous range per label with
-// a single global atomic, then writes perm. Global atomics drop from one per row to one per
-// (block, label present).
-constexpr int kScatterRows = 16;
-__global__ void __launch_bounds__(256)
-scatter_block_kernel(const int32_t* __restrict__ labels, int64_t n, int k,
-                     int* __restrict__ cursor, int* __restrict__ perm) {
-    extern __shared__ int sh[];
-    const int64_t base = (int64_t)blockIdx.x * blockDim.x * kScatterRows;
-    for (int j = threadIdx.x; j < k; j += blockDim.x) sh[j] = 0;
+// Deterministic U1/U3 (k <= kHistMax): rows are taken in blocks of kDetRows; a row's slot is
+//   offs[l] + (rows with label l in earlier blocks) + (rows with label l earlier in its block),
+// i.e. perm lists each cluster's rows in increasing row index — a stable bucket sort, the same
+// on every run (only integer counts use atomics, and counts do not depend on order).
+constexpr int kDetThreads = 512;
+constexpr int kDetRows = 8192;                    // rows per counting / scatter block
+
+// U1a: per-block label histogram -> CB[b * k + l] (block-major: coalesced stores).
+__global__ void __launch_bounds__(kDetThreads)
+block_count_kernel(const int32_t* __restrict__ labels, int64_t n, int k, int* __restrict__ CB) {
+    extern __shared__ int hist[];
+    for (int j = threadIdx.x; j < k; j += blockDim.x) hist[j] = 0;
     __syncthreads();
-    int lab[kScatterRows], rk[kScatterRows];
-#pragma unroll
-    for (int r = 0; r < kScatterRows; ++r) {
-        const int64_t i = base + (int64_t)r * blockDim.x + threadIdx.x;
-        lab[r] = i < n ? labels[i] : -1;
+    const int64_t base = (int64_t)blockIdx.x * kDetRows;
+#pragma unroll 4
+    for (int r = 0; r < kDetRows / kDetThreads; ++r) {
+        const int64_t i = base + (int64_t)r * kDetThreads + threadIdx.x;
+        if (i < n) atomicAdd(&hist[labels[i]], 1);
     }
+    __syncthreads();
+    int* out = CB + (int64_t)blockIdx.x * k;
+    for (int j = threadIdx.x; j < k; j += blockDim.x) out[j] = hist[j];
+}
+
+// U1b: exclusive scan of CB[., l] over the blocks in order (in place) and the counts. A CTA takes
+// 32 labels (lanes) and its 32 warps take consecutive segments of blocks: segment totals,
+// a scan of the 32 totals, then the segments rewritten with their offsets.
+__global__ void __launch_bounds__(1024)
+block_scan_kernel(int* __restrict__ CB, int64_t nb, int k, int* __restrict__ cnt) {
+    __shared__ int tot[32][33];
+    const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
+    const int l = blockIdx.x * 32 + lane;
+    const int64_t per = (nb + 31) / 32;
+    const int64_t b0 = seg * per, b1 = min(nb, b0 + per);
+    int sum = 0;
+    if (l < k)
+        for (int64_t b = b0; b < b1; ++b) sum += CB[b * k + l];
+    tot[seg][lane] = sum;
+    __syncthreads();
+    if (seg == 0) {
+        int run = 0;
+        for (int s2 = 0; s2 < 32; ++s2) {
+            const int v = tot[s2][lane];
+            tot[s2][lane] = run;
+            run += v;
+        }
+        if (l < k) cnt[l] = run;
+    }
+    __syncthreads();
+    if (l < k) {
+        int run = tot[seg][lane];
+        for (int64_t b = b0; b < b1; ++b) {
+            const int v = CB[b * k + l];
+            CB[b * k + l] = run;
+            run += v;
+        }
+    }
+}
+
+// U3: stable in-block ranks without a serial chain. The block's rows are split among its warps
+// in contiguous spans (warp w: rows [w * span, (w + 1) * span)).
+//   1. each warp walks its span in rounds of 32 rows (__syncwarp between rounds orders its
+//      shared-memory updates): a round's lanes with equal labels take consecutive ranks from the
+//      warp's own histogram H[w][.] -> rank of the row among the span's earlier rows with its label
+//   2. per label, an exclusive scan of H[.][l] over the warps
+//   3. slot = offs[l] + CB[b][l] + H[w][l] + rank (ranks kept in shared memory)
+// Warps per block = scatter_warps(k) keeps H within kDetHistBytes.
+constexpr int kDetHistBytes = 64 * 1024;
+int scatter_warps(int k) {
+    int w = 16;
+    while (w > 1 && (size_t)w * k * sizeof(int) > (size_t)kDetHistBytes) w >>= 1;
+    return w;
+}
+size_t scatter_smem(int k) {
+    return (size_t)scatter_warps(k) * k * sizeof(int) + (size_t)kDetRows * sizeof(int);
+}
+
+// Lanes holding the same key (0 <= key < 2^bits): the AND of one ballot per key bit. Cheaper than
+// __match_any_sync, whose cost grows with the number of distinct values in the warp.
+MPK_DEV unsigned match_bits(int key, int bits) {
+    unsigned m = 0xffffffffu;
+    for (int b = 0; b < bits; ++b) {
+        const bool on = (key >> b) & 1;
+        const unsigned bal = __ballot_sync(0xffffffffu, on);
+        m &= on ? bal : ~bal;
+    }
+    return m;
+}
+
+__global__ void __launch_bounds__(kDetThreads)
+scatter_det_kernel(const int32_t* __restrict__ labels, int64_t n, int k,
+                   const int* __restrict__ offs, const int* __restrict__ CB,
+                   int* __restrict__ perm) {
+    const int kbits = 32 - __clz(k);              // keys l + 1 in [0, k]
+    extern __shared__ int smem_i[];
+    const int nwarps = blockDim.x >> 5;
+    int* H = smem_i;                              // [nwarps][k]
+    int* rk = smem_i + (size_t)nwarps * k;        // [kDetRows]
+    for (int j = threadIdx.x; j < nwarps * k; j += blockDim.x) H[j] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int span = kDetRows / nwarps;
+    const int64_t b0 = (int64_t)blockIdx.x * kDetRows;
+    int* Hw = H + (size_t)warp * k;
+    const unsigned lt = (1u << lane) - 1u;
+    // span is a multiple of 512: labels are fetched 16 rounds at a time, ahead of the ordered
+    // walk (the walk's shared-memory updates would otherwise serialise the global loads)
+    for (int g = warp * span; g < (warp + 1) * span; g += 512) {
+        int lb[16];
 #pragma unroll
-    for (int r = 0; r < kScatterRows; ++r) rk[r] = lab[r] >= 0 ? atomicAdd(&sh[lab[r]], 1) : 0;
+        for (int u = 0; u < 16; ++u) {
+            const int64_t i = b0 + g + u * 32 + lane;
+            lb[u] = i < n ? labels[i] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int l = lb[u];
+            const unsigned peers = match_bits(l + 1, kbits);
+            const int leader = __ffs(peers) - 1;
+            int base = 0;
+            if (l >= 0 && lane == leader) {       // H[w] is this warp's alone: plain update
+                base = Hw[l];
+                Hw[l] = base + __popc(peers);
+            }
+            base = __shfl_sync(0xffffffffu, base, leader);
+            rk[g + u * 32 + lane] = base + __popc(peers & lt);
+            __syncwarp();
+        }
+    }
     __syncthreads();
     for (int j = threadIdx.x; j < k; j += blockDim.x) {
-        const int c = sh[j];
-        if (c) sh[j] = atomicAdd(&cursor[j], c);
+        int run = 0;
+        for (int w = 0; w < nwarps; ++w) {
+            const int t = H[(size_t)w * k + j];
+            H[(size_t)w * k + j] = run;
+            run += t;
+        }
     }
     __syncthreads();
-#pragma unroll
-    for (int r = 0; r < kScatterRows; ++r) {
-        const int64_t i = base + (int64_t)r * blockDim.x + threadIdx.x;
-        if (lab[r] >= 0) perm[sh[lab[r]] + rk[r]] = (int)i;
+    const int* cb = CB + (int64_t)blockIdx.x * k;
+#pragma unroll 8
+    for (int r = warp * span + lane; r < (warp + 1) * span; r += 32) {
+        const int64_t i = b0 + r;
+        if (i < n) {
+            const int l = labels[i];
+            perm[offs[l] + cb[l] + Hw[l] + rk[r]] = (int)i;
+        }
     }
 }
 
@@ -149,119 +281,170 @@ MPK_DEV void load_vec(const W* p, bool aligned, int ncols, W (&out)[VEC]) {
     }
 }
 
-// U4: warps own contiguous chunks of perm; grid.y = column blocks of 32*VEC.
+// U4: each cluster's bucket is cut into pieces of P rows counted from the bucket's start, and a
+// warp sums the pieces whose first row lies in its chunk of C rows of perm (one wave of warps,
+// each reading fewer than C + P rows); grid.y = column blocks of 32*VEC. A piece's rows are
+// added in bucket order (increasing row index, U3), in batches of U rows aligned to the piece
+// start, so every sum depends only on the cluster's members — not on where other clusters'
+// buckets end — and a cluster whose members do not change gets bit-identical sums. A
+// one-piece cluster is stored directly; the pieces of longer ones go to slots mpo[j] + p, added
+// in a fixed order by U4b. No floating-point atomics.
 template <typename W, int VEC, int U>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)   // 4 blocks/SM: the 32-warps-per-SM grid is one wave
 segsum_kernel(const W* __restrict__ X, int64_t n, int d, int k, const int* __restrict__ perm,
-              const int* __restrict__ offs, int64_t chunk, double* __restrict__ sums) {
+              const int* __restrict__ offs, const int* __restrict__ mpo, int64_t P, int64_t C,
+              double* __restrict__ sums, double* __restrict__ part) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int col0 = blockIdx.y * 32 * VEC + lane * VEC;
     const int ncols = max(0, min(VEC, d - col0));
     const bool aligned = (d % VEC) == 0;
-    int64_t e0 = warp * chunk;
+    const int64_t e0 = warp * C;
     if (e0 >= n) return;
-    int64_t e1 = min(n, e0 + chunk);
-    // label of entry e0: largest j with offs[j] <= e0 (binary search over k+1 offsets)
+    const int64_t e1 = min(n, e0 + C);
+    // the cluster holding entry e0: largest j with offs[j] <= e0 (binary search over k+1 offsets)
     int lo = 0, hi = k;   // offs[0] = 0 <= e0 < offs[k] = n
     while (hi - lo > 1) {
         int mid = (lo + hi) >> 1;
         if (offs[mid] <= e0) lo = mid; else hi = mid;
     }
-    int cur = lo;
-    int64_t next_boundary = offs[cur + 1];
-    double acc[VEC];
+    int j = lo;
+    // first piece of cluster j starting at or after e0
+    int64_t pidx = (e0 - offs[j] + P - 1) / P;
+    int64_t ps = offs[j] + pidx * P;
+    for (;;) {
+        if (ps >= offs[j + 1]) {            // past cluster j: next non-empty cluster's piece 0
+            do { ++j; } while (j < k && offs[j] == offs[j + 1]);
+            if (j >= k) break;
+            pidx = 0;
+            ps = offs[j];
+        }
+        if (ps >= e1) break;
+        const int64_t pe = min((int64_t)offs[j + 1], ps + P);
+        double acc[VEC];
 #pragma unroll
-    for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
-
-    auto flush = [&](int j) {
+        for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
+        for (int64_t e = ps; e < pe; e += 32) {
+            const int myrow = (e + lane < pe) ? perm[e + lane] : 0;
+            const int cnt = (int)min((int64_t)32, pe - e);
+            for (int u0 = 0; u0 < cnt; u0 += U) {
+                W xv[U][VEC];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int row = __shfl_sync(0xffffffffu, myrow, (u0 + u) & 31);
+                    if (u0 + u < cnt && ncols > 0)
+                        load_vec<W, VEC>(X + (int64_t)row * d + col0, aligned, ncols, xv[u]);
+                    else {
+#pragma unroll
+                        for (int q = 0; q < VEC; ++q) xv[u][q] = (W)0;
+                    }
+                }
+                if (u0 + U <= cnt) {
+                    // a full batch: sum the U rows in the working type first (one conversion to
+                    // fp64 per batch; the conversion unit, not HBM, bounded the per-row form)
+#pragma unroll
+                    for (int q = 0; q < VEC; ++q) {
+                        W sm = xv[0][q];
+#pragma unroll
+                        for (int u = 1; u < U; ++u) sm += xv[u][q];
+                        acc[q] += (double)sm;
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (u0 + u < cnt) {
+#pragma unroll
+                            for (int q = 0; q < VEC; ++q) acc[q] += (double)xv[u][q];
+                        }
+                }
+            }
+        }
+        const bool single = offs[j + 1] - offs[j] <= P;
+        double* dst = single ? sums + (int64_t)j * d : part + (int64_t)(mpo[j] + pidx) * d;
         if (ncols > 0) {
 #pragma unroll
             for (int q = 0; q < VEC; ++q)
-                if (q < ncols && acc[q] != 0.0) atomicAdd(&sums[(int64_t)j * d + col0 + q], acc[q]);
+                if (q < ncols) dst[col0 + q] = acc[q];
         }
-#pragma unroll
-        for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
-    };
-
-    for (int64_t e = e0; e < e1; e += 32) {
-        // lanes fetch up to 32 perm entries, then broadcast
-        int myrow = (e + lane < e1) ? perm[e + lane] : 0;
-        const int cnt = (int)min((int64_t)32, e1 - e);
-        for (int u0 = 0; u0 < cnt; u0 += U) {
-            W xv[U][VEC];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                int row = __shfl_sync(0xffffffffu, myrow, (u0 + u) & 31);
-                if (u0 + u < cnt && ncols > 0)
-                    load_vec<W, VEC>(X + (int64_t)row * d + col0, aligned, ncols, xv[u]);
-                else {
-#pragma unroll
-                    for (int q = 0; q < VEC; ++q) xv[u][q] = (W)0;
-                }
-            }
-            const int64_t elast = e + u0 + U - 1;
-            if (u0 + U <= cnt && elast < next_boundary) {
-                // common case: the whole batch belongs to the current cluster. Sum the U rows
-                // in the working type first (one conversion to fp64 per batch instead of per
-                // row; the conversion unit, not HBM, bounded the per-row form).
-#pragma unroll
-                for (int q = 0; q < VEC; ++q) {
-                    W s = xv[0][q];
-#pragma unroll
-                    for (int u = 1; u < U; ++u) s += xv[u][q];
-                    acc[q] += (double)s;
-                }
-            } else {
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (u0 + u < cnt) {
-                        int64_t epos = e + u0 + u;
-                        while (epos >= next_boundary) {   // label changes (warp-uniform)
-                            flush(cur);
-                            ++cur;
-                            next_boundary = offs[cur + 1];
-                        }
-#pragma unroll
-                        for (int q = 0; q < VEC; ++q) acc[q] += (double)xv[u][q];
-                    }
-                }
-            }
-        }
+        ++pidx;
+        ps += P;
     }
-    flush(cur);
+}
+
+// U4b: the pieces of each multi-piece cluster: a CTA per (cluster, 32-column block); warp w adds
+// pieces w, w + 8, ... in order (lanes over columns: coalesced), then lane sums the 8 warp
+// partials in warp order.
+__global__ void __launch_bounds__(256)
+segsum_fix_kernel(int d, const int* __restrict__ mpo, const double* __restrict__ part,
+                  double* __restrict__ sums) {
+    const int j = blockIdx.x;
+    const int np = mpo[j + 1] - mpo[j];
+    if (np == 0) return;
+    __shared__ double red[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int col = blockIdx.y * 32 + lane;
+    double sum = 0.0;
+    if (col < d) {
+        const double* pp = part + (int64_t)mpo[j] * d + col;
+#pragma unroll 4
+        for (int p = w; p < np; p += 8) sum += pp[(int64_t)p * d];
+    }
+    red[w][lane] = sum;
+    __syncthreads();
+    if (w == 0 && col < d) {
+        double t = red[0][lane];
+#pragma unroll
+        for (int q = 1; q < 8; ++q) t += red[q][lane];
+        sums[(int64_t)j * d + col] = t;
+    }
 }
 
 template <typename W>
 __global__ void finalize_kernel(int64_t k, int d, const double* __restrict__ acc, AccLayout L,
                                 W* __restrict__ C, IterRec* __restrict__ rec) {
+    // A7 (Alg 3 step 4's division, rounded once to u; empty clusters keep their centre) with one
+    // warp per cluster, which also yields Thm 5.3's per-cluster quantities:
+    //   num_j = |c^ - mu^|^T |c^ - mu^|  (the cluster's share of the shift ||C_t+1 - C_t||^2)
+    //   den_j = |c^ - mu^|^T |mu^|
+    // u must stay below num_j / (2 den_j); rec->ub_inv collects max_j 2 den_j / num_j.
     constexpr int WORK = sizeof(W) == 8 ? KMEANS_FP64 : KMEANS_FP32;
-    const int64_t total = k * d;
-    double sh = 0.0;
-    double empty = 0.0;
-    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        int64_t j = idx / d;
-        int t = (int)(idx - j * d);
-        double c = acc[L.counts() + j];
-        W old = C[idx];
-        W nw = old;
-        if (c > 0.0) nw = rounder<WORK>::from(acc[L.sums() + idx] / c);
-        else if (t == 0) empty += 1.0;
-        double df = (double)nw - (double)old;
-        sh += df * df;
-        C[idx] = nw;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double sh = 0.0, empty = 0.0, rmax = 0.0;
+    for (int64_t j = warp; j < k; j += nwarps) {
+        const double c = acc[L.counts() + j];
+        double num = 0.0, den = 0.0;
+        for (int t = lane; t < d; t += 32) {
+            const int64_t idx = j * d + t;
+            const W old = C[idx];
+            W nw = old;
+            if (c > 0.0) nw = rounder<WORK>::from(acc[L.sums() + idx] / c);
+            const double df = (double)nw - (double)old;
+            num += df * df;
+            den += fabs(df) * fabs((double)nw);
+            C[idx] = nw;
+        }
+        num = warp_sum(num);
+        den = warp_sum(den);
+        if (lane == 0) {
+            sh += num;
+            if (c == 0.0) empty += 1.0;
+            if (num > 0.0 && den > 0.0) rmax = fmax(rmax, 2.0 * den / num);
+        }
     }
-    sh = warp_sum(sh);
-    empty = warp_sum(empty);
-    __shared__ double red[2][8];
-    if ((threadIdx.x & 31) == 0) { red[0][threadIdx.x >> 5] = sh; red[1][threadIdx.x >> 5] = empty; }
+    __shared__ double red[3][8];
+    if (lane == 0) { red[0][threadIdx.x >> 5] = sh; red[1][threadIdx.x >> 5] = empty; red[2][threadIdx.x >> 5] = rmax; }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double a = 0.0, b = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += red[0][w]; b += red[1][w]; }
+        double a = 0.0, b = 0.0, r = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += red[0][w]; b += red[1][w]; r = fmax(r, red[2][w]); }
         atomicAdd(&rec->shift2, a);
         if (b != 0.0) atomicAdd(&rec->empty, b);
+        // non-negative doubles order like their bit patterns: a 64-bit atomicMax is a max
+        if (r > 0.0)
+            atomicMax(reinterpret_cast<unsigned long long*>(&rec->ub_inv),
+                      (unsigned long long)__double_as_longlong(r));
         if (blockIdx.x == 0) {
             rec->sse = acc[L.sse()];
             rec->changed = acc[L.changed()];
@@ -269,46 +452,62 @@ __global__ void finalize_kernel(int64_t k, int d, const double* __restrict__ acc
     }
 }
 
+// Segmented sums: pieces of kPiece rows (the unit whose sum depends only on the cluster's
+// members); warps take chunks of C >= kPiece rows of perm, one wave of 32 warps per SM.
+constexpr int64_t kPiece = 256;
+int64_t segsum_chunk(int64_t n) {
+    const int64_t warps = (int64_t)kNumSMs * 32;
+    return std::max<int64_t>(kPiece, (n + warps - 1) / warps);
+}
+
 template <typename W>
 cudaError_t update_dispatch(const W* X, int64_t n, int d, int k, const int32_t* labels, int* cnt,
                             int* offs, int* cursor, int* perm, double* acc, AccLayout L,
-                            cudaStream_t s) {
-    cudaError_t e = cudaMemsetAsync(cnt, 0, sizeof(int) * k, s);
-    if (e != cudaSuccess) return e;
+                            const UpdateScratch& us, cudaStream_t s) {
     int g = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 4);
     if (g < 1) g = 1;
-    size_t hist_bytes = k <= kHistMax ? sizeof(int) * k : 0;
-    count_kernel<<<g, 256, hist_bytes, s>>>(labels, n, k, cnt);
-    scan_kernel<<<1, 1024, 0, s>>>(cnt, k, offs, cursor, acc + L.counts());
-    if (k <= kHistMax) {
-        const int64_t sb = (n + 256LL * kScatterRows - 1) / (256LL * kScatterRows);
-        scatter_block_kernel<<<(unsigned)sb, 256, sizeof(int) * k, s>>>(labels, n, k, cursor, perm);
+    const bool det = k <= kHistMax;
+    const int64_t nb = (n + kDetRows - 1) / kDetRows;
+    if (det) {
+        block_count_kernel<<<(unsigned)nb, kDetThreads, sizeof(int) * k, s>>>(labels, n, k, us.cb);
+        block_scan_kernel<<<(unsigned)((k + 31) / 32), 1024, 0, s>>>(us.cb, nb, k, cnt);
     } else {
-        scatter_kernel<<<g, 256, 0, s>>>(labels, n, cursor, perm);
+        cudaError_t e = cudaMemsetAsync(cnt, 0, sizeof(int) * k, s);
+        if (e != cudaSuccess) return e;
+        count_kernel<<<g, 256, 0, s>>>(labels, n, k, cnt);
     }
-    // segmented sums: ~8 warps per SM-slot, chunks of >= 256 rows
+    const int64_t P = kPiece;
+    scan_kernel<<<1, 1024, 0, s>>>(cnt, k, P, offs, cursor, us.mpo, acc + L.counts());
+    if (det) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(scatter_det_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kDetHistBytes + kDetRows * (int)sizeof(int));
+            attr = true;
+        }
+        scatter_det_kernel<<<(unsigned)nb, 32 * scatter_warps(k), scatter_smem(k), s>>>(
+            labels, n, k, offs, us.cb, perm);
+    } else
+        scatter_kernel<<<g, 256, 0, s>>>(labels, n, cursor, perm);
     const int VEC = (sizeof(W) == 8) ? (d <= 32 ? 1 : 2) : (d <= 32 ? 1 : (d <= 64 ? 2 : 4));
     const int colblk = 32 * VEC;
     dim3 grid;
-    int64_t warps = (int64_t)kNumSMs * 32;
-    int64_t chunk = std::max<int64_t>(256, (n + warps - 1) / warps);
-    int64_t nw = (n + chunk - 1) / chunk;
+    const int64_t C = segsum_chunk(n);
+    const int64_t nw = (n + C - 1) / C;
     grid.x = (unsigned)((nw + 7) / 8);
     grid.y = (unsigned)((d + colblk - 1) / colblk);
     grid.z = 1;
+    double* sums = acc + L.sums();
+#define SEGSUM(V) segsum_kernel<W, V, 8><<<grid, 256, 0, s>>>(X, n, d, k, perm, offs, us.mpo, P, C, \
+                                                              sums, us.part)
     if constexpr (sizeof(W) == 8) {
-        if (VEC == 1)
-            segsum_kernel<W, 1, 8><<<grid, 256, 0, s>>>(X, n, d, k, perm, offs, chunk, acc + L.sums());
-        else
-            segsum_kernel<W, 2, 8><<<grid, 256, 0, s>>>(X, n, d, k, perm, offs, chunk, acc + L.sums());
+        if (VEC == 1) SEGSUM(1); else SEGSUM(2);
     } else {
-        if (VEC == 1)
-            segsum_kernel<W, 1, 8><<<grid, 256, 0, s>>>(X, n, d, k, perm, offs, chunk, acc + L.sums());
-        else if (VEC == 2)
-            segsum_kernel<W, 2, 8><<<grid, 256, 0, s>>>(X, n, d, k, perm, offs, chunk, acc + L.sums());
-        else
-            segsum_kernel<W, 4, 8><<<grid, 256, 0, s>>>(X, n, d, k, perm, offs, chunk, acc + L.sums());
+        if (VEC == 1) SEGSUM(1); else if (VEC == 2) SEGSUM(2); else SEGSUM(4);
     }
+#undef SEGSUM
+    segsum_fix_kernel<<<dim3((unsigned)k, (unsigned)((d + 31) / 32)), 256, 0, s>>>(d, us.mpo,
+                                                                                  us.part, sums);
     return cudaGetLastError();
 }
 
@@ -316,20 +515,29 @@ cudaError_t update_dispatch(const W* X, int64_t n, int d, int k, const int32_t* 
 
 cudaError_t launch_update(int work, const void* Xw, int64_t n, int d, int k,
                           const int32_t* labels, int* cnt, int* offs, int* cursor, int* perm,
-                          double* acc, AccLayout L, cudaStream_t s) {
-    launches_add(4);
+                          double* acc, AccLayout L, const UpdateScratch& us, cudaStream_t s) {
+    launches_add(6);
     if (work == KMEANS_FP64)
         return update_dispatch<double>((const double*)Xw, n, d, k, labels, cnt, offs, cursor,
-                                       perm, acc, L, s);
+                                       perm, acc, L, us, s);
     return update_dispatch<float>((const float*)Xw, n, d, k, labels, cnt, offs, cursor, perm, acc,
-                                  L, s);
+                                  L, us, s);
+}
+
+size_t update_scratch_bytes(int64_t n, int d, int k, size_t* cb, size_t* part, size_t* mpo) {
+    const int64_t nb = (n + kDetRows - 1) / kDetRows;
+    // clusters with >= 2 pieces have > P rows each: sum ceil(c_j / P) <= 2 n / P slots
+    const int64_t slots = 2 * ((n + kPiece - 1) / kPiece) + 1;
+    *cb = (size_t)(k <= kHistMax ? nb * k : 1) * sizeof(int);
+    *part = (size_t)slots * d * sizeof(double);
+    *mpo = (size_t)(k + 1) * sizeof(int);
+    return *cb + *part + *mpo;
 }
 
 cudaError_t launch_finalize(int work, int64_t k, int d, const double* acc, AccLayout L, void* Cw,
                             IterRec* rec, cudaStream_t s) {
     launches_add(1);
-    int64_t total = k * d;
-    int g = (int)std::min<int64_t>((total + 255) / 256, kNumSMs * 2);
+    int g = (int)std::min<int64_t>((k + 7) / 8, kNumSMs * 2);   // one warp per cluster
     if (g < 1) g = 1;
     if (work == KMEANS_FP64)
         finalize_kernel<double><<<g, 256, 0, s>>>(k, d, acc, L, (double*)Cw, rec);

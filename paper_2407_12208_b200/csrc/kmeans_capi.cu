@@ -40,6 +40,7 @@ struct kmeans_ctx {
     int32_t* labels = nullptr;     // n
     double* acc = nullptr;         // packed accumulator (AccLayout)
     int *cnt = nullptr, *offs = nullptr, *cursor = nullptr, *perm = nullptr;
+    UpdateScratch us;
     IterRec* trace = nullptr;      // KMEANS_MAX_TRACE records
     double* shift = nullptr;       // d (fp64)
     double* scale = nullptr;       // d (fp64)
@@ -169,7 +170,8 @@ void free_all(kmeans_ctx* h) {
         if (b) cudaFree(b);
     void* bufs[] = {h->Xw, h->xl_alias ? nullptr : h->Xl, h->xn, h->sx, h->Cw, h->Cl, h->cn,
                     h->sc, h->labels, h->acc, h->cnt, h->offs, h->cursor, h->perm, h->trace,
-                    h->shift, h->scale, h->partials, h->census, h->sse_dev};
+                    h->shift, h->scale, h->partials, h->census, h->sse_dev, h->us.cb,
+                    h->us.part, h->us.mpo};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
@@ -271,6 +273,13 @@ int create_impl(int64_t n, int32_t d, int32_t k, int work, int dist, int flags,
     CA(dalloc(&h->offs, (size_t)(k + 1) * sizeof(int)));
     CA(dalloc(&h->cursor, (size_t)k * sizeof(int)));
     CA(dalloc(&h->perm, (size_t)n * sizeof(int)));
+    {
+        size_t b_cb, b_part, b_pid;
+        update_scratch_bytes(n, d, k, &b_cb, &b_part, &b_pid);
+        CA(dalloc(&h->us.cb, b_cb));
+        CA(dalloc(&h->us.part, b_part));
+        CA(dalloc(&h->us.mpo, b_pid));
+    }
     CA(dalloc(&h->trace, (size_t)KMEANS_MAX_TRACE * sizeof(IterRec)));
     CA(dalloc(&h->shift, (size_t)d * sizeof(double)));
     CA(dalloc(&h->scale, (size_t)d * sizeof(double)));
@@ -607,7 +616,7 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
                 return rc;                                                   // A4
             if (timing) CK(cudaEventRecord(t1, s));
             CK(launch_update(h->work, h->Xw, n, d, k, h->labels, h->cnt, h->offs, h->cursor,
-                             h->perm, h->acc, h->L, s));                     // A5
+                             h->perm, h->acc, h->L, h->us, s));              // A5
             if (timing) CK(cudaEventRecord(t2, s));
         }
         if (h->comm)                                                         // A6
@@ -678,6 +687,8 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
         st.shift2_t[t] = tr[t].shift2;
         st.changed_t[t] = (int64_t)tr[t].changed;
         st.empty_t[t] = (int32_t)tr[t].empty;
+        st.u_bound_t[t] = tr[t].ub_inv > 0.0 ? 1.0 / tr[t].ub_inv : INFINITY;
+        if (st.u_bound_t[t] < (h->work == KMEANS_FP64 ? 0x1p-53 : 0x1p-24)) st.n_update_prec_short++;
         if (tr[t].empty > 0) any_empty = 1;
     }
     if (timing) {

@@ -286,3 +286,38 @@ def test_dist_handle_single_rank_matches_plain_handle():
     assert np.mean(outs[0][0] == outs[1][0]) > 0.999
     assert np.allclose(outs[0][1], outs[1][1], rtol=1e-5, atol=1e-6)
     assert abs(outs[0][2] - outs[1][2]) <= 1e-6 * outs[0][2]
+
+
+def test_center_update_bound_trace_matches_oracle():
+    """Thm 5.3's per-iteration bound (kmeans_stats.u_bound_t) against the oracle's O11 on the
+    same fit; the centres agree to the update's rounding, so the early (large-movement)
+    iterations agree closely."""
+    X, _, C0 = synth.make("c3_blobs_1m_d64", n=20011, seed=2)
+    C0 = C0[:32].copy()
+    ref = oracle.fit(X, C0, work="fp32", dist="fp32", norm="zscore", max_iter=6, tol=-1.0)
+    km = mpk.KMeans(len(X), 64, 32, "fp32", "fp32", norm="zscore")
+    km.fit(dev(X), dev(C0), max_iter=6, tol=-1.0)
+    st = km.stats()
+    km.close()
+    ub = np.array(st["u_bound_t"])
+    assert len(ub) == 6
+    np.testing.assert_allclose(ub[:3], ref["u_bound_t"][:3], rtol=1e-3)
+    assert st["n_update_prec_short"] == int(np.sum(ub < 2.0 ** -24))
+
+
+@pytest.mark.parametrize("work,dist,k", [("fp32", "fp16", 300), ("fp64", "fp64", 40),
+                                         ("fp32", "fp32", 1)])
+def test_update_is_bit_reproducible(work, dist, k):
+    """The update (stable bucket sort + ordered boundary reduction, no floating-point atomics)
+    gives bit-identical centres, labels and traces on repeated fits — clusters that span many
+    segsum chunks (k = 1) and many small clusters (k = 300) alike."""
+    X, _, _ = synth.make("c3_blobs_1m_d64", n=250007, seed=11)
+    X = X.astype(NP[work])
+    C0 = X[np.random.default_rng(k).choice(len(X), k, replace=False)].copy()
+    runs = [gpu_fit(X, C0, work, dist, norm="zscore", max_iter=5) for _ in range(3)]
+    for r in runs[1:]:
+        np.testing.assert_array_equal(r["centroids"], runs[0]["centroids"])
+        np.testing.assert_array_equal(r["labels"], runs[0]["labels"])
+        assert r["sse"] == pytest.approx(runs[0]["sse"], rel=1e-12)   # atomic fp64 SSE sum
+        assert r["stats"]["u_bound_t"] == runs[0]["stats"]["u_bound_t"]
+
