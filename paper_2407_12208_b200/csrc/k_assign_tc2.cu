@@ -34,6 +34,8 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 namespace mpk {
 namespace tcdev {
 
@@ -41,9 +43,6 @@ constexpr int P_BM = 128;
 constexpr int P_NON_EPI = 4;
 #ifndef MPK_PAIR_EWG
 #define MPK_PAIR_EWG 2
-#endif
-#ifndef MPK_PAIR_DBUF
-#define MPK_PAIR_DBUF 0                  // double-buffered TMEM loads (measured slower: 2.88 vs 2.77 ms)
 #endif
 constexpr int P_EWG = MPK_PAIR_EWG;      // epilogue warpgroups (split the columns)
 constexpr int P_EPI = 4 * P_EWG;
@@ -100,6 +99,8 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                    const __grid_constant__ CUtensorMap tmap_c, PairParams p) {
     constexpr bool FINAL = MODE == PAIR_FINAL;
     constexpr bool CAND = MODE == PAIR_CAND;
+    // ASSIGN: reverse column scan with 3-input minima (tc_common.cuh fold_rev_m3)
+    constexpr bool REV = MODE == PAIR_ASSIGN;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* b_base = smem;                                             // resident centroid halves
@@ -223,7 +224,9 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                         const bool tr = trace_me && ai < TRACE_T;
                         if (tr) trace[ai * 8 + 0] = clock64();
                         const uint32_t d_tmem = tmem_base + (uint32_t)buf * NB;
-                        const uint32_t b_lo = b_lo0 + t * b_half16;
+                        // ASSIGN visits the centroid tiles in reverse (fold_rev_m3)
+                        const int tb = REV ? NT - 1 - t : t;
+                        const uint32_t b_lo = b_lo0 + tb * b_half16;
                         if (!(dbg & 2)) {
                             for (int kb = 0; kb < KB; ++kb) {
                                 for (int ks = 0; ks < ksteps; ++ks) {
@@ -296,6 +299,9 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 }
                 const int64_t row = rb * rows_per_rb + rank * P_BM + q;
                 if (row >= n) continue;
+                // ||x||^2 not finite (a NaN / inf coordinate): every distance xn + v is NaN or
+                // +inf, and the scan's default is column 0 (the kernel's v omits xn)
+                if (!FINAL && !(xn_r[u] < INFINITY)) j1 = 0;
                 p.labels[row] = j1;
                 if (!FINAL) {
                     if (old_r[u] != j1) my_changed += 1.0;
@@ -377,11 +383,9 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 const bool tr = trace_me && ai < TRACE_T;
                 if (tr) trace[ai * 8 + 2] = clock64();
                 const uint32_t col0 = tmem_base + lane_addr + (uint32_t)buf * NB + col_off;
-                const int jbase = t * NB + col_off;
+                const int jbase = (REV ? NT - 1 - t : t) * NB + col_off;
                 if (!(dbg & 1)) {
-                    // 32-column chunks with the TMEM loads double-buffered: chunk i+1 is in
-                    // flight while chunk i folds (both warps of a sub-partition start a tile
-                    // together, so an unhidden load stalls the pair; measured ~150 cycles/chunk)
+                    // 32-column chunks (double-buffering the TMEM loads measured slower)
                     const int nch = wcols >> 5;
                     const int c = nch << 5;
                     auto fold = [&](const uint32_t (&vr)[32], int cc) {
@@ -399,27 +403,36 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                         }
                     };
                     uint32_t va[32];
-#if MPK_PAIR_DBUF
-                    uint32_t vb[32];
-                    if (nch > 0) tmem_ld32(col0, va);
-                    for (int i = 0; i < nch; i += 2) {
-                        tmem_wait_ld_dep(va);
-                        if (i + 1 < nch) tmem_ld32(col0 + (i + 1) * 32, vb);
-                        fold(va, i * 32);
-                        if (i + 1 < nch) {
-                            tmem_wait_ld_dep(vb);
-                            if (i + 2 < nch) tmem_ld32(col0 + (i + 2) * 32, va);
-                            fold(vb, (i + 1) * 32);
+                    if (REV) {
+                        // highest columns first: the 16-column remainder, then the chunks; each
+                        // chunk's ||c||^2 is loaded before its TMEM load (latencies overlap)
+                        auto rev_tile = [&](auto guard_tag) {
+                            constexpr bool GD = decltype(guard_tag)::value;
+                            if (c < wcols) {
+                                ChunkCn<2, GD> q;
+                                load_chunk_cn<2, GD>(cn_s, sc_s, jbase + c, q);
+                                tmem_ld16(col0 + c, va);
+                                tmem_wait_ld_dep(va);
+                                fold_rev_m3<2, GD>(va, q, m2, cv, s2);
+                            }
+                            for (int i = nch - 1; i >= 0; --i) {
+                                ChunkCn<4, GD> q;
+                                load_chunk_cn<4, GD>(cn_s, sc_s, jbase + i * 32, q);
+                                tmem_ld32(col0 + i * 32, va);
+                                tmem_wait_ld_dep(va);
+                                fold_rev_m3<4, GD>(va, q, m2, cv, s2);
+                            }
+                        };
+                        if (guard) rev_tile(std::true_type{});
+                        else rev_tile(std::false_type{});
+                    } else {
+                        for (int i = 0; i < nch; ++i) {
+                            tmem_ld32(col0 + i * 32, va);
+                            tmem_wait_ld_dep(va);
+                            fold(va, i * 32);
                         }
                     }
-#else
-                    for (int i = 0; i < nch; ++i) {
-                        tmem_ld32(col0 + i * 32, va);
-                        tmem_wait_ld_dep(va);
-                        fold(va, i * 32);
-                    }
-#endif
-                    if (c < wcols) {   // a 16-column remainder (wcols is a multiple of 16)
+                    if (!REV && c < wcols) {   // a 16-column remainder (wcols is a multiple of 16)
                         uint32_t va[32];
                         tmem_ld16(col0 + c, va);
                         tmem_wait_ld_dep(va);
@@ -465,14 +478,18 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             int jj[NCH];
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
-                const int v = chain_ordinal(cs[c], NT * gpt);
+                // REV: forward ordinal of the last improving visit = -1 - s (NT * gpt: never)
+                const int v = REV ? -1 - (int)cs[c] : chain_ordinal(cs[c], NT * gpt);
                 const int t = v >> gsh;
                 jj[c] = 8 * (t * (NB >> 3) + (col_off >> 3) + (v - t * gpt)) + c;
+                if (REV && v >= NT * gpt) jj[c] = 0x7FFFFFFF;
             }
             int w = 0;
             float b1;
             int j1;
             merge_chains(cv, jj, b1, j1, &w);
+            // no value below +inf: the forward scan's default column 0
+            if (REV && !(b1 < INFINITY)) j1 = 0;
             float b2 = INFINITY;
             if (FINAL) {
 #pragma unroll

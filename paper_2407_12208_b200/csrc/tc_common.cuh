@@ -262,6 +262,109 @@ MPK_DEV void fold32_x2(const uint32_t (&v)[32], const float* cn_s, const float* 
     }
 }
 
+// ---------------------------------------------------------------- reverse scan, 3-input minima
+// ASSIGN mode of the pair kernel visits the columns in DECREASING order (tiles, chunks and
+// groups reversed), so the sequential scan's "first column among equal minima" becomes "the
+// LAST visit among equal minima": a non-strict improvement. That lets one chain take two
+// columns per step with a single FMNMX3:
+//   v' = min(v, xa, xb)            (xa visited first = the larger column; FMNMX3: alu)
+//   na = (xa > v)  ? 1 : 0         (set.gtu: alu; NaN -> 1)
+//   nb = (xb > v') ? 1 : 0         (set.gtu: alu; xb <= min(v, xa) <=> xb == v', NaN -> 1)
+//   s  = (s * na - 1) * nb - 1     (two FFMA: fma pipe; packed over chains c, c+1)
+// i.e. 1.5 alu ops per distance instead of 2. s is minus the number of visits since (and
+// including) the chain's last improvement, so the forward ordinal of that visit is -1 - s
+// (== V, out of range, if the chain never improved: all its values NaN). min ignores a NaN
+// operand, so v never becomes NaN; NaN never improves. A chain whose minimum is +inf reports
+// some +inf column; the caller maps a +inf row minimum to column 0, the forward scan's
+// default, so results equal fold32_x2's.
+// xa2 / xb2: the (chain c, chain c+1) values of the first / second visited group.
+MPK_DEV void chain_pair_x2(uint64_t xa2, uint64_t xb2, float& va, float& vb, uint64_t& s2,
+                           uint64_t m1) {
+    asm("{\n\t"
+        ".reg .b64 na2, nb2;\n\t"
+        ".reg .f32 a0, a1, b0, b1, n0, n1, p0, p1, w0, w1;\n\t"
+        "mov.b64 {a0, a1}, %3;\n\t"
+        "mov.b64 {b0, b1}, %4;\n\t"
+        "min.f32 w0, %0, a0, b0;\n\t"
+        "min.f32 w1, %1, a1, b1;\n\t"
+        "set.gtu.f32.f32 n0, a0, %0;\n\t"
+        "set.gtu.f32.f32 n1, a1, %1;\n\t"
+        "set.gtu.f32.f32 p0, b0, w0;\n\t"
+        "set.gtu.f32.f32 p1, b1, w1;\n\t"
+        "mov.f32 %0, w0;\n\t"
+        "mov.f32 %1, w1;\n\t"
+        "mov.b64 na2, {n0, n1};\n\t"
+        "mov.b64 nb2, {p0, p1};\n\t"
+        "fma.rn.f32x2 %2, %2, na2, %5;\n\t"
+        "fma.rn.f32x2 %2, %2, nb2, %5;\n\t"
+        "}"
+        : "+f"(va), "+f"(vb), "+l"(s2)
+        : "l"(xa2), "l"(xb2), "l"(m1));
+}
+MPK_DEV uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+// ||c_j||^2 (and the guard scales s_j) of G groups of 8 columns, loaded into registers ahead of
+// the chunk's TMEM load so that the shared-memory latency overlaps the tcgen05.ld.
+template <int G, bool GUARD>
+struct ChunkCn {
+    float4 cc[2 * G];
+    float4 ss[GUARD ? 2 * G : 1];
+};
+template <int G, bool GUARD>
+MPK_DEV void load_chunk_cn(const float* cn_s, const float* sc_s, int j0, ChunkCn<G, GUARD>& q) {
+    const uint32_t cn_a = smem_u32(cn_s + j0);
+    const uint32_t sc_a = smem_u32(sc_s + j0);
+#pragma unroll
+    for (int e = 0; e < 2 * G; ++e) {
+        q.cc[e] = lds_f4(cn_a + 16 * e);
+        if (GUARD) q.ss[e] = lds_f4(sc_a + 16 * e);
+    }
+}
+// Fold G groups of 8 columns (j0 .. j0 + 8G - 1; G even) in reverse: group pairs (G-1, G-2),
+// ..., (1, 0). Each value is the same single-rounding fma(acc, -2 s_i s_j, ||c_j||^2) as in
+// fold32 / fold32_x2.
+template <int G, bool GUARD>
+MPK_DEV void fold_rev_m3(const uint32_t (&v)[32], const ChunkCn<G, GUARD>& q, float m2,
+                         float (&cv)[NCH], uint64_t (&s2)[NCH / 2]) {
+    static_assert(G % 2 == 0 && G <= 4, "group pairs");
+    const uint64_t m1 = pack2(-1.0f, -1.0f);
+    const uint64_t mm = pack2(-2.0f, -2.0f);
+#pragma unroll
+    for (int gp = G / 2 - 1; gp >= 0; --gp) {
+        uint64_t x2[2][4];                   // [a = group 2gp+1, b = group 2gp][chain pair]
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int g = 2 * gp + 1 - h;
+#pragma unroll
+            for (int qq = 0; qq < 2; ++qq) {
+                const int col = 8 * g + 4 * qq;      // columns col .. col+3 = chains 4qq .. 4qq+3
+                const float4 cc = q.cc[col / 4];
+                uint64_t s01 = mm, s23 = mm;
+                if (GUARD) {
+                    const float4 ss = q.ss[col / 4];
+                    s01 = pack2(m2 * ss.x, m2 * ss.y);
+                    s23 = pack2(m2 * ss.z, m2 * ss.w);
+                }
+                x2[h][2 * qq + 0] = fma2(pack2u(v[col + 0], v[col + 1]), s01, pack2(cc.x, cc.y));
+                x2[h][2 * qq + 1] = fma2(pack2u(v[col + 2], v[col + 3]), s23, pack2(cc.z, cc.w));
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < NCH / 2; ++m)
+            chain_pair_x2(x2[0][m], x2[1][m], cv[2 * m], cv[2 * m + 1], s2[m], m1);
+    }
+}
+template <int G, bool GUARD>
+MPK_DEV void fold_rev_m3(const uint32_t (&v)[32], const float* cn_s, const float* sc_s, float m2,
+                         int j0, float (&cv)[NCH], uint64_t (&s2)[NCH / 2]) {
+    ChunkCn<G, GUARD> q;
+    load_chunk_cn<G, GUARD>(cn_s, sc_s, j0, q);
+    fold_rev_m3<G, GUARD>(v, q, m2, cv, s2);
+}
+
 // Merge the chains of one point given each chain's column jj[c]: smallest value, then smallest
 // column (the sequential scan's result). Returns the winning chain in *w (for TOP2).
 MPK_DEV void merge_chains(const float (&cv)[NCH], const int (&jj)[NCH], float& b1, int& j1,

@@ -136,3 +136,56 @@ def test_final_pass_candidates_match_full_evaluation(dist, guard, monkeypatch):
     assert cand["n_final_fallback"] < 0.2 * cand["n_final_uncertified"]
     assert full["n_final_fallback"] == full["n_final_uncertified"]
     np.testing.assert_array_equal(labs[0], labs[1])
+
+
+@pytest.mark.parametrize("dist,guard", [("fp16", False), ("e5m2", False), ("bf16", True)])
+@pytest.mark.parametrize("k", [1024, 200])
+def test_tc_exact_ties_take_the_first_column(dist, guard, k):
+    """Duplicated centroids give bit-identical distances (same operands, same accumulation):
+    the argmin must take the FIRST of the tied columns (the sequential scan's rule, Alg 3 step 3,
+    PAPER.md:546), wherever the duplicates sit (same chain, same tile, other tiles). The ASSIGN
+    kernel scans columns in reverse (fold_rev_m3), so this pins its non-strict tie rule."""
+    n, d = 6000, 128
+    rng = np.random.default_rng(k)
+    C = rng.standard_normal((k, d)).astype(np.float32)
+    pairs = [(0, 8), (3, k - 1), (5, 13), (17, k // 2 + 1), (k // 2, k // 2 + 8), (40, 41)]
+    later = set()
+    for a, b in pairs:
+        C[b] = C[a]
+        later.add(b)
+    src = np.array([a for a, _ in pairs])
+    X = C[src[rng.integers(0, len(src), n)]] + 0.05 * rng.standard_normal((n, d)).astype(np.float32)
+    X[: n // 4] = rng.standard_normal((n // 4, d)).astype(np.float32)
+    km = mpk.KMeans(n, d, k, "fp32", dist, guard=guard)
+    mpk.kmeans_set_centroids(km.h, dev(C))
+    lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    km.assign(dev(X), lab)
+    km.close()
+    g = lab.cpu().numpy()
+    assert not np.isin(g, list(later)).any()
+    ref, _, _ = oracle.assign(X, C, work="fp32", dist=dist, guard=guard)
+    D, B = distances_on_rounded_operands(X, C, "fp32", dist, guard)
+    assert check_labels_admissible(g, ref, D, B) <= 2e-3
+
+
+@pytest.mark.parametrize("dist", ["fp16", "e5m2"])
+def test_tc_nonfinite_rows_match_the_scan(dist):
+    """Rows whose distances are all NaN / +inf take column 0 and rows with a -inf distance take
+    the first such column — the sequential scan's results, as the oracle computes them."""
+    n, d, k = 600, 64, 300
+    rng = np.random.default_rng(7)
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    C = rng.standard_normal((k, d)).astype(np.float32)
+    X[0] = np.nan
+    X[1, 3] = np.inf
+    X[2, 5] = -np.inf
+    X[3, :] = 1e30
+    km = mpk.KMeans(n, d, k, "fp32", dist)
+    mpk.kmeans_set_centroids(km.h, dev(C))
+    lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    km.assign(dev(X), lab)
+    km.close()
+    g = lab.cpu().numpy()
+    ref, _, _ = oracle.assign(X, C, work="fp32", dist=dist, guard=False)
+    assert g[0] == 0
+    assert np.array_equal(g[:4], ref[:4]), (g[:4], ref[:4])

@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(512, 1) k(int iters, unsigned long long* out, 
         const int j0 = (i * 32) & 1023;
         if (MODE == 0 || MODE == 2) fold32_x2<false>(va, cn_s, cn_s, -2.f, j0, cv, s2);
         else if (MODE == 1) fold32<false, false>(va, cn_s, cn_s, -2.f, j0, cv, cs, c2);
+        else if (MODE == 4) fold_rev_m3<4, false>(va, cn_s, cn_s, -2.f, j0, cv, s2);
         else {   // MODE 3: two chunks interleaved into two independent chain sets
             fold32_x2<false>(va, cn_s, cn_s, -2.f, j0, cv, s2);
             fold32_x2<false>(vb, cn_s, cn_s, -2.f, (j0 + 32) & 1023, cv2, s22);
@@ -65,5 +66,6 @@ int main() {
     run<1>("fold32 scalar, 2 warps/SMSP");
     run<2>("fold32_x2, 4 warps/SMSP", 512);
     run<3>("fold32_x2 x2 interleaved, 2 warps/SMSP");
+    run<4>("fold_rev_m3 (alu floor 96), 2 warps/SMSP");
     return 0;
 }

@@ -64,6 +64,23 @@ __global__ void __launch_bounds__(256, 1) k(int iters, unsigned long long* out, 
                 mpk::tcdev::chain_step_x2(acc2, 0x3F8000003F800000ull, 0xC0000000C0000000ull,
                                           v[e & 7], v[(e + 1) & 7], *reinterpret_cast<uint64_t*>(&s[(e & 3) * 2]),
                                           0xBF800000BF800000ull);
+            } else if (MODE == 12) {  // FMNMX3 alone (independent chains)
+                float r;
+                asm volatile("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(x));
+                a = r;
+            } else if (MODE == 13) {  // FMNMX3 + 2 FSET (the reverse fold's alu mix, 2 columns)
+                float r, p0, p1;
+                asm volatile("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(x));
+                asm volatile("set.gtu.f32.f32 %0, %1, %2;" : "=f"(p0) : "f"(b), "f"(a));
+                asm volatile("set.gtu.f32.f32 %0, %1, %2;" : "=f"(p1) : "f"(x), "f"(r));
+                a = r;
+                b = fmaf(fmaf(b, p0, -1.0f), p1, -1.0f);
+            } else if (MODE == 14) {  // chain_pair_x2 (4 columns: 2 chains x 2 groups)
+                uint64_t xa = ((uint64_t)__float_as_uint(x + e) << 32) | __float_as_uint(x - e);
+                uint64_t xb = ((uint64_t)__float_as_uint(x * e) << 32) | __float_as_uint(x + 2 * e);
+                mpk::tcdev::chain_pair_x2(xa, xb, v[e & 7], v[(e + 1) & 7],
+                                          *reinterpret_cast<uint64_t*>(&s[(e & 3) * 2]),
+                                          0xBF800000BF800000ull);
             } else if (MODE == 5) {   // SEL int
                 int ia = __float_as_int(a), ib = __float_as_int(b);
                 ia = (ia & 1) ? ib : ia;
@@ -110,5 +127,8 @@ int main() {
     run<9>("FFMA2 + 2 FMNMX");
     run<10>("FFMA imm + FADD + 2 FMNMX");
     run<11>("chain_step_x2 (2 columns)");
+    run<12>("FMNMX3");
+    run<13>("FMNMX3 + 2 FSET + 2 FFMA");
+    run<14>("chain_pair_x2 (4 columns)");
     return 0;
 }
