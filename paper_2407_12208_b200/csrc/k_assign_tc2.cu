@@ -44,6 +44,9 @@ constexpr int P_NON_EPI = 4;
 #ifndef MPK_PAIR_EWG
 #define MPK_PAIR_EWG 2
 #endif
+#ifndef MPK_PAIR_WARP_ARRIVE
+#define MPK_PAIR_WARP_ARRIVE 1           // 0: named barrier, then one arrival per CTA (slower)
+#endif
 constexpr int P_EWG = MPK_PAIR_EWG;      // epilogue warpgroups (split the columns)
 constexpr int P_EPI = 4 * P_EWG;
 constexpr int P_THREADS = (P_NON_EPI + P_EPI) * 32;
@@ -133,7 +136,8 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
         mbar_init(smem_u32(b_full), 1);
         for (int i = 0; i < p.nacc; ++i) {
             mbar_init(smem_u32(&t_full[i]), 1);
-            mbar_init(smem_u32(&t_empty[i]), 2);           // one arrival per CTA
+            // one arrival per CTA (named barrier first), or one per epilogue warp
+            mbar_init(smem_u32(&t_empty[i]), MPK_PAIR_WARP_ARRIVE ? 2 * P_EPI : 2);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x)) : "memory");
@@ -415,6 +419,28 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                                 tmem_wait_ld_dep(va);
                                 fold_rev_m3<2, GD>(va, q, m2, cv, s2);
                             }
+                            if (!GD && nch == 4 && c == wcols) {
+                                // NB = 256: four chunks unrolled, ||c||^2 of the next chunk
+                                // loaded while this one folds (two register sets, no copies)
+                                ChunkCn<4, GD> qa, qb;
+                                load_chunk_cn<4, GD>(cn_s, sc_s, jbase + 96, qa);
+                                tmem_ld32(col0 + 96, va);
+                                load_chunk_cn<4, GD>(cn_s, sc_s, jbase + 64, qb);
+                                tmem_wait_ld_dep(va);
+                                fold_rev_m3<4, GD>(va, qa, m2, cv, s2);
+                                tmem_ld32(col0 + 64, va);
+                                load_chunk_cn<4, GD>(cn_s, sc_s, jbase + 32, qa);
+                                tmem_wait_ld_dep(va);
+                                fold_rev_m3<4, GD>(va, qb, m2, cv, s2);
+                                tmem_ld32(col0 + 32, va);
+                                load_chunk_cn<4, GD>(cn_s, sc_s, jbase, qb);
+                                tmem_wait_ld_dep(va);
+                                fold_rev_m3<4, GD>(va, qa, m2, cv, s2);
+                                tmem_ld32(col0, va);
+                                tmem_wait_ld_dep(va);
+                                fold_rev_m3<4, GD>(va, qb, m2, cv, s2);
+                                return;
+                            }
                             for (int i = nch - 1; i >= 0; --i) {
                                 ChunkCn<4, GD> q;
                                 load_chunk_cn<4, GD>(cn_s, sc_s, jbase + i * 32, q);
@@ -462,9 +488,14 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 // one arrival per CTA: the epilogue warps meet at a named barrier, then a single
                 // thread signals the leader's "accumulator empty"
                 tc_fence_before();
-                named_bar_sync(BAR_TILE, P_EPI * 32);
-                if (warp == P_NON_EPI && lane == 0)
-                    mbar_arrive_cluster(mapa(smem_u32(&t_empty[buf]), 0));
+                if (MPK_PAIR_WARP_ARRIVE) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&t_empty[buf]), 0));
+                } else {
+                    named_bar_sync(BAR_TILE, P_EPI * 32);
+                    if (warp == P_NON_EPI && lane == 0)
+                        mbar_arrive_cluster(mapa(smem_u32(&t_empty[buf]), 0));
+                }
                 if (tr) trace[ai * 8 + 4] = clock64();
                 if (++buf == nacc) { buf = 0; tph ^= 1; }
             }
