@@ -47,6 +47,12 @@ constexpr int P_NON_EPI = 4;
 #ifndef MPK_PAIR_WARP_ARRIVE
 #define MPK_PAIR_WARP_ARRIVE 1           // 0: named barrier, then one arrival per CTA (slower)
 #endif
+#ifndef MPK_PAIR_ACC_DBUF
+#define MPK_PAIR_ACC_DBUF 1              // NB = 256 ASSIGN: double-buffered TMEM loads
+#endif
+#ifndef MPK_PAIR_HOT_WAIT
+#define MPK_PAIR_HOT_WAIT 1              // epilogue: test_wait before a bare try_wait loop
+#endif
 constexpr int P_EWG = MPK_PAIR_EWG;      // epilogue warpgroups (split the columns)
 constexpr int P_EPI = 4 * P_EWG;
 constexpr int P_THREADS = (P_NON_EPI + P_EPI) * 32;
@@ -382,7 +388,8 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
 #pragma unroll
             for (int m = 0; m < NCH / 2; ++m) s2[m] = pack2(-1.0f, -1.0f);
             for (int t = 0; t < NT; ++t, ++ai) {
-                mbar_wait(smem_u32(&t_full[buf]), tph);
+                if (MPK_PAIR_HOT_WAIT) mbar_wait_hot(smem_u32(&t_full[buf]), tph);
+                else mbar_wait(smem_u32(&t_full[buf]), tph);
                 tc_fence_after();
                 const bool tr = trace_me && ai < TRACE_T;
                 if (tr) trace[ai * 8 + 2] = clock64();
@@ -418,6 +425,30 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                                 tmem_ld16(col0 + c, va);
                                 tmem_wait_ld_dep(va);
                                 fold_rev_m3<2, GD>(va, q, m2, cv, s2);
+                            }
+                            if (MPK_PAIR_ACC_DBUF && !GD && nch == 4 && c == wcols) {
+                                // NB = 256: four chunks unrolled, the TMEM load of the next chunk
+                                // in flight while this one folds (the load's ~180-cycle latency
+                                // is hidden; tools/tmem_bench.cu)
+                                uint32_t vb[32];
+                                ChunkCn<4, GD> q;
+                                tmem_ld32(col0 + 96, va);
+                                tmem_wait_ld_dep(va);
+                                tmem_ld32(col0 + 64, vb);
+                                load_chunk_cn<4, GD>(cn_s, sc_s, jbase + 96, q);
+                                fold_rev_m3<4, GD>(va, q, m2, cv, s2);
+                                tmem_wait_ld_dep(vb);
+                                tmem_ld32(col0 + 32, va);
+                                load_chunk_cn<4, GD>(cn_s, sc_s, jbase + 64, q);
+                                fold_rev_m3<4, GD>(vb, q, m2, cv, s2);
+                                tmem_wait_ld_dep(va);
+                                tmem_ld32(col0, vb);
+                                load_chunk_cn<4, GD>(cn_s, sc_s, jbase + 32, q);
+                                fold_rev_m3<4, GD>(va, q, m2, cv, s2);
+                                tmem_wait_ld_dep(vb);
+                                load_chunk_cn<4, GD>(cn_s, sc_s, jbase, q);
+                                fold_rev_m3<4, GD>(vb, q, m2, cv, s2);
+                                return;
                             }
                             if (!GD && nch == 4 && c == wcols) {
                                 // NB = 256: four chunks unrolled, ||c||^2 of the next chunk
