@@ -62,7 +62,8 @@ constexpr uint32_t TRACE_T = 256;        // tiles traced under MPK_PAIR_TRACE
 // named barriers (0 is __syncthreads)
 constexpr int BAR_TILE = 1;              // the epilogue warps, once per tile
 constexpr int BAR_PART = 2;              // + parity: partials written (epilogue -> warp 3)
-constexpr int BAR_FREE = 4;              // + parity: partials consumed (warp 3 -> epilogue)
+// "partials consumed" (warp 3 -> epilogue) is an mbarrier per parity (part_free), not a named
+// barrier: the epilogue warps only wait on it, so they do not all meet once per row-block
 
 MPK_DEV void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -127,6 +128,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
     __shared__ float part_v[2 * P_EWG * P_BM];
     __shared__ float part_v2[2 * P_EWG * P_BM];        // second minima (FINAL)
     __shared__ int part_j[2 * P_EWG * P_BM];
+    __shared__ __align__(8) uint64_t part_free[2];
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -140,6 +142,8 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
     if (threadIdx.x == 0) {
         for (int i = 0; i < p.SA; ++i) { mbar_init(smem_u32(&a_full[i]), 1); mbar_init(smem_u32(&a_empty[i]), 1); }
         mbar_init(smem_u32(b_full), 1);
+        mbar_init(smem_u32(&part_free[0]), 1);
+        mbar_init(smem_u32(&part_free[1]), 1);
         for (int i = 0; i < p.nacc; ++i) {
             mbar_init(smem_u32(&t_full[i]), 1);
             // one arrival per CTA (named barrier first), or one per epilogue warp
@@ -346,7 +350,8 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 }
             }
             // hand the parity's partial buffer back (only if the epilogue will write it again)
-            if (rbi + 2 < my_rbs) named_bar_arrive(BAR_FREE + par, P_EPI * 32 + 32);
+            __syncwarp();
+            if (rbi + 2 < my_rbs && lane == 0) mbar_arrive(smem_u32(&part_free[par]));
         }
         if (!FINAL) {
             my_sse = warp_sum(my_sse);
@@ -537,21 +542,35 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
 #pragma unroll
                 for (int m = 0; m < NCH / 2; ++m) unpack2(s2[m], cs[2 * m], cs[2 * m + 1]);
             }
-            int jj[NCH];
-#pragma unroll
-            for (int c = 0; c < NCH; ++c) {
-                // REV: forward ordinal of the last improving visit = -1 - s (NT * gpt: never)
-                const int v = REV ? -1 - (int)cs[c] : chain_ordinal(cs[c], NT * gpt);
-                const int t = v >> gsh;
-                jj[c] = 8 * (t * (NB >> 3) + (col_off >> 3) + (v - t * gpt)) + c;
-                if (REV && v >= NT * gpt) jj[c] = 0x7FFFFFFF;
-            }
             int w = 0;
             float b1;
             int j1;
-            merge_chains(cv, jj, b1, j1, &w);
-            // no value below +inf: the forward scan's default column 0
-            if (REV && !(b1 < INFINITY)) j1 = 0;
+            if (REV) {
+                // forward ordinal of chain c's last improving visit: v = -1 - s (NT * gpt if it
+                // never improved). The column is increasing in (v, c), so the chains merge on the
+                // exact float key 8 v + c = -8 s - 8 + c (one FFMA each, no conversions) and
+                // only the winner's key becomes a column.
+                float k1 = fmaf(cs[0], -8.0f, -8.0f);
+                b1 = cv[0];
+#pragma unroll
+                for (int c = 1; c < NCH; ++c) {
+                    const float kc = fmaf(cs[c], -8.0f, (float)(c - 8));
+                    if (cv[c] < b1 || (cv[c] == b1 && kc < k1)) { b1 = cv[c]; k1 = kc; }
+                }
+                const int key = (int)k1, v = key >> 3, t = v >> gsh;
+                j1 = 8 * (t * (NB >> 3) + (col_off >> 3) + (v - t * gpt)) + (key & 7);
+                // no value below +inf: the forward scan's default column 0
+                if (!(b1 < INFINITY)) j1 = 0;
+            } else {
+                int jj[NCH];
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) {
+                    const int v = chain_ordinal(cs[c], NT * gpt);
+                    const int t = v >> gsh;
+                    jj[c] = 8 * (t * (NB >> 3) + (col_off >> 3) + (v - t * gpt)) + c;
+                }
+                merge_chains(cv, jj, b1, j1, &w);
+            }
             float b2 = INFINITY;
             if (FINAL) {
 #pragma unroll
@@ -559,7 +578,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             }
             // hand the partial to warp 3 (double-buffered by row-block parity)
             const int par = (int)(rbi & 1);
-            if (rbi >= 2) named_bar_sync(BAR_FREE + par, P_EPI * 32 + 32);
+            if (rbi >= 2) mbar_wait_hot(smem_u32(&part_free[par]), (uint32_t)((rbi >> 1) - 1) & 1u);
             const int slot = (par * P_EWG + wg) * P_BM + q;
             part_v[slot] = b1;
             part_j[slot] = j1;
