@@ -232,7 +232,8 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 tc_fence_after();
                 const uint32_t a_lo = a_lo0 + slot * a_tile16;
                 for (int t = 0; t < NT; ++t, ++ai) {
-                    mbar_wait(smem_u32(&t_empty[buf]), tph ^ 1);
+                    if (MPK_PAIR_HOT_WAIT) mbar_wait_hot(smem_u32(&t_empty[buf]), tph ^ 1);
+                    else mbar_wait(smem_u32(&t_empty[buf]), tph ^ 1);
                     tc_fence_after();
                     if (elect_one()) {
                         const bool tr = trace_me && ai < TRACE_T;
