@@ -18,7 +18,10 @@ namespace mpk {
 namespace {
 
 constexpr int kStatThreads = 256;
-constexpr int kApplySmemD = 2048;        // norm_apply caches shift / scale / 1/scale up to this d
+constexpr int kApplySmemD = 2048;
+#ifndef MPK_PREP_NO_VEC
+#define MPK_PREP_NO_VEC 0               // 1: always the scalar prep_fast_kernel (A/B)
+#endif        // norm_apply caches shift / scale / 1/scale up to this d
 
 // One kernel for the three column statistics: mode 0 = sum x, mode 1 = sum (x - mu)^2,
 // mode 2 = (min, max). Thread layout: column c = tid % d, row lane = tid / d (d <= 256), else a
@@ -515,6 +518,136 @@ prep_fast_kernel(const float* __restrict__ Xin, int64_t rows, int d, int d_pad, 
     }
 }
 
+// Vectorised form of prep_fast_kernel for rows whose width is a multiple of 128 (d = d_pad,
+// d <= 256): a lane owns V float4 column groups (columns 128 w + 4 lane + e), so each row costs
+// one 16-byte load, one 16-byte store of the normalised row and one 4-element store of the
+// operands per group, and the guard's division runs only for rows with s != 1 (a warp-uniform
+// branch). Same arithmetic per element as prep_row_fast: the fp64 correctly rounded quotient
+// rounded once to fp32, exact-product TwoSum partials of ||x||^2 summed in fp64 across lanes,
+// x~ = round_l(x / s).
+template <typename L> struct vec4_of;
+template <> struct vec4_of<float> { using T = float4; };
+template <> struct vec4_of<__half> { using T = uint2; };
+template <> struct vec4_of<__nv_bfloat16> { using T = uint2; };
+template <> struct vec4_of<e5m2_t> { using T = uint32_t; };
+template <typename L>
+MPK_DEV void store_low4(L* dst, const L (&o)[4]) {
+    using T = typename vec4_of<L>::T;
+    union { L l[4]; T t; } u;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) u.l[e] = o[e];
+    *reinterpret_cast<T*>(dst) = u.t;
+}
+
+template <int DIST, bool NORM, int V, int RPS>
+__global__ void __launch_bounds__(256)
+prep_vec_kernel(const float* __restrict__ Xin, int64_t rows, int d, int guard,
+                float* __restrict__ norms, float* __restrict__ scales,
+                typename low_type<DIST>::T* __restrict__ Xl,
+                unsigned long long* __restrict__ census, float* __restrict__ Xout,
+                const double* __restrict__ shift, const double* __restrict__ scale) {
+    using L = typename low_type<DIST>::T;
+    constexpr bool same = DIST == KMEANS_FP32;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double sh[V][4], sc[V][4], rc[V][4];
+#pragma unroll
+    for (int w = 0; w < V; ++w)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int c = 128 * w + 4 * lane + e;
+            sh[w][e] = NORM ? shift[c] : 0.0;
+            sc[w][e] = NORM ? scale[c] : 1.0;
+            rc[w][e] = 1.0 / sc[w][e];
+        }
+    unsigned n_nonfinite = 0, n_under = 0;
+    for (int64_t i = warp; i < rows; i += RPS * nwarps) {
+        float4 xv[RPS][V];
+#pragma unroll
+        for (int r = 0; r < RPS; ++r) {
+            const int64_t ir = i + r * nwarps;
+#pragma unroll
+            for (int w = 0; w < V; ++w)
+                xv[r][w] = ir < rows ? __ldg(reinterpret_cast<const float4*>(Xin + ir * d + 128 * w) + lane)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int r = 0; r < RPS; ++r) {
+            const int64_t ir = i + r * nwarps;
+            if (ir >= rows) break;
+            float v[V][4];
+#pragma unroll
+            for (int w = 0; w < V; ++w) {
+                v[w][0] = xv[r][w].x; v[w][1] = xv[r][w].y; v[w][2] = xv[r][w].z; v[w][3] = xv[r][w].w;
+                if (NORM) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        v[w][e] = __double2float_rn(div_rn((double)v[w][e] - sh[w][e], sc[w][e], rc[w][e]));
+                    reinterpret_cast<float4*>(Xout + ir * d + 128 * w)[lane] =
+                        make_float4(v[w][0], v[w][1], v[w][2], v[w][3]);
+                }
+            }
+            float ss = 0.0f, cs = 0.0f;
+#pragma unroll
+            for (int w = 0; w < V; ++w)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float x = v[w][e];
+                    const float p = x * x;
+                    const float ep = fmaf(x, x, -p);
+                    const float t = ss + p;
+                    const float z = t - ss;
+                    cs += (ss - (t - z)) + (p - z) + ep;
+                    ss = t;
+                }
+            const double acc = warp_sum((double)ss + (double)cs);
+            float s = 1.0f;
+            if (guard && !same) {
+                float amax = 0.0f;
+#pragma unroll
+                for (int w = 0; w < V; ++w)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) amax = fmaxf(amax, fabsf(v[w][e]));
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+                s = (amax == 0.0f || isnan(amax)) ? 1.0f : amax;
+                if (s != 1.0f) {          // warp-uniform: s is the row's
+#pragma unroll
+                    for (int w = 0; w < V; ++w)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) v[w][e] = v[w][e] / s;   // precision-u division
+                }
+            }
+            if (lane == 0) {
+                norms[ir] = __double2float_rn(acc);
+                if (scales) scales[ir] = s;
+            }
+#pragma unroll
+            for (int w = 0; w < V; ++w) {
+                L o[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    o[e] = rounder<DIST>::from(v[w][e]);
+                    if (!same) {
+                        if (is_nonfinite_low(o[e])) n_nonfinite++;
+                        else if (v[w][e] != 0.0f && is_zero_or_subnormal_low(o[e])) n_under++;
+                    }
+                }
+                store_low4<L>(Xl + ir * d + 128 * w + 4 * lane, o);
+            }
+        }
+    }
+    if (census) {
+        const unsigned long long a = warp_sum((unsigned long long)n_nonfinite);
+        const unsigned long long b = warp_sum((unsigned long long)n_under);
+        if (lane == 0 && (a | b)) {
+            atomicAdd(&census[0], a);
+            atomicAdd(&census[1], b);
+        }
+    }
+}
+
 template <int DIST>
 static void prep_fast_launch(const float* Xin, int64_t rows, int d, int d_pad, int guard,
                              float* norms, float* scales, void* Xl, unsigned long long* census,
@@ -522,6 +655,25 @@ static void prep_fast_launch(const float* Xin, int64_t rows, int d, int d_pad, i
                              cudaStream_t s) {
     using L = typename low_type<DIST>::T;
     const int g = grid_for(rows * 8, 256, 8);
+    const bool aligned = (((uintptr_t)Xin | (uintptr_t)Xout | (uintptr_t)Xl) & 15) == 0;
+    if (d == d_pad && (d == 128 || d == 256) && aligned && !MPK_PREP_NO_VEC) {
+        if (d == 128) {
+            if (shift)
+                prep_vec_kernel<DIST, true, 1, 4><<<g, 256, 0, s>>>(Xin, rows, d, guard, norms, scales,
+                                                                    (L*)Xl, census, Xout, shift, scale);
+            else
+                prep_vec_kernel<DIST, false, 1, 4><<<g, 256, 0, s>>>(Xin, rows, d, guard, norms, scales,
+                                                                     (L*)Xl, census, Xout, shift, scale);
+        } else {
+            if (shift)
+                prep_vec_kernel<DIST, true, 2, 2><<<g, 256, 0, s>>>(Xin, rows, d, guard, norms, scales,
+                                                                    (L*)Xl, census, Xout, shift, scale);
+            else
+                prep_vec_kernel<DIST, false, 2, 2><<<g, 256, 0, s>>>(Xin, rows, d, guard, norms, scales,
+                                                                     (L*)Xl, census, Xout, shift, scale);
+        }
+        return;
+    }
     // d_pad columns of Xl must be covered by the lane's Q slots too
     const int w = d_pad > d ? d_pad : d;
     if (w <= 128) {

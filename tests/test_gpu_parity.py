@@ -321,3 +321,24 @@ def test_update_is_bit_reproducible(work, dist, k):
         assert r["sse"] == pytest.approx(runs[0]["sse"], rel=1e-12)   # atomic fp64 SSE sum
         assert r["stats"]["u_bound_t"] == runs[0]["stats"]["u_bound_t"]
 
+
+
+@pytest.mark.parametrize("d", [128, 256])
+@pytest.mark.parametrize("dist,guard", [("fp16", False), ("e5m2", True), ("bf16", False)])
+def test_wide_rows_zscore_fit_parity(d, dist, guard):
+    """Rows of 128 / 256 columns take the vectorised prep (normalise + ||x||^2 + guard scale +
+    operand rounding, one pass): z-score transform, per-iteration SSE trace and final SSE agree
+    with the oracle (Alg 3 on eq:z-norm data); labels ARI >= 0.99."""
+    from sklearn.metrics import adjusted_rand_score
+    n, k = 4099, 40
+    X, _ = synth.blobs(n, d, 16, sigma=1.5, seed=d, dtype=np.float32)
+    X = (X * 3.0 + 5.0).astype(np.float32)
+    C0 = synth.init_rows(X, k, 2)
+    g = gpu_fit(X, C0, "fp32", dist, norm="zscore", guard=guard, max_iter=4)
+    ref = oracle.fit(X, C0, work="fp32", dist=dist, norm="zscore", guard=guard, max_iter=4,
+                     tol=-1.0)
+    assert abs(g["sse"] - ref["sse"]) <= 1e-3 * ref["sse"]
+    st = g["stats"]
+    for a, b in zip(st["sse_t"], ref["sse_t"]):
+        assert abs(a - b) <= 1e-3 * b
+    assert adjusted_rand_score(ref["labels"], g["labels"]) >= 0.99
