@@ -916,6 +916,64 @@ __global__ void final_sse_fast_kernel(const float* __restrict__ X, int64_t n, in
     }
 }
 
+// fp32 rows of 128 / 256 columns (V float4 groups per lane): one 16-byte load of x and of its
+// centre per row and group, RW rows in flight per warp; per column the same exact-product TwoSum
+// over the RW rows as final_sse_fast_kernel, then fp64.
+template <int V>
+__global__ void __launch_bounds__(256)
+final_sse_vec_kernel(const float* __restrict__ X, int64_t n, int d, const float* __restrict__ C,
+                     const int32_t* __restrict__ labels, double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    constexpr int RW = 8 / V;
+    double acc = 0.0;
+    for (int64_t i0 = warp * RW; i0 < n; i0 += nwarps * RW) {
+        int lab[RW];
+#pragma unroll
+        for (int r = 0; r < RW; ++r) lab[r] = (i0 + r < n) ? __ldg(labels + i0 + r) : 0;
+        float4 xv[V][RW], cv[V][RW];
+#pragma unroll
+        for (int w = 0; w < V; ++w)
+#pragma unroll
+            for (int r = 0; r < RW; ++r) {
+                const bool ok = i0 + r < n;
+                xv[w][r] = ok ? __ldg(reinterpret_cast<const float4*>(X + (i0 + r) * d + 128 * w) + lane)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+                cv[w][r] = ok ? __ldg(reinterpret_cast<const float4*>(C + (int64_t)lab[r] * d + 128 * w) + lane)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+        for (int w = 0; w < V; ++w)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                float sum = 0.0f, comp = 0.0f;
+#pragma unroll
+                for (int r = 0; r < RW; ++r) {
+                    const float xa = e == 0 ? xv[w][r].x : e == 1 ? xv[w][r].y : e == 2 ? xv[w][r].z : xv[w][r].w;
+                    const float ca = e == 0 ? cv[w][r].x : e == 1 ? cv[w][r].y : e == 2 ? cv[w][r].z : cv[w][r].w;
+                    const float df = xa - ca;
+                    const float p2 = df * df;
+                    const float e2 = fmaf(df, df, -p2);
+                    const float t = sum + p2;
+                    const float z = t - sum;
+                    comp += (sum - (t - z)) + (p2 - z) + e2;
+                    sum = t;
+                }
+                acc += (double)sum + (double)comp;
+            }
+    }
+    acc = warp_sum(acc);
+    __shared__ double red[8];
+    if (lane == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += red[w];
+        atomicAdd(out, a);
+    }
+}
+
 template <typename LT, typename W>
 cudaError_t simt_dispatch_acc(int dist, const Problem& p, const void* Xl, const void* xn,
                               const void* sx, const void* Cl, const void* cn, const void* sc,
@@ -1022,9 +1080,14 @@ cudaError_t launch_final_sse(int work, const void* Xw, int64_t n, int d, const v
     launches_add(1);
     int64_t want = (n * 32 + 255) / 256;
     int grid = (int)(want < 1 ? 1 : (want > kNumSMs * 8 ? kNumSMs * 8 : want));
+    const bool vec_ok = (d == 128 || d == 256) && ((((uintptr_t)Xw) | ((uintptr_t)Cw)) & 15) == 0;
     if (work == KMEANS_FP64)
         final_sse_kernel<double><<<grid, 256, 0, s>>>((const double*)Xw, n, d, (const double*)Cw,
                                                      labels, sse_out);
+    else if (vec_ok && d == 128)
+        final_sse_vec_kernel<1><<<grid, 256, 0, s>>>((const float*)Xw, n, d, (const float*)Cw, labels, sse_out);
+    else if (vec_ok)
+        final_sse_vec_kernel<2><<<grid, 256, 0, s>>>((const float*)Xw, n, d, (const float*)Cw, labels, sse_out);
     else if (d <= 32)
         final_sse_fast_kernel<1><<<grid, 256, 0, s>>>((const float*)Xw, n, d, (const float*)Cw, labels, sse_out);
     else if (d <= 64)

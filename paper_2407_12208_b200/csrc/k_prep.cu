@@ -101,6 +101,100 @@ norm_col_stats_kernel(int mode, const W* __restrict__ X, int64_t n, int d,
     }
 }
 
+// Vectorised norm_col_stats_kernel for fp32 rows with d % 4 == 0 (d <= 1024): a thread owns
+// four adjacent columns (one 16-byte load per row, four independent compensated sums) and
+// keeps the next batch of rows in flight while it accumulates the current one. Same per-column
+// arithmetic (Neumaier in fp64 over the thread's rows in increasing order, then the row lanes
+// combined in lane order), with a different split of rows over lanes than the scalar kernel.
+constexpr int kVecBatch = 4;
+__global__ void __launch_bounds__(kStatThreads)
+norm_col_stats_vec_kernel(int mode, const float* __restrict__ X, int64_t n, int d,
+                          const double* __restrict__ mu, double* __restrict__ partials) {
+    const int tid = threadIdx.x;
+    const int cg = d >> 2;                          // column groups (<= 256)
+    const int lanes = kStatThreads / cg;
+    const int g = tid % cg, lane = tid / cg;
+    const bool active = lane < lanes;
+    const int64_t rows_per_block = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
+    const int64_t r1 = min(n, r0 + rows_per_block);
+    __shared__ double sh_s[kStatThreads * 4], sh_c[kStatThreads * 4];
+    double s[4], comp[4], m[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        s[e] = mode == 2 ? INFINITY : 0.0;
+        comp[e] = mode == 2 ? -INFINITY : 0.0;
+        m[e] = (mode == 1 && active) ? mu[4 * g + e] : 0.0;
+    }
+    if (active) {
+        const float4* X4 = reinterpret_cast<const float4*>(X) + g;
+        const int64_t step = (int64_t)lanes;
+        float4 nxt[kVecBatch];
+        int64_t i0 = r0 + lane;
+#pragma unroll
+        for (int u = 0; u < kVecBatch; ++u) {
+            const int64_t i = i0 + u * step;
+            nxt[u] = i < r1 ? __ldg(X4 + i * cg) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        for (; i0 < r1; i0 += step * kVecBatch) {
+            float4 cur[kVecBatch];
+#pragma unroll
+            for (int u = 0; u < kVecBatch; ++u) cur[u] = nxt[u];
+            const int64_t j0 = i0 + step * kVecBatch;
+#pragma unroll
+            for (int u = 0; u < kVecBatch; ++u) {
+                const int64_t i = j0 + u * step;
+                nxt[u] = i < r1 ? __ldg(X4 + i * cg) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < kVecBatch; ++u) {
+                if (i0 + u * step >= r1) break;
+                const float xv[4] = {cur[u].x, cur[u].y, cur[u].z, cur[u].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    double x = (double)xv[e];
+                    if (mode == 2) {
+                        s[e] = fmin(s[e], x);
+                        comp[e] = fmax(comp[e], x);
+                    } else {
+                        if (mode == 1) { const double z = x - m[e]; x = z * z; }
+                        const double t = s[e] + x;
+                        comp[e] += (fabs(s[e]) >= fabs(x)) ? ((s[e] - t) + x) : ((x - t) + s[e]);
+                        s[e] = t;
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        sh_s[tid * 4 + e] = s[e];
+        sh_c[tid * 4 + e] = comp[e];
+    }
+    __syncthreads();
+    // combine row lanes of the same column in fixed order (lane 0..lanes-1)
+    if (active && lane == 0) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            double S = s[e], Cc = comp[e];
+            for (int l = 1; l < lanes; ++l) {
+                const double s2 = sh_s[(l * cg + g) * 4 + e], c2 = sh_c[(l * cg + g) * 4 + e];
+                if (mode == 2) {
+                    S = fmin(S, s2);
+                    Cc = fmax(Cc, c2);
+                } else {
+                    const double t = S + s2;
+                    Cc += ((fabs(S) >= fabs(s2)) ? ((S - t) + s2) : ((s2 - t) + S)) + c2;
+                    S = t;
+                }
+            }
+            const int c = 4 * g + e;
+            partials[((int64_t)blockIdx.x * d + c) * 2 + 0] = S;
+            partials[((int64_t)blockIdx.x * d + c) * 2 + 1] = Cc;
+        }
+    }
+}
+
 // Combine the per-block partials of one column in block order.
 // mode 0: compensated sum (-> a), mode 2: min (-> a) and max (-> b).
 __global__ void norm_combine_kernel(int mode, const double* __restrict__ partials, int nblocks,
@@ -336,6 +430,10 @@ inline int grid_for(int64_t work_items, int threads, int per_sm = 8) {
 
 }  // namespace
 
+static bool stats_vec_ok(const void* X, int d) {
+    return !MPK_PREP_NO_VEC && d % 4 == 0 && d <= 4 * kStatThreads && ((uintptr_t)X & 15) == 0;
+}
+
 int norm_stats_blocks(int64_t n, int d) {
     int64_t b = (n * d + 8191) / 8192;
     if (b < 1) b = 1;
@@ -351,6 +449,9 @@ cudaError_t launch_norm_stats(int work, int norm, const void* X, int64_t n, int 
     if (work == KMEANS_FP64)
         norm_col_stats_kernel<double><<<nblocks, kStatThreads, 0, s>>>(mode, (const double*)X, n,
                                                                        d, nullptr, partials);
+    else if (stats_vec_ok(X, d))
+        norm_col_stats_vec_kernel<<<nblocks, kStatThreads, 0, s>>>(mode, (const float*)X, n, d,
+                                                                   nullptr, partials);
     else
         norm_col_stats_kernel<float><<<nblocks, kStatThreads, 0, s>>>(mode, (const float*)X, n,
                                                                       d, nullptr, partials);
@@ -364,6 +465,9 @@ cudaError_t launch_norm_ssq(int work, const void* X, int64_t n, int d, double* p
     if (work == KMEANS_FP64)
         norm_col_stats_kernel<double><<<nblocks, kStatThreads, 0, s>>>(1, (const double*)X, n, d,
                                                                        mean, partials);
+    else if (stats_vec_ok(X, d))
+        norm_col_stats_vec_kernel<<<nblocks, kStatThreads, 0, s>>>(1, (const float*)X, n, d,
+                                                                   mean, partials);
     else
         norm_col_stats_kernel<float><<<nblocks, kStatThreads, 0, s>>>(1, (const float*)X, n, d,
                                                                       mean, partials);
