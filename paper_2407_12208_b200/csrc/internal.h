@@ -175,6 +175,28 @@ cudaError_t launch_update(int work, const void* Xw, int64_t n, int d, int k,
                           const int32_t* labels, int* cnt, int* offs, int* cursor, int* perm,
                           double* acc, AccLayout L, const UpdateScratch& us, cudaStream_t s);
 
+// FX: exact fixed-point cluster totals with incremental updates (k_update.cu, R9).
+struct FxState {
+    unsigned* amax = nullptr;   // d: max |x_t| (float bits)
+    float2* sc = nullptr;       // d: (c1, c2) of the feature's grid (k_update.cu fx_q)
+    double* isc = nullptr;      // d: the grid step 2^(e_t - 45)
+    long long* Shi = nullptr;   // k*d: sum of i1 (coarse parts)
+    long long* Slo = nullptr;   // k*d: sum of i2 (fine parts)
+    long long* part = nullptr;  // piece totals of multi-piece clusters (hi d, lo d per slot)
+    int32_t* prev = nullptr;    // n: labels of the previous iteration
+    int3* list = nullptr;       // changed rows (row, old, new), capacity gate[1]
+    int* gate = nullptr;        // [0] changed rows, [1] capacity, [2] non-finite X flag
+    int cap = 0;
+};
+cudaError_t launch_fx_prepare(const float* Xw, int64_t n, int d, FxState& fx, cudaStream_t s);
+cudaError_t launch_update_fx(const float* Xw, int64_t n, int d, int k, const int32_t* labels,
+                             int* cnt, int* offs, int* cursor, int* perm, const UpdateScratch& us,
+                             FxState& fx, cudaStream_t s);
+cudaError_t launch_finalize_fx(int64_t k, int d, const FxState& fx, const int* cnt,
+                               const double* acc, AccLayout L, float* Cw, IterRec* rec,
+                               cudaStream_t s);
+size_t fx_part_bytes(int64_t n, int d);
+
 // K8: finalize: C = round_u(sum / count) (empty -> keep), shift^2, empty count, trace record.
 cudaError_t launch_finalize(int work, int64_t k, int d, const double* acc, AccLayout L,
                             void* Cw, IterRec* rec, cudaStream_t s);

@@ -19,6 +19,9 @@
 // whole rows (coalesced 16-byte vector loads), so U4 is HBM-bound.
 // K8: c_j = round_u(sum_j / count_j), empty clusters keep c_j (reading Z14); shift^2 and the
 //     number of empty clusters go to the iteration record.
+// FX (fp32 work, one rank; R9, default): the same U1-U4 with exact integer totals on a
+// per-feature grid, kept across iterations and updated from the rows whose label changed (integer
+// atomics) while few rows change — bit-identical to re-summing every row (tested).
 #include "common.cuh"
 #include "internal.h"
 
@@ -27,6 +30,10 @@ namespace mpk {
 namespace {
 
 constexpr int kHistMax = 12288;   // 48 KB of int bins in smem
+
+// Fixed-point mode (FX, below): the full-recompute kernels run only when the iteration's list
+// of changed rows overflowed (gate[0] = changed rows, gate[1] = list capacity); nullptr = always.
+MPK_DEV bool gated_off(const int* gate) { return gate != nullptr && gate[0] <= gate[1]; }
 
 __global__ void count_kernel(const int32_t* __restrict__ labels, int64_t n, int k,
                              int* __restrict__ cnt) {
@@ -54,7 +61,8 @@ __global__ void count_kernel(const int32_t* __restrict__ labels, int64_t n, int 
 // it spans several segsum pieces of P rows (ceil(cnt_j / P) >= 2 slots; else 0 slots).
 __global__ void scan_kernel(const int* __restrict__ cnt, int k, int64_t P, int* __restrict__ offs,
                             int* __restrict__ cursor, int* __restrict__ mpo,
-                            double* __restrict__ acc_counts) {
+                            double* __restrict__ acc_counts, const int* gate = nullptr) {
+    if (gated_off(gate)) return;
     __shared__ int sh[1024], sh2[1024];
     __shared__ int carry, carry2;
     if (threadIdx.x == 0) carry = carry2 = 0;
@@ -80,7 +88,7 @@ __global__ void scan_kernel(const int* __restrict__ cnt, int k, int64_t P, int* 
             offs[j] = ex;
             cursor[j] = ex;
             mpo[j] = carry2 + sh2[threadIdx.x] - v2;
-            acc_counts[j] = (double)v;
+            if (acc_counts) acc_counts[j] = (double)v;
         }
         __syncthreads();
         if (threadIdx.x == 1023) { carry += sh[1023]; carry2 += sh2[1023]; }
@@ -98,7 +106,9 @@ constexpr int kDetRows = 8192;                    // rows per counting / scatter
 
 // U1a: per-block label histogram -> CB[b * k + l] (block-major: coalesced stores).
 __global__ void __launch_bounds__(kDetThreads)
-block_count_kernel(const int32_t* __restrict__ labels, int64_t n, int k, int* __restrict__ CB) {
+block_count_kernel(const int32_t* __restrict__ labels, int64_t n, int k, int* __restrict__ CB,
+                   const int* gate = nullptr) {
+    if (gated_off(gate)) return;
     extern __shared__ int hist[];
     for (int j = threadIdx.x; j < k; j += blockDim.x) hist[j] = 0;
     __syncthreads();
@@ -117,7 +127,9 @@ block_count_kernel(const int32_t* __restrict__ labels, int64_t n, int k, int* __
 // 32 labels (lanes) and its 32 warps take consecutive segments of blocks: segment totals,
 // a scan of the 32 totals, then the segments rewritten with their offsets.
 __global__ void __launch_bounds__(1024)
-block_scan_kernel(int* __restrict__ CB, int64_t nb, int k, int* __restrict__ cnt) {
+block_scan_kernel(int* __restrict__ CB, int64_t nb, int k, int* __restrict__ cnt,
+                  const int* gate = nullptr) {
+    if (gated_off(gate)) return;
     __shared__ int tot[32][33];
     const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
     const int l = blockIdx.x * 32 + lane;
@@ -181,7 +193,8 @@ MPK_DEV unsigned match_bits(int key, int bits) {
 __global__ void __launch_bounds__(kDetThreads)
 scatter_det_kernel(const int32_t* __restrict__ labels, int64_t n, int k,
                    const int* __restrict__ offs, const int* __restrict__ CB,
-                   int* __restrict__ perm) {
+                   int* __restrict__ perm, const int* gate = nullptr) {
+    if (gated_off(gate)) return;
     const int kbits = 32 - __clz(k);              // keys l + 1 in [0, k]
     extern __shared__ int smem_i[];
     const int nwarps = blockDim.x >> 5;
@@ -511,6 +524,326 @@ cudaError_t update_dispatch(const W* X, int64_t n, int d, int k, const int32_t* 
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------------------------
+// FX: the update with exact fixed-point sums (fp32 working precision, one rank, k <= kHistMax).
+// Each coordinate is put on a per-feature grid once, q = RN(x * 2^F_t) as an int64 with
+// F_t = 61 - e_t (2^e_t > max_i |x_it|, so |q| < 2^61), split q = hi * 2^31 + lo (lo in
+// [0, 2^31)); a cluster's sum is the pair of int64 totals (sum hi, sum lo). Integer addition is
+// associative, so the totals — and the centre round_u(S / (count 2^F_t)), K8 — depend only on
+// the cluster's members: the same whatever the summation order or history. That makes it legal
+// to UPDATE the totals from the rows whose label changed (S[new] += q, S[old] -= q, integer
+// atomics) instead of re-summing all n rows: both give the same bits. The full re-summation
+// (U1-U4 above, integer accumulators) runs when the changed-row list overflows (the first
+// iterations); afterwards each iteration reads only the changed rows (~0.1-1 % of n at C5).
+// The grid costs 2^-61 max|x_t| per coordinate: far below u = 2^-24 of the means.
+// Per-column max |x| (bits of a non-negative float order like unsigned ints) and flags[2] = 1 on
+// a non-finite value. d % 4 == 0: a thread owns 4 adjacent columns, 16-byte loads, the next rows
+// in flight; else a warp per row.
+__global__ void __launch_bounds__(256)
+fx_colmax_vec_kernel(const float* __restrict__ X, int64_t n, int d, unsigned* __restrict__ amax,
+                     int* __restrict__ flags) {
+    const int cg = d >> 2, lanes = 256 / cg;
+    const int g = threadIdx.x % cg, lane = threadIdx.x / cg;
+    unsigned mx[4] = {0u, 0u, 0u, 0u};
+    unsigned bad = 0;
+    if (lane < lanes) {
+        const float4* X4 = reinterpret_cast<const float4*>(X) + g;
+        const int64_t step = (int64_t)gridDim.x * lanes;
+        for (int64_t i0 = (int64_t)blockIdx.x * lanes + lane; i0 < n; i0 += 4 * step) {
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t i = i0 + u * step;
+                v[u] = i < n ? __ldg(X4 + i * cg) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float a[4] = {fabsf(v[u].x), fabsf(v[u].y), fabsf(v[u].z), fabsf(v[u].w)};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if (!(a[e] <= 3.402823466e38f)) bad = 1;
+                    else mx[e] = max(mx[e], __float_as_uint(a[e]));
+                }
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (mx[e]) atomicMax(&amax[4 * g + e], mx[e]);
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&flags[2], 1);
+}
+__global__ void fx_colmax_kernel(const float* __restrict__ X, int64_t n, int d,
+                                 unsigned* __restrict__ amax, int* __restrict__ flags) {
+    extern __shared__ unsigned sm[];
+    for (int j = threadIdx.x; j < d; j += blockDim.x) sm[j] = 0u;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned bad = 0;
+    for (int64_t i = warp; i < n; i += nwarps)
+        for (int c = lane; c < d; c += 32) {
+            const float v = fabsf(__ldg(X + i * d + c));
+            if (!(v <= 3.402823466e38f)) bad = 1;
+            else atomicMax(&sm[c], __float_as_uint(v));
+        }
+    __syncthreads();
+    for (int j = threadIdx.x; j < d; j += blockDim.x)
+        if (sm[j]) atomicMax(&amax[j], sm[j]);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&flags[2], 1);
+}
+__global__ void fx_scale_kernel(const unsigned* __restrict__ amax, int d, float2* __restrict__ c12,
+                                double* __restrict__ g2, int* __restrict__ flags) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= d) return;
+    int e = 0;
+    frexp((double)__uint_as_float(amax[t]), &e);      // amax < 2^e (amax = 0: e = 0)
+    if (e < -90 || e > 100) { atomicOr(&flags[2], 2); e = 0; }   // c2 / c1 out of fp32 range
+    c12[t] = make_float2(ldexpf(1.5f, e + 1), ldexpf(1.5f, e - 22));
+    g2[t] = ldexp(1.0, e - 45);
+}
+// The grid value of x, with fp32 adds and integer subtractions only. With |x| < 2^e (e from
+// max |x_t|) and the constants c1 = 1.5 2^(e+1), c2 = 1.5 2^(e-22) of the feature:
+//   t1 = RN(x + c1)  -> i1 = bits(t1) - bits(c1) = x / 2^(e-22) rounded (ties even), |i1| <= 2^22
+//   r  = x - (t1 - c1)   (exact: Sterbenz, or x itself when t1 - c1 = 0)
+//   t2 = RN(r + c2)  -> i2 = bits(t2) - bits(c2) = r / 2^(e-45) rounded, |i2| <= 2^22
+// so x ~ q 2^(e-45) with q = i1 2^23 + i2 (t1, t2 stay in the binade of c1, c2, where ulps are
+// 2^(e-22) and 2^(e-45); at the upper edge a bit difference still counts those ulps). A piece
+// of <= 2^8 rows sums i1 and i2 in int32 without overflow; cluster totals are int64 pairs
+// (H = sum i1, L = sum i2). The full re-summation and the incremental update call this same
+// function, so both produce the same integers.
+MPK_DEV void fx_q(float x, float2 c, int& i1, int& i2) {
+    const float t1 = __fadd_rn(x, c.x);
+    const float r = __fsub_rn(x, __fsub_rn(t1, c.x));
+    const float t2 = __fadd_rn(r, c.y);
+    i1 = __float_as_int(t1) - __float_as_int(c.x);
+    i2 = __float_as_int(t2) - __float_as_int(c.y);
+}
+// Rows whose label changed since the previous iteration -> list (row, old, new); prev <- labels.
+// gate[0] counts them; when gate[0] > gate[1] (capacity) the list is incomplete and the full
+// re-summation runs instead.
+__global__ void fx_diff_kernel(const int32_t* __restrict__ labels, int32_t* __restrict__ prev,
+                               int64_t n, int3* __restrict__ list, int* __restrict__ gate) {
+    const int lane = threadIdx.x & 31;
+    const int cap = gate[1];
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n;
+         base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        int l = 0, o = 0;
+        bool ch = false;
+        if (i < n) {
+            l = labels[i];
+            o = prev[i];
+            ch = l != o;
+            if (ch) prev[i] = l;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, ch);
+        if (!m) continue;
+        int slot = 0;
+        if (lane == 0) slot = atomicAdd(&gate[0], __popc(m));
+        slot = __shfl_sync(0xffffffffu, slot, 0) + __popc(m & ((1u << lane) - 1u));
+        if (ch && slot < cap) list[slot] = make_int3((int)i, o, l);
+    }
+}
+// Incremental update from the changed-row list: a warp per row, lanes over columns.
+__global__ void __launch_bounds__(256)
+fx_incr_kernel(const float* __restrict__ X, int d, const int3* __restrict__ list,
+               const int* __restrict__ gate, const float2* __restrict__ sc,
+               long long* __restrict__ Shi, long long* __restrict__ Slo, int* __restrict__ cnt) {
+    const int m = gate[0];
+    if (m > gate[1]) return;                              // the full path ran
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t w = warp; w < m; w += nwarps) {
+        const int3 e = list[w];
+        const float* xr = X + (int64_t)e.x * d;
+        for (int t = lane; t < d; t += 32) {
+            int i1, i2;
+            fx_q(__ldg(xr + t), sc[t], i1, i2);
+            const long long hi = i1, lo = i2;
+            atomicAdd(reinterpret_cast<unsigned long long*>(Shi + (int64_t)e.z * d + t), (unsigned long long)hi);
+            atomicAdd(reinterpret_cast<unsigned long long*>(Slo + (int64_t)e.z * d + t), (unsigned long long)lo);
+            if (e.y >= 0) {
+                atomicAdd(reinterpret_cast<unsigned long long*>(Shi + (int64_t)e.y * d + t), (unsigned long long)(-hi));
+                atomicAdd(reinterpret_cast<unsigned long long*>(Slo + (int64_t)e.y * d + t), (unsigned long long)(-lo));
+            }
+        }
+        if (lane == 0) {
+            atomicAdd(&cnt[e.z], 1);
+            if (e.y >= 0) atomicSub(&cnt[e.y], 1);
+        }
+    }
+}
+// U4 in fixed point (same pieces and traversal as segsum_kernel<float, VEC, U>; int64 totals).
+template <int VEC, int U>
+__global__ void __launch_bounds__(256, 4)
+segsum_fx_kernel(const float* __restrict__ X, int64_t n, int d, int k, const int* __restrict__ perm,
+                 const int* __restrict__ offs, const int* __restrict__ mpo, int64_t P, int64_t C,
+                 const float2* __restrict__ sc, long long* __restrict__ Shi,
+                 long long* __restrict__ Slo, long long* __restrict__ part, const int* gate) {
+    if (gated_off(gate)) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int col0 = blockIdx.y * 32 * VEC + lane * VEC;
+    const int ncols = max(0, min(VEC, d - col0));
+    const bool aligned = (d % VEC) == 0;
+    const int64_t e0 = warp * C;
+    if (e0 >= n) return;
+    const int64_t e1 = min(n, e0 + C);
+    float2 scl[VEC];
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) scl[q] = q < ncols ? sc[col0 + q] : make_float2(3.0f, 3.0f);
+    int lo_ = 0, hi_ = k;
+    while (hi_ - lo_ > 1) {
+        int mid = (lo_ + hi_) >> 1;
+        if (offs[mid] <= e0) lo_ = mid; else hi_ = mid;
+    }
+    int j = lo_;
+    int64_t pidx = (e0 - offs[j] + P - 1) / P;
+    int64_t ps = offs[j] + pidx * P;
+    for (;;) {
+        if (ps >= offs[j + 1]) {
+            do { ++j; } while (j < k && offs[j] == offs[j + 1]);
+            if (j >= k) break;
+            pidx = 0;
+            ps = offs[j];
+        }
+        if (ps >= e1) break;
+        const int64_t pe = min((int64_t)offs[j + 1], ps + P);
+        int ah[VEC], al[VEC];                         // <= 2^8 rows of |i| <= 2^22 each
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) { ah[q] = 0; al[q] = 0; }
+        for (int64_t e = ps; e < pe; e += 32) {
+            const int myrow = (e + lane < pe) ? perm[e + lane] : 0;
+            const int cnt = (int)min((int64_t)32, pe - e);
+            for (int u0 = 0; u0 < cnt; u0 += U) {
+                float xv[U][VEC];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int row = __shfl_sync(0xffffffffu, myrow, (u0 + u) & 31);
+                    if (u0 + u < cnt && ncols > 0)
+                        load_vec<float, VEC>(X + (int64_t)row * d + col0, aligned, ncols, xv[u]);
+                    else {
+#pragma unroll
+                        for (int q = 0; q < VEC; ++q) xv[u][q] = 0.0f;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int q = 0; q < VEC; ++q) {
+                        int h, l;
+                        fx_q(xv[u][q], scl[q], h, l);         // zero rows / columns add 0
+                        ah[q] += h;
+                        al[q] += l;
+                    }
+            }
+        }
+        const bool single = offs[j + 1] - offs[j] <= P;
+        if (ncols > 0) {
+#pragma unroll
+            for (int q = 0; q < VEC; ++q)
+                if (q < ncols) {
+                    if (single) {
+                        Shi[(int64_t)j * d + col0 + q] = (long long)ah[q];
+                        Slo[(int64_t)j * d + col0 + q] = (long long)al[q];
+                    } else {
+                        long long* pp = part + (int64_t)(mpo[j] + pidx) * d * 2;
+                        pp[col0 + q] = (long long)ah[q];
+                        pp[d + col0 + q] = (long long)al[q];
+                    }
+                }
+        }
+        ++pidx;
+        ps += P;
+    }
+}
+// U4b in fixed point: the pieces of each multi-piece cluster (any order: integers); empty
+// clusters get zero totals (the incremental path adds to them later).
+__global__ void __launch_bounds__(256)
+segsum_fix_fx_kernel(int d, const int* __restrict__ offs, const int* __restrict__ mpo,
+                     const long long* __restrict__ part, long long* __restrict__ Shi,
+                     long long* __restrict__ Slo, const int* gate) {
+    if (gated_off(gate)) return;
+    const int j = blockIdx.x;
+    const int np = mpo[j + 1] - mpo[j];
+    const int col = blockIdx.y * 32 + (threadIdx.x & 31);
+    const int w = threadIdx.x >> 5;
+    if (offs[j + 1] == offs[j]) {                         // empty cluster
+        if (w == 0 && col < d) { Shi[(int64_t)j * d + col] = 0; Slo[(int64_t)j * d + col] = 0; }
+        return;
+    }
+    if (np == 0) return;
+    __shared__ long long red[2][8][32];
+    long long sh = 0, sl = 0;
+    if (col < d) {
+        const long long* pp = part + (int64_t)mpo[j] * d * 2 + col;
+        for (int p = w; p < np; p += 8) { sh += pp[(int64_t)p * d * 2]; sl += pp[(int64_t)p * d * 2 + d]; }
+    }
+    red[0][w][threadIdx.x & 31] = sh;
+    red[1][w][threadIdx.x & 31] = sl;
+    __syncthreads();
+    if (w == 0 && col < d) {
+        long long a = 0, b = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { a += red[0][q][threadIdx.x & 31]; b += red[1][q][threadIdx.x & 31]; }
+        Shi[(int64_t)j * d + col] = a;
+        Slo[(int64_t)j * d + col] = b;
+    }
+}
+// K8 from the fixed-point totals: c_j = round_u((S_hi 2^31 + S_lo) 2^-F_t / count_j); the rest
+// as finalize_kernel (shift^2, empty clusters keep their centre, Thm 5.3 terms, trace record).
+__global__ void finalize_fx_kernel(int64_t k, int d, const long long* __restrict__ Shi,
+                                   const long long* __restrict__ Slo, const int* __restrict__ cnt,
+                                   const double* __restrict__ isc, const double* __restrict__ acc,
+                                   AccLayout L, float* __restrict__ C, IterRec* __restrict__ rec) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double sh = 0.0, empty = 0.0, rmax = 0.0;
+    for (int64_t j = warp; j < k; j += nwarps) {
+        const double c = (double)cnt[j];
+        double num = 0.0, den = 0.0;
+        for (int t = lane; t < d; t += 32) {
+            const int64_t idx = j * d + t;
+            const float old = C[idx];
+            float nw = old;
+            if (c > 0.0) {
+                const double S = fma((double)Shi[idx], 8388608.0, (double)Slo[idx]) * isc[t];   // (H 2^23 + L) 2^(e-45)
+                nw = __double2float_rn(S / c);
+            }
+            const double df = (double)nw - (double)old;
+            num += df * df;
+            den += fabs(df) * fabs((double)nw);
+            C[idx] = nw;
+        }
+        num = warp_sum(num);
+        den = warp_sum(den);
+        if (lane == 0) {
+            sh += num;
+            if (c == 0.0) empty += 1.0;
+            if (num > 0.0 && den > 0.0) rmax = fmax(rmax, 2.0 * den / num);
+        }
+    }
+    __shared__ double red[3][8];
+    if (lane == 0) { red[0][threadIdx.x >> 5] = sh; red[1][threadIdx.x >> 5] = empty; red[2][threadIdx.x >> 5] = rmax; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0, r = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += red[0][w]; b += red[1][w]; r = fmax(r, red[2][w]); }
+        atomicAdd(&rec->shift2, a);
+        if (b != 0.0) atomicAdd(&rec->empty, b);
+        if (r > 0.0)
+            atomicMax(reinterpret_cast<unsigned long long*>(&rec->ub_inv),
+                      (unsigned long long)__double_as_longlong(r));
+        if (blockIdx.x == 0) {
+            rec->sse = acc[L.sse()];
+            rec->changed = acc[L.changed()];
+        }
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_update(int work, const void* Xw, int64_t n, int d, int k,
@@ -544,6 +877,79 @@ cudaError_t launch_finalize(int work, int64_t k, int d, const double* acc, AccLa
     else
         finalize_kernel<float><<<g, 256, 0, s>>>(k, d, acc, L, (float*)Cw, rec);
     return cudaGetLastError();
+}
+
+// ---- FX public entry points (internal.h) ---------------------------------------------------
+cudaError_t launch_fx_prepare(const float* Xw, int64_t n, int d, FxState& fx, cudaStream_t s) {
+    launches_add(2);
+    cudaError_t e = cudaMemsetAsync(fx.amax, 0, sizeof(unsigned) * d, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(fx.gate, 0, sizeof(int) * 4, s);
+    if (e != cudaSuccess) return e;
+    if (d % 4 == 0 && d <= 1024 && ((uintptr_t)Xw & 15) == 0) {
+        fx_colmax_vec_kernel<<<kNumSMs * 8, 256, 0, s>>>(Xw, n, d, fx.amax, fx.gate);
+    } else {
+        int g = (int)std::min<int64_t>((n + 7) / 8, kNumSMs * 8);
+        if (g < 1) g = 1;
+        fx_colmax_kernel<<<g, 256, sizeof(unsigned) * d, s>>>(Xw, n, d, fx.amax, fx.gate);
+    }
+    fx_scale_kernel<<<(d + 127) / 128, 128, 0, s>>>(fx.amax, d, fx.sc, fx.isc, fx.gate);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_update_fx(const float* Xw, int64_t n, int d, int k, const int32_t* labels,
+                             int* cnt, int* offs, int* cursor, int* perm, const UpdateScratch& us,
+                             FxState& fx, cudaStream_t s) {
+    launches_add(9);
+    // gate[0] = changed rows (reset), gate[1] = capacity (kept)
+    cudaError_t e = cudaMemsetAsync(fx.gate, 0, sizeof(int), s);
+    if (e != cudaSuccess) return e;
+    int g = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 8);
+    if (g < 1) g = 1;
+    fx_diff_kernel<<<g, 256, 0, s>>>(labels, fx.prev, n, fx.list, fx.gate);
+    const int* gate = fx.gate;
+    // full re-summation, gated: runs only when the list overflowed
+    const int64_t nb = (n + kDetRows - 1) / kDetRows;
+    block_count_kernel<<<(unsigned)nb, kDetThreads, sizeof(int) * k, s>>>(labels, n, k, us.cb, gate);
+    block_scan_kernel<<<(unsigned)((k + 31) / 32), 1024, 0, s>>>(us.cb, nb, k, cnt, gate);
+    const int64_t P = kPiece;
+    scan_kernel<<<1, 1024, 0, s>>>(cnt, k, P, offs, cursor, us.mpo, nullptr, gate);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(scatter_det_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kDetHistBytes + kDetRows * (int)sizeof(int));
+        attr = true;
+    }
+    scatter_det_kernel<<<(unsigned)nb, 32 * scatter_warps(k), scatter_smem(k), s>>>(
+        labels, n, k, offs, us.cb, perm, gate);
+    const int VEC = d <= 32 ? 1 : (d <= 64 ? 2 : 4);
+    const int colblk = 32 * VEC;
+    const int64_t C = segsum_chunk(n);
+    const int64_t nw = (n + C - 1) / C;
+    dim3 grid((unsigned)((nw + 7) / 8), (unsigned)((d + colblk - 1) / colblk), 1);
+#define SEGSUMFX(V) segsum_fx_kernel<V, 8><<<grid, 256, 0, s>>>(Xw, n, d, k, perm, offs, us.mpo, P, C, \
+                                                                fx.sc, fx.Shi, fx.Slo, fx.part, gate)
+    if (VEC == 1) SEGSUMFX(1); else if (VEC == 2) SEGSUMFX(2); else SEGSUMFX(4);
+#undef SEGSUMFX
+    segsum_fix_fx_kernel<<<dim3((unsigned)k, (unsigned)((d + 31) / 32)), 256, 0, s>>>(
+        d, offs, us.mpo, fx.part, fx.Shi, fx.Slo, gate);
+    // incremental update, gated the other way
+    fx_incr_kernel<<<kNumSMs * 4, 256, 0, s>>>(Xw, d, fx.list, gate, fx.sc, fx.Shi, fx.Slo, cnt);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize_fx(int64_t k, int d, const FxState& fx, const int* cnt,
+                               const double* acc, AccLayout L, float* Cw, IterRec* rec,
+                               cudaStream_t s) {
+    launches_add(1);
+    int g = (int)std::min<int64_t>((k + 7) / 8, kNumSMs * 2);
+    if (g < 1) g = 1;
+    finalize_fx_kernel<<<g, 256, 0, s>>>(k, d, fx.Shi, fx.Slo, cnt, fx.isc, acc, L, Cw, rec);
+    return cudaGetLastError();
+}
+
+size_t fx_part_bytes(int64_t n, int d) {
+    const int64_t slots = 2 * ((n + kPiece - 1) / kPiece) + 1;
+    return (size_t)slots * d * 2 * sizeof(long long);
 }
 
 }  // namespace mpk

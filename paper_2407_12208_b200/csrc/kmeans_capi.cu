@@ -80,6 +80,10 @@ struct kmeans_ctx {
     unsigned long long* cand_key = nullptr;   // per row: min (value, column) key
     int dist_kernel = 0;
     AccLayout L{0, 0};
+    // exact fixed-point totals with incremental updates (R9): fp32 work, one rank,
+    // k <= 12288, not the fused small-d path; off for a fit whose X holds a non-finite value
+    bool fx_ok = false;
+    FxState fx;
 
     // distributed
     ncclComm_t comm = nullptr;
@@ -171,7 +175,8 @@ void free_all(kmeans_ctx* h) {
     void* bufs[] = {h->Xw, h->xl_alias ? nullptr : h->Xl, h->xn, h->sx, h->Cw, h->Cl, h->cn,
                     h->sc, h->labels, h->acc, h->cnt, h->offs, h->cursor, h->perm, h->trace,
                     h->shift, h->scale, h->partials, h->census, h->sse_dev, h->us.cb,
-                    h->us.part, h->us.mpo};
+                    h->us.part, h->us.mpo, h->fx.amax, h->fx.sc, h->fx.isc, h->fx.Shi,
+                    h->fx.Slo, h->fx.part, h->fx.prev, h->fx.list, h->fx.gate};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
@@ -279,6 +284,23 @@ int create_impl(int64_t n, int32_t d, int32_t k, int work, int dist, int flags,
         CA(dalloc(&h->us.cb, b_cb));
         CA(dalloc(&h->us.part, b_part));
         CA(dalloc(&h->us.mpo, b_pid));
+    }
+    h->fx_ok = work == KMEANS_FP32 && nranks == 1 && k <= 12288 && d <= 8192 &&
+               h->dist_kernel != DK_SMALLD && !getenv("MPK_NO_FX");
+    if (h->fx_ok) {
+        // list capacity n/16 rows: beyond it the full re-summation is the cheaper path.
+        // MPK_FX_CAP overrides (tests: 0 = always the full path, n = always incremental)
+        h->fx.cap = (int)std::min<int64_t>(std::max<int64_t>(n / 16, 4096), n);
+        if (const char* e = getenv("MPK_FX_CAP")) h->fx.cap = (int)std::min<int64_t>(atoll(e), n);
+        CA(dalloc(&h->fx.amax, (size_t)d * sizeof(unsigned)));
+        CA(dalloc(&h->fx.sc, (size_t)d * sizeof(float2)));
+        CA(dalloc(&h->fx.isc, (size_t)d * sizeof(double)));
+        CA(dalloc(&h->fx.Shi, (size_t)k * d * sizeof(long long)));
+        CA(dalloc(&h->fx.Slo, (size_t)k * d * sizeof(long long)));
+        CA(dalloc(&h->fx.part, fx_part_bytes(n, d)));
+        CA(dalloc(&h->fx.prev, (size_t)n * sizeof(int32_t)));
+        CA(dalloc(&h->fx.list, (size_t)h->fx.cap * sizeof(int3)));
+        CA(dalloc(&h->fx.gate, 4 * sizeof(int)));
     }
     CA(dalloc(&h->trace, (size_t)KMEANS_MAX_TRACE * sizeof(IterRec)));
     CA(dalloc(&h->shift, (size_t)d * sizeof(double)));
@@ -589,6 +611,22 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
     CK(cudaMemsetAsync(h->n_low_dev, 0, sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(h->labels, 0xff, (size_t)n * sizeof(int32_t), s));   // labels_prev = -1
     CK(cudaMemsetAsync(h->trace, 0, sizeof(IterRec) * KMEANS_MAX_TRACE, s));
+    bool fx_on = false;
+    if (h->fx_ok) {
+        // FX state for this fit: per-feature grids from max |x|, zero totals and counts, previous
+        // labels -1 (every row is "changed" in iteration 1). One host read: a non-finite X
+        // disables FX for the fit (the grid needs finite values).
+        CK(launch_fx_prepare((const float*)h->Xw, n, d, h->fx, s));
+        CK(cudaMemsetAsync(h->fx.Shi, 0, (size_t)k * d * sizeof(long long), s));
+        CK(cudaMemsetAsync(h->fx.Slo, 0, (size_t)k * d * sizeof(long long), s));
+        CK(cudaMemsetAsync(h->cnt, 0, (size_t)k * sizeof(int), s));
+        CK(cudaMemsetAsync(h->fx.prev, 0xff, (size_t)n * sizeof(int32_t), s));
+        CK(cudaMemcpyAsync(h->fx.gate + 1, &h->fx.cap, sizeof(int), cudaMemcpyHostToDevice, s));
+        int bad = 0;
+        CK(cudaMemcpyAsync(&bad, h->fx.gate + 2, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        fx_on = bad == 0;
+    }
     CK(cudaEventRecord(e1, s));
 
     // ---- A3..A7: Lloyd iterations ---------------------------------------------------------
@@ -615,14 +653,21 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
             if (int rc = run_assign(h, n, h->acc + h->L.sse(), h->acc + h->L.changed()))
                 return rc;                                                   // A4
             if (timing) CK(cudaEventRecord(t1, s));
-            CK(launch_update(h->work, h->Xw, n, d, k, h->labels, h->cnt, h->offs, h->cursor,
-                             h->perm, h->acc, h->L, h->us, s));              // A5
+            if (fx_on)
+                CK(launch_update_fx((const float*)h->Xw, n, d, k, h->labels, h->cnt, h->offs,
+                                    h->cursor, h->perm, h->us, h->fx, s));   // A5 (R9)
+            else
+                CK(launch_update(h->work, h->Xw, n, d, k, h->labels, h->cnt, h->offs, h->cursor,
+                                 h->perm, h->acc, h->L, h->us, s));          // A5
             if (timing) CK(cudaEventRecord(t2, s));
         }
         if (h->comm)                                                         // A6
             CKN(ncclAllReduce(h->acc, h->acc, h->L.total(), ncclDouble, ncclSum, h->comm, s));
         if (timing) CK(cudaEventRecord(t3, s));
-        CK(launch_finalize(h->work, k, d, h->acc, h->L, h->Cw, rec, s));    // A7
+        if (fx_on)
+            CK(launch_finalize_fx(k, d, h->fx, h->cnt, h->acc, h->L, (float*)h->Cw, rec, s));
+        else
+            CK(launch_finalize(h->work, k, d, h->acc, h->L, h->Cw, rec, s));    // A7
         if (timing) { CK(cudaEventRecord(t4, s)); kev.insert(kev.end(), {t0, t1, t2, t3, t4}); }
         if (tol >= 0.0) {
             CK(cudaMemcpyAsync(&rec_h, rec, sizeof(IterRec), cudaMemcpyDeviceToHost, s));

@@ -342,3 +342,47 @@ def test_wide_rows_zscore_fit_parity(d, dist, guard):
     for a, b in zip(st["sse_t"], ref["sse_t"]):
         assert abs(a - b) <= 1e-3 * b
     assert adjusted_rand_score(ref["labels"], g["labels"]) >= 0.99
+
+
+def _fit_env(env, X, C0, work, dist, **kw):
+    import os
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return gpu_fit(X, C0, work, dist, **kw)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("dist,norm", [("fp16", "zscore"), ("e5m2", "none"), ("fp32", "none")])
+def test_fx_incremental_equals_full_resummation(dist, norm):
+    """R9: the exact fixed-point totals make a cluster's centre a function of its members only,
+    so updating them from the changed rows (MPK_FX_CAP = n: always incremental) and re-summing
+    all rows every iteration (MPK_FX_CAP = 0: always the full path) give bit-identical labels,
+    centres, SSE traces and counts — over a whole fit in which labels keep changing."""
+    X, _, C0 = synth.make("c3_blobs_1m_d64", n=30000, seed=4)
+    C0 = C0[:200].copy()
+    a = _fit_env({"MPK_FX_CAP": "0"}, X, C0, "fp32", dist, norm=norm, max_iter=12)
+    b = _fit_env({"MPK_FX_CAP": str(len(X))}, X, C0, "fp32", dist, norm=norm, max_iter=12)
+    assert np.array_equal(a["labels"], b["labels"])
+    assert np.array_equal(a["centroids"].view(np.uint32), b["centroids"].view(np.uint32))
+    assert a["stats"]["sse_t"] == b["stats"]["sse_t"]
+    assert a["stats"]["changed_t"] == b["stats"]["changed_t"]
+    # several iterations after the first two moved labels (the incremental path had work)
+    assert sum(1 for c in a["stats"]["changed_t"][2:] if c > 0) >= 2
+
+
+def test_fx_matches_fp64_summation_path():
+    """The fixed-point totals (default) and the fp64 summation of R7 (MPK_NO_FX) agree: the means
+    differ at most by the fp64 path's own rounding (a few fp32 ulps), labels essentially equal."""
+    X, _, C0 = synth.make("c3_blobs_1m_d64", n=30000, seed=6)
+    C0 = C0[:64].copy()
+    a = _fit_env({}, X, C0, "fp32", "fp16", norm="zscore", max_iter=8)
+    b = _fit_env({"MPK_NO_FX": "1"}, X, C0, "fp32", "fp16", norm="zscore", max_iter=8)
+    assert np.mean(a["labels"] == b["labels"]) > 0.999
+    assert np.allclose(a["centroids"], b["centroids"], rtol=4 * 2.0 ** -24, atol=1e-6)
+    assert abs(a["sse"] - b["sse"]) <= 1e-6 * b["sse"]

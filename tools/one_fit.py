@@ -20,3 +20,4 @@ for _ in range(2):
 torch.cuda.synchronize()
 st = km.stats()
 print("rc", rc, "sse", sse, "iters", it, {k: v for k, v in st.items() if k.startswith("t_")})
+print("changed fraction per iteration:", [round(c / cfg.n, 4) for c in st["changed_t"]])
