@@ -386,3 +386,29 @@ def test_fx_matches_fp64_summation_path():
     assert np.mean(a["labels"] == b["labels"]) > 0.999
     assert np.allclose(a["centroids"], b["centroids"], rtol=4 * 2.0 ** -24, atol=1e-6)
     assert abs(a["sse"] - b["sse"]) <= 1e-6 * b["sse"]
+
+
+def test_fx_centres_are_the_rounded_exact_means():
+    """R9: eq:center in precision u (Alg 3 step 4) from the fixed-point totals
+    is the exact mean of the members rounded once to fp32 — up to the grid (2^-45 of max |x_t|)
+    and the fp64 division, i.e. equal to round_fp32(mean in fp64) except at rounding ties."""
+    n, d, k = 40000, 48, 37
+    X, _ = synth.blobs(n, d, 12, sigma=2.0, seed=11, dtype=np.float32)
+    X[:, 3] *= 1e-3                                   # features of different magnitudes
+    X[:, 7] += 100.0
+    C0 = synth.init_rows(X, k, 5)
+    km = mpk.KMeans(n, d, k, "fp32", "fp16")
+    mpk.kmeans_set_centroids(km.h, dev(C0))
+    lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    km.assign(dev(X), lab)
+    cent = torch.empty((k, d), dtype=torch.float32, device="cuda")
+    km.fit(dev(X), dev(C0), max_iter=1, tol=-1.0, centroids=cent)
+    km.close()
+    g = lab.cpu().numpy()
+    C = cent.cpu().numpy()
+    exact = np.stack([X[g == j].astype(np.float64).mean(0) if np.any(g == j)
+                      else C0[j].astype(np.float64) for j in range(k)])
+    want = exact.astype(np.float32)
+    ulps = np.abs(C.view(np.int32).astype(np.int64) - want.view(np.int32).astype(np.int64))
+    assert ulps.max() <= 1
+    assert np.mean(ulps == 0) >= 0.999
