@@ -81,7 +81,8 @@ bool prep_fast_ok(int work, int d);
 cudaError_t launch_prep_fast(int dist, const void* Xin, int64_t rows, int d, int d_pad, int guard,
                              void* norms, void* scales, void* Xl, unsigned long long* census,
                              void* Xout, const double* shift, const double* scale,
-                             cudaStream_t s);
+                             cudaStream_t s, unsigned* amax = nullptr, int* flags = nullptr,
+                             bool* amax_done = nullptr);
 cudaError_t launch_prep(int work, int dist, const void* Xw, int64_t rows, int d, int d_pad,
                         int guard, void* norms, void* scales, void* Xl,
                         unsigned long long* census /* [nonfinite, underflow] */, cudaStream_t s);
@@ -188,7 +189,8 @@ struct FxState {
     int* gate = nullptr;        // [0] changed rows, [1] capacity, [2] non-finite X flag
     int cap = 0;
 };
-cudaError_t launch_fx_prepare(const float* Xw, int64_t n, int d, FxState& fx, cudaStream_t s);
+cudaError_t launch_fx_prepare(const float* Xw, int64_t n, int d, FxState& fx, bool have_amax,
+                              cudaStream_t s);
 cudaError_t launch_update_fx(const float* Xw, int64_t n, int d, int k, const int32_t* labels,
                              int* cnt, int* offs, int* cursor, int* perm, const UpdateScratch& us,
                              FxState& fx, cudaStream_t s);

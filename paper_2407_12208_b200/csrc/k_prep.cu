@@ -649,10 +649,15 @@ prep_vec_kernel(const float* __restrict__ Xin, int64_t rows, int d, int guard,
                 float* __restrict__ norms, float* __restrict__ scales,
                 typename low_type<DIST>::T* __restrict__ Xl,
                 unsigned long long* __restrict__ census, float* __restrict__ Xout,
-                const double* __restrict__ shift, const double* __restrict__ scale) {
+                const double* __restrict__ shift, const double* __restrict__ scale,
+                unsigned* __restrict__ amax, int* __restrict__ flags) {
     using L = typename low_type<DIST>::T;
     constexpr bool same = DIST == KMEANS_FP32;
     const int lane = threadIdx.x & 31;
+    // amax != nullptr: also the per-column max |x| of the (normalised) rows and flags[2] |= 1 on
+    // a non-finite value, for the fixed-point update (k_update.cu FX) — saves it a pass over X
+    unsigned mx[V][4] = {};
+    unsigned bad = 0;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     double sh[V][4], sc[V][4], rc[V][4];
@@ -691,6 +696,16 @@ prep_vec_kernel(const float* __restrict__ Xin, int64_t rows, int d, int guard,
                     reinterpret_cast<float4*>(Xout + ir * d + 128 * w)[lane] =
                         make_float4(v[w][0], v[w][1], v[w][2], v[w][3]);
                 }
+            }
+            if (amax) {
+#pragma unroll
+                for (int w = 0; w < V; ++w)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float a = fabsf(v[w][e]);
+                        if (!(a <= 3.402823466e38f)) bad = 1;
+                        else mx[w][e] = max(mx[w][e], __float_as_uint(a));
+                    }
             }
             float ss = 0.0f, cs = 0.0f;
 #pragma unroll
@@ -742,6 +757,20 @@ prep_vec_kernel(const float* __restrict__ Xin, int64_t rows, int d, int guard,
             }
         }
     }
+    if (amax) {
+        __shared__ unsigned smx[256];
+        for (int t = threadIdx.x; t < d; t += blockDim.x) smx[t] = 0u;
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < V; ++w)
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (mx[w][e]) atomicMax(&smx[128 * w + 4 * lane + e], mx[w][e]);
+        __syncthreads();
+        for (int t = threadIdx.x; t < d; t += blockDim.x)
+            if (smx[t]) atomicMax(&amax[t], smx[t]);
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&flags[2], 1);
+    }
     if (census) {
         const unsigned long long a = warp_sum((unsigned long long)n_nonfinite);
         const unsigned long long b = warp_sum((unsigned long long)n_under);
@@ -756,7 +785,7 @@ template <int DIST>
 static void prep_fast_launch(const float* Xin, int64_t rows, int d, int d_pad, int guard,
                              float* norms, float* scales, void* Xl, unsigned long long* census,
                              float* Xout, const double* shift, const double* scale,
-                             cudaStream_t s) {
+                             cudaStream_t s, unsigned* amax, int* flags, bool* amax_done) {
     using L = typename low_type<DIST>::T;
     const int g = grid_for(rows * 8, 256, 8);
     const bool aligned = (((uintptr_t)Xin | (uintptr_t)Xout | (uintptr_t)Xl) & 15) == 0;
@@ -764,18 +793,19 @@ static void prep_fast_launch(const float* Xin, int64_t rows, int d, int d_pad, i
         if (d == 128) {
             if (shift)
                 prep_vec_kernel<DIST, true, 1, 4><<<g, 256, 0, s>>>(Xin, rows, d, guard, norms, scales,
-                                                                    (L*)Xl, census, Xout, shift, scale);
+                                                                    (L*)Xl, census, Xout, shift, scale, amax, flags);
             else
                 prep_vec_kernel<DIST, false, 1, 4><<<g, 256, 0, s>>>(Xin, rows, d, guard, norms, scales,
-                                                                     (L*)Xl, census, Xout, shift, scale);
+                                                                     (L*)Xl, census, Xout, shift, scale, amax, flags);
         } else {
             if (shift)
                 prep_vec_kernel<DIST, true, 2, 2><<<g, 256, 0, s>>>(Xin, rows, d, guard, norms, scales,
-                                                                    (L*)Xl, census, Xout, shift, scale);
+                                                                    (L*)Xl, census, Xout, shift, scale, amax, flags);
             else
                 prep_vec_kernel<DIST, false, 2, 2><<<g, 256, 0, s>>>(Xin, rows, d, guard, norms, scales,
-                                                                     (L*)Xl, census, Xout, shift, scale);
+                                                                     (L*)Xl, census, Xout, shift, scale, amax, flags);
         }
+        if (amax_done) *amax_done = amax != nullptr;
         return;
     }
     // d_pad columns of Xl must be covered by the lane's Q slots too
@@ -835,18 +865,19 @@ bool prep_fast_ok(int work, int d) { return work == KMEANS_FP32 && d <= 256; }
 cudaError_t launch_prep_fast(int dist, const void* Xin, int64_t rows, int d, int d_pad, int guard,
                              void* norms, void* scales, void* Xl, unsigned long long* census,
                              void* Xout, const double* shift, const double* scale,
-                             cudaStream_t s) {
+                             cudaStream_t s, unsigned* amax, int* flags, bool* amax_done) {
     launches_add(1);
+    if (amax_done) *amax_done = false;
     if (rows <= 0) return cudaSuccess;
     const float* xi = (const float*)Xin;
     float* xo = (float*)Xout;
     float* nr = (float*)norms;
     float* sc = (float*)scales;
     switch (dist) {
-        case KMEANS_FP32: prep_fast_launch<KMEANS_FP32>(xi, rows, d, d_pad, guard, nr, sc, Xl, census, xo, shift, scale, s); break;
-        case KMEANS_FP16: prep_fast_launch<KMEANS_FP16>(xi, rows, d, d_pad, guard, nr, sc, Xl, census, xo, shift, scale, s); break;
-        case KMEANS_BF16: prep_fast_launch<KMEANS_BF16>(xi, rows, d, d_pad, guard, nr, sc, Xl, census, xo, shift, scale, s); break;
-        case KMEANS_E5M2: prep_fast_launch<KMEANS_E5M2>(xi, rows, d, d_pad, guard, nr, sc, Xl, census, xo, shift, scale, s); break;
+        case KMEANS_FP32: prep_fast_launch<KMEANS_FP32>(xi, rows, d, d_pad, guard, nr, sc, Xl, census, xo, shift, scale, s, amax, flags, amax_done); break;
+        case KMEANS_FP16: prep_fast_launch<KMEANS_FP16>(xi, rows, d, d_pad, guard, nr, sc, Xl, census, xo, shift, scale, s, amax, flags, amax_done); break;
+        case KMEANS_BF16: prep_fast_launch<KMEANS_BF16>(xi, rows, d, d_pad, guard, nr, sc, Xl, census, xo, shift, scale, s, amax, flags, amax_done); break;
+        case KMEANS_E5M2: prep_fast_launch<KMEANS_E5M2>(xi, rows, d, d_pad, guard, nr, sc, Xl, census, xo, shift, scale, s, amax, flags, amax_done); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

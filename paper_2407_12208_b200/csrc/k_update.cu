@@ -880,12 +880,13 @@ cudaError_t launch_finalize(int work, int64_t k, int d, const double* acc, AccLa
 }
 
 // ---- FX public entry points (internal.h) ---------------------------------------------------
-cudaError_t launch_fx_prepare(const float* Xw, int64_t n, int d, FxState& fx, cudaStream_t s) {
+// amax and gate are zeroed by the caller before the point prep (which may fill amax itself:
+// have_amax skips the pass over X here)
+cudaError_t launch_fx_prepare(const float* Xw, int64_t n, int d, FxState& fx, bool have_amax,
+                              cudaStream_t s) {
     launches_add(2);
-    cudaError_t e = cudaMemsetAsync(fx.amax, 0, sizeof(unsigned) * d, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(fx.gate, 0, sizeof(int) * 4, s);
-    if (e != cudaSuccess) return e;
-    if (d % 4 == 0 && d <= 1024 && ((uintptr_t)Xw & 15) == 0) {
+    if (have_amax) {
+    } else if (d % 4 == 0 && d <= 1024 && ((uintptr_t)Xw & 15) == 0) {
         fx_colmax_vec_kernel<<<kNumSMs * 8, 256, 0, s>>>(Xw, n, d, fx.amax, fx.gate);
     } else {
         int g = (int)std::min<int64_t>((n + 7) / 8, kNumSMs * 8);

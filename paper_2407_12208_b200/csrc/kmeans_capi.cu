@@ -83,6 +83,7 @@ struct kmeans_ctx {
     // exact fixed-point totals with incremental updates (R9): fp32 work, one rank,
     // k <= 12288, not the fused small-d path; off for a fit whose X holds a non-finite value
     bool fx_ok = false;
+    bool fx_amax_done = false;     // this fit's prep computed the column maxima
     FxState fx;
 
     // distributed
@@ -572,6 +573,11 @@ int prepare_points(kmeans_ctx* h, const void* X) {
     const int64_t n = h->n;
     const int d = h->d;
     const bool norm = h->norm != KMEANS_NORM_NONE;
+    h->fx_amax_done = false;
+    if (h->fx_ok) {             // the prep may fill the fixed-point update's column maxima
+        CK(cudaMemsetAsync(h->fx.amax, 0, sizeof(unsigned) * d, s));
+        CK(cudaMemsetAsync(h->fx.gate, 0, sizeof(int) * 4, s));
+    }
     const void* Xsrc = h->Xw;
     if (norm && is_device_ptr(X)) Xsrc = X;
     else if (int rc = stage_rows(h, X, n, h->Xw)) return rc;
@@ -581,7 +587,8 @@ int prepare_points(kmeans_ctx* h, const void* X) {
     if (prep_fast_ok(h->work, d)) {
         CK(launch_prep_fast(h->dist, Xsrc, n, d, h->d_pad, h->guard, h->xn, h->sx, h->Xl,
                             h->census, norm ? h->Xw : nullptr, norm ? h->shift : nullptr,
-                            norm ? h->scale : nullptr, s));
+                            norm ? h->scale : nullptr, s, h->fx_ok ? h->fx.amax : nullptr,
+                            h->fx_ok ? h->fx.gate : nullptr, &h->fx_amax_done));
     } else {
         if (norm) CK(launch_norm_apply(h->work, h->Xw, n, d, h->shift, h->scale, s, Xsrc));
         CK(launch_prep(h->work, h->dist, h->Xw, n, d, h->d_pad, h->guard, h->xn, h->sx, h->Xl,
@@ -616,7 +623,7 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
         // FX state for this fit: per-feature grids from max |x|, zero totals and counts, previous
         // labels -1 (every row is "changed" in iteration 1). One host read: a non-finite X
         // disables FX for the fit (the grid needs finite values).
-        CK(launch_fx_prepare((const float*)h->Xw, n, d, h->fx, s));
+        CK(launch_fx_prepare((const float*)h->Xw, n, d, h->fx, h->fx_amax_done, s));
         CK(cudaMemsetAsync(h->fx.Shi, 0, (size_t)k * d * sizeof(long long), s));
         CK(cudaMemsetAsync(h->fx.Slo, 0, (size_t)k * d * sizeof(long long), s));
         CK(cudaMemsetAsync(h->cnt, 0, (size_t)k * sizeof(int), s));
