@@ -50,6 +50,9 @@ constexpr int P_NON_EPI = 4;
 #ifndef MPK_PAIR_ACC_DBUF
 #define MPK_PAIR_ACC_DBUF 1              // NB = 256 ASSIGN: double-buffered TMEM loads
 #endif
+#ifndef MPK_PAIR_FWD
+#define MPK_PAIR_FWD 1                   // ASSIGN NB=256: release accumulators via warp 2 (below)
+#endif
 #ifndef MPK_PAIR_HOT_WAIT
 #define MPK_PAIR_HOT_WAIT 1              // epilogue: test_wait before a bare try_wait loop
 #endif
@@ -62,6 +65,7 @@ constexpr uint32_t TRACE_T = 256;        // tiles traced under MPK_PAIR_TRACE
 // named barriers (0 is __syncthreads)
 constexpr int BAR_TILE = 1;              // the epilogue warps, once per tile
 constexpr int BAR_PART = 2;              // + parity: partials written (epilogue -> warp 3)
+constexpr int BAR_REL = 5;               // + buffer: accumulator's TMEM loads done (epilogue -> warp 2)
 // "partials consumed" (warp 3 -> epilogue) is an mbarrier per parity (part_free), not a named
 // barrier: the epilogue warps only wait on it, so they do not all meet once per row-block
 
@@ -134,6 +138,14 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
     const int lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
     const bool leader = rank == 0;
+    // ASSIGN with 256-column tiles: each epilogue warp signals a named barrier (bar.arrive, no
+    // wait) as soon as its last TMEM load of the tile has landed — before folding that chunk —
+    // and warp 2 (idle once C~ is resident) turns the completed barrier into the one remote
+    // "accumulator empty" arrival of its CTA. The MMA for tile t+2 then starts a quarter of a
+    // fold earlier than with the arrival after the fold.
+    const bool fwd = REV && MPK_PAIR_FWD && p.NB == 256 && p.nacc == 2 && (P_EWG == 2 || P_EWG == 4) &&
+                     !p.is_f8 &&
+                     MPK_PAIR_ACC_DBUF && !p.guard;
 
     for (int j = threadIdx.x; j < p.k_pad; j += blockDim.x) {
         cn_s[j] = j < p.k ? p.cn[j] : INFINITY;       // padded centroids never win
@@ -147,7 +159,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
         for (int i = 0; i < p.nacc; ++i) {
             mbar_init(smem_u32(&t_full[i]), 1);
             // one arrival per CTA (named barrier first), or one per epilogue warp
-            mbar_init(smem_u32(&t_empty[i]), MPK_PAIR_WARP_ARRIVE ? 2 * P_EPI : 2);
+            mbar_init(smem_u32(&t_empty[i]), (fwd || !MPK_PAIR_WARP_ARRIVE) ? 2 : 2 * P_EPI);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x)) : "memory");
@@ -187,6 +199,16 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             }
         }
         __syncwarp();
+        if (fwd) {
+            int b = 0;
+            for (int64_t rb = pair; rb < num_rb; rb += npairs)
+                for (int t = 0; t < p.NT; ++t) {
+                    named_bar_sync(BAR_REL + b, P_EPI * 32 + 32);
+                    if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&t_empty[b]), 0));
+                    __syncwarp();
+                    b ^= 1;
+                }
+        }
     } else if (warp == 0) {
         // ------------------------------------------------ X~ producer (this CTA's 128 rows);
         // the whole warp waits, one elected lane issues
@@ -432,6 +454,24 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                                 tmem_wait_ld_dep(va);
                                 fold_rev_m3<2, GD>(va, q, m2, cv, s2);
                             }
+                            if (P_EWG == 4 && nch == 2 && c == wcols) {
+                                // 4 warps per SMSP: two chunks per warp and tile, scalar
+                                // offsets; the other warps hide the TMEM load latency
+                                ChunkCn<4, GD> q;
+                                load_chunk_cn<4, GD>(cn_s, sc_s, jbase + 32, q);
+                                tmem_ld32(col0 + 32, va);
+                                tmem_wait_ld_dep(va);
+                                fold_rev_m3s<4, GD>(va, q, m2, cv, cs);
+                                load_chunk_cn<4, GD>(cn_s, sc_s, jbase, q);
+                                tmem_ld32(col0, va);
+                                tmem_wait_ld_dep(va);
+                                if (fwd) {
+                                    tc_fence_before();
+                                    named_bar_arrive(BAR_REL + buf, P_EPI * 32 + 32);
+                                }
+                                fold_rev_m3s<4, GD>(va, q, m2, cv, cs);
+                                return;
+                            }
                             if (MPK_PAIR_ACC_DBUF && !GD && nch == 4 && c == wcols) {
                                 // NB = 256: four chunks unrolled, the TMEM load of the next chunk
                                 // in flight while this one folds (the load's ~180-cycle latency
@@ -452,6 +492,10 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                                 load_chunk_cn<4, GD>(cn_s, sc_s, jbase + 32, q);
                                 fold_rev_m3<4, GD>(va, q, m2, cv, s2);
                                 tmem_wait_ld_dep(vb);
+                                if (fwd) {
+                                    tc_fence_before();
+                                    named_bar_arrive(BAR_REL + buf, P_EPI * 32 + 32);
+                                }
                                 load_chunk_cn<4, GD>(cn_s, sc_s, jbase, q);
                                 fold_rev_m3<4, GD>(vb, q, m2, cv, s2);
                                 return;
@@ -525,7 +569,9 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 // one arrival per CTA: the epilogue warps meet at a named barrier, then a single
                 // thread signals the leader's "accumulator empty"
                 tc_fence_before();
-                if (MPK_PAIR_WARP_ARRIVE) {
+                if (fwd) {
+                    // released through warp 2 before the last chunk's fold
+                } else if (MPK_PAIR_WARP_ARRIVE) {
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&t_empty[buf]), 0));
                 } else {
@@ -539,7 +585,8 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             if (CAND) continue;
             // chains -> columns: ordinal v = t * gpt + g' (tile t, g'-th group of this
             // warpgroup's columns in it); merge: lowest value, then lowest column
-            if (!FINAL) {
+            // (the 4-warpgroup ASSIGN path keeps scalar offsets in cs already)
+            if (!FINAL && !(REV && P_EWG == 4 && wcols == 64)) {
 #pragma unroll
                 for (int m = 0; m < NCH / 2; ++m) unpack2(s2[m], cs[2 * m], cs[2 * m + 1]);
             }

@@ -381,6 +381,47 @@ MPK_DEV void fold_rev_m3(const uint32_t (&v)[32], const float* cn_s, const float
     fold_rev_m3<G, GUARD>(v, q, m2, cv, s2);
 }
 
+// Scalar-offset form of fold_rev_m3 (same values, same chain rule; two scalar FFMAs per chain
+// step instead of two packed FFMA2 per chain pair): with 4 warps per SM sub-partition it issued
+// faster than the packed form in tools/fold_bench.cu (112 vs 143 cycles per chunk per SMSP).
+MPK_DEV void chain_pair(float xa, float xb, float& v, float& s) {
+    float w, na, nb;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(w) : "f"(v), "f"(xa), "f"(xb));
+    asm("set.gtu.f32.f32 %0, %1, %2;" : "=f"(na) : "f"(xa), "f"(v));
+    asm("set.gtu.f32.f32 %0, %1, %2;" : "=f"(nb) : "f"(xb), "f"(w));
+    v = w;
+    s = fmaf(fmaf(s, na, -1.0f), nb, -1.0f);
+}
+template <int G, bool GUARD>
+MPK_DEV void fold_rev_m3s(const uint32_t (&v)[32], const ChunkCn<G, GUARD>& q, float m2,
+                          float (&cv)[NCH], float (&cs)[NCH]) {
+    static_assert(G % 2 == 0 && G <= 4, "group pairs");
+#pragma unroll
+    for (int gp = G / 2 - 1; gp >= 0; --gp) {
+        float x[2][NCH];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int g = 2 * gp + 1 - h;
+#pragma unroll
+            for (int qq = 0; qq < 2; ++qq) {
+                const int col = 8 * g + 4 * qq;
+                const float4 cc = q.cc[col / 4];
+                float sc[4] = {-2.0f, -2.0f, -2.0f, -2.0f};
+                if (GUARD) {
+                    const float4 ss = q.ss[col / 4];
+                    sc[0] = m2 * ss.x; sc[1] = m2 * ss.y; sc[2] = m2 * ss.z; sc[3] = m2 * ss.w;
+                }
+                x[h][4 * qq + 0] = fmaf(__uint_as_float(v[col + 0]), sc[0], cc.x);
+                x[h][4 * qq + 1] = fmaf(__uint_as_float(v[col + 1]), sc[1], cc.y);
+                x[h][4 * qq + 2] = fmaf(__uint_as_float(v[col + 2]), sc[2], cc.z);
+                x[h][4 * qq + 3] = fmaf(__uint_as_float(v[col + 3]), sc[3], cc.w);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) chain_pair(x[0][c], x[1][c], cv[c], cs[c]);
+    }
+}
+
 // Merge the chains of one point given each chain's column jj[c]: smallest value, then smallest
 // column (the sequential scan's result). Returns the winning chain in *w (for TOP2).
 MPK_DEV void merge_chains(const float (&cv)[NCH], const int (&jj)[NCH], float& b1, int& j1,
