@@ -113,8 +113,8 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                    const __grid_constant__ CUtensorMap tmap_c, PairParams p) {
     constexpr bool FINAL = MODE == PAIR_FINAL;
     constexpr bool CAND = MODE == PAIR_CAND;
-    // ASSIGN: reverse column scan with 3-input minima (tc_common.cuh fold_rev_m3)
-    constexpr bool REV = MODE == PAIR_ASSIGN;
+    // ASSIGN and FINAL: reverse column scan with 3-input minima (tc_common.cuh fold_rev_*)
+    constexpr bool REV = MODE == PAIR_ASSIGN || MODE == PAIR_FINAL;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* b_base = smem;                                             // resident centroid halves
@@ -143,7 +143,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
     // and warp 2 (idle once C~ is resident) turns the completed barrier into the one remote
     // "accumulator empty" arrival of its CTA. The MMA for tile t+2 then starts a quarter of a
     // fold earlier than with the arrival after the fold.
-    const bool fwd = REV && MPK_PAIR_FWD && p.NB == 256 && p.nacc == 2 && (P_EWG == 2 || P_EWG == 4) &&
+    const bool fwd = MODE == PAIR_ASSIGN && MPK_PAIR_FWD && p.NB == 256 && p.nacc == 2 && (P_EWG == 2 || P_EWG == 4) &&
                      !p.is_f8 &&
                      MPK_PAIR_ACC_DBUF && !p.guard;
 
@@ -447,6 +447,23 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                         // chunk's ||c||^2 is loaded before its TMEM load (latencies overlap)
                         auto rev_tile = [&](auto guard_tag) {
                             constexpr bool GD = decltype(guard_tag)::value;
+                            if (FINAL) {      // top-2 chains (the certified filter's gap)
+                                if (c < wcols) {
+                                    ChunkCn<2, GD> q;
+                                    load_chunk_cn<2, GD>(cn_s, sc_s, jbase + c, q);
+                                    tmem_ld16(col0 + c, va);
+                                    tmem_wait_ld_dep(va);
+                                    fold_rev_t2<2, GD>(va, q, m2, cv, c2, cs);
+                                }
+                                for (int i = nch - 1; i >= 0; --i) {
+                                    ChunkCn<4, GD> q;
+                                    load_chunk_cn<4, GD>(cn_s, sc_s, jbase + i * 32, q);
+                                    tmem_ld32(col0 + i * 32, va);
+                                    tmem_wait_ld_dep(va);
+                                    fold_rev_t2<4, GD>(va, q, m2, cv, c2, cs);
+                                }
+                                return;
+                            }
                             if (c < wcols) {
                                 ChunkCn<2, GD> q;
                                 load_chunk_cn<2, GD>(cn_s, sc_s, jbase + c, q);
@@ -498,28 +515,6 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                                 }
                                 load_chunk_cn<4, GD>(cn_s, sc_s, jbase, q);
                                 fold_rev_m3<4, GD>(vb, q, m2, cv, s2);
-                                return;
-                            }
-                            if (!GD && nch == 4 && c == wcols) {
-                                // NB = 256: four chunks unrolled, ||c||^2 of the next chunk
-                                // loaded while this one folds (two register sets, no copies)
-                                ChunkCn<4, GD> qa, qb;
-                                load_chunk_cn<4, GD>(cn_s, sc_s, jbase + 96, qa);
-                                tmem_ld32(col0 + 96, va);
-                                load_chunk_cn<4, GD>(cn_s, sc_s, jbase + 64, qb);
-                                tmem_wait_ld_dep(va);
-                                fold_rev_m3<4, GD>(va, qa, m2, cv, s2);
-                                tmem_ld32(col0 + 64, va);
-                                load_chunk_cn<4, GD>(cn_s, sc_s, jbase + 32, qa);
-                                tmem_wait_ld_dep(va);
-                                fold_rev_m3<4, GD>(va, qb, m2, cv, s2);
-                                tmem_ld32(col0 + 32, va);
-                                load_chunk_cn<4, GD>(cn_s, sc_s, jbase, qb);
-                                tmem_wait_ld_dep(va);
-                                fold_rev_m3<4, GD>(va, qa, m2, cv, s2);
-                                tmem_ld32(col0, va);
-                                tmem_wait_ld_dep(va);
-                                fold_rev_m3<4, GD>(va, qb, m2, cv, s2);
                                 return;
                             }
                             for (int i = nch - 1; i >= 0; --i) {
@@ -606,6 +601,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                     if (cv[c] < b1 || (cv[c] == b1 && kc < k1)) { b1 = cv[c]; k1 = kc; }
                 }
                 const int key = (int)k1, v = key >> 3, t = v >> gsh;
+                w = key & 7;                              // the winning chain (FINAL's b2)
                 j1 = 8 * (t * (NB >> 3) + (col_off >> 3) + (v - t * gpt)) + (key & 7);
                 // no value below +inf: the forward scan's default column 0
                 if (!(b1 < INFINITY)) j1 = 0;

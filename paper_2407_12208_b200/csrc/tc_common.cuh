@@ -422,6 +422,54 @@ MPK_DEV void fold_rev_m3s(const uint32_t (&v)[32], const ChunkCn<G, GUARD>& q, f
     }
 }
 
+// Reverse-scan chain step that also keeps the chain's second smallest value v2 (FINAL mode's
+// certified filter): with m = min(xa, xb) (NaN ignored) and M = max.NaN(xa, xb) (NaN kept, so a
+// NaN column contributes nothing),
+//   v2' = min(v2, max(v, m), M)     (the second smallest of {v <= v2, xa, xb})
+//   v'  = min(v, m);  n_a = [xa > v];  n_b = [xb > v'];  s = (s n_a - 1) n_b - 1
+// 7 ALU ops per two columns instead of 4 per column (chain_step2).
+MPK_DEV void chain_pair_t2(float xa, float xb, float& v, float& v2, float& s) {
+    float m, M, t, w, na, nb;
+    asm("min.f32 %0, %1, %2;" : "=f"(m) : "f"(xa), "f"(xb));
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(M) : "f"(xa), "f"(xb));
+    asm("max.f32 %0, %1, %2;" : "=f"(t) : "f"(v), "f"(m));
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(v2) : "f"(v2), "f"(t), "f"(M));
+    asm("min.f32 %0, %1, %2;" : "=f"(w) : "f"(v), "f"(m));
+    asm("set.gtu.f32.f32 %0, %1, %2;" : "=f"(na) : "f"(xa), "f"(v));
+    asm("set.gtu.f32.f32 %0, %1, %2;" : "=f"(nb) : "f"(xb), "f"(w));
+    v = w;
+    s = fmaf(fmaf(s, na, -1.0f), nb, -1.0f);
+}
+template <int G, bool GUARD>
+MPK_DEV void fold_rev_t2(const uint32_t (&v)[32], const ChunkCn<G, GUARD>& q, float m2,
+                         float (&cv)[NCH], float (&c2)[NCH], float (&cs)[NCH]) {
+    static_assert(G % 2 == 0 && G <= 4, "group pairs");
+#pragma unroll
+    for (int gp = G / 2 - 1; gp >= 0; --gp) {
+        float x[2][NCH];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int g = 2 * gp + 1 - h;
+#pragma unroll
+            for (int qq = 0; qq < 2; ++qq) {
+                const int col = 8 * g + 4 * qq;
+                const float4 cc = q.cc[col / 4];
+                float sc[4] = {-2.0f, -2.0f, -2.0f, -2.0f};
+                if (GUARD) {
+                    const float4 ss = q.ss[col / 4];
+                    sc[0] = m2 * ss.x; sc[1] = m2 * ss.y; sc[2] = m2 * ss.z; sc[3] = m2 * ss.w;
+                }
+                x[h][4 * qq + 0] = fmaf(__uint_as_float(v[col + 0]), sc[0], cc.x);
+                x[h][4 * qq + 1] = fmaf(__uint_as_float(v[col + 1]), sc[1], cc.y);
+                x[h][4 * qq + 2] = fmaf(__uint_as_float(v[col + 2]), sc[2], cc.z);
+                x[h][4 * qq + 3] = fmaf(__uint_as_float(v[col + 3]), sc[3], cc.w);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) chain_pair_t2(x[0][c], x[1][c], cv[c], c2[c], cs[c]);
+    }
+}
+
 // Merge the chains of one point given each chain's column jj[c]: smallest value, then smallest
 // column (the sequential scan's result). Returns the winning chain in *w (for TOP2).
 MPK_DEV void merge_chains(const float (&cv)[NCH], const int (&jj)[NCH], float& b1, int& j1,
