@@ -67,6 +67,11 @@ cudaError_t launch_norm_stats(int work, int norm, const void* X, int64_t n, int 
                               cudaStream_t s);
 cudaError_t launch_norm_ssq(int work, const void* X, int64_t n, int d, double* partials,
                             int nblocks, const double* mean, double* ssq, cudaStream_t s);
+// One-pass z-score (fp32, d % 4 == 0, one rank): moments about row 0, then shift and scale.
+bool norm_moments_ok(int work, const void* X, int d);
+cudaError_t launch_norm_moments(const void* X, int64_t n, int d, double* part1, double* part2,
+                                int nblocks, double* kbuf, double* shift, double* scale,
+                                double n_total, cudaStream_t s);
 cudaError_t launch_norm_post(int mode, int d, double n_total, double* shift, double* scale,
                              cudaStream_t s);
 cudaError_t launch_norm_apply(int work, void* X, int64_t rows, int d, const double* shift,

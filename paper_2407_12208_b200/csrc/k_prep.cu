@@ -195,6 +195,111 @@ norm_col_stats_vec_kernel(int mode, const float* __restrict__ X, int64_t n, int 
     }
 }
 
+// One-pass z-score moments (fp32 rows, d % 4 == 0, one rank): per column the compensated sums
+// S1 = sum (x - K) and S2 = sum (x - K)^2 about K = the column's value in row 0, so that
+// mu = K + S1 / n and sigma^2 = S2 / n - (S1 / n)^2 come from ONE read of X. Shifting by a data
+// value keeps the cancellation in sigma^2 at u64 (1 + ((mu - K) / sigma)^2) relative (DESIGN.md
+// R4); block 0 also stores K. Partials: S1 in part1, S2 in part2 (same layout as the scalar
+// kernel's).
+__global__ void __launch_bounds__(kStatThreads)
+norm_moments_vec_kernel(const float* __restrict__ X, int64_t n, int d, double* __restrict__ part1,
+                        double* __restrict__ part2, double* __restrict__ kbuf) {
+    const int tid = threadIdx.x;
+    const int cg = d >> 2;
+    const int lanes = kStatThreads / cg;
+    const int g = tid % cg, lane = tid / cg;
+    const bool active = lane < lanes;
+    const int64_t rows_per_block = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
+    const int64_t r1 = min(n, r0 + rows_per_block);
+    __shared__ double sh[4][kStatThreads * 4];
+    double s1[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0}, s2[4] = {0, 0, 0, 0}, c2[4] = {0, 0, 0, 0};
+    double K[4] = {0, 0, 0, 0};
+    if (active) {
+        const float4 k4 = __ldg(reinterpret_cast<const float4*>(X) + g);
+        K[0] = k4.x; K[1] = k4.y; K[2] = k4.z; K[3] = k4.w;
+        if (blockIdx.x == 0 && lane == 0)
+            for (int e = 0; e < 4; ++e) kbuf[4 * g + e] = K[e];
+        const float4* X4 = reinterpret_cast<const float4*>(X) + g;
+        const int64_t step = (int64_t)lanes;
+        float4 nxt[kVecBatch];
+        int64_t i0 = r0 + lane;
+#pragma unroll
+        for (int u = 0; u < kVecBatch; ++u) {
+            const int64_t i = i0 + u * step;
+            nxt[u] = i < r1 ? __ldg(X4 + i * cg) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        for (; i0 < r1; i0 += step * kVecBatch) {
+            float4 cur[kVecBatch];
+#pragma unroll
+            for (int u = 0; u < kVecBatch; ++u) cur[u] = nxt[u];
+            const int64_t j0 = i0 + step * kVecBatch;
+#pragma unroll
+            for (int u = 0; u < kVecBatch; ++u) {
+                const int64_t i = j0 + u * step;
+                nxt[u] = i < r1 ? __ldg(X4 + i * cg) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < kVecBatch; ++u) {
+                if (i0 + u * step >= r1) break;
+                const float xv[4] = {cur[u].x, cur[u].y, cur[u].z, cur[u].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const double z = (double)xv[e] - K[e];
+                    double t = s1[e] + z;
+                    c1[e] += (fabs(s1[e]) >= fabs(z)) ? ((s1[e] - t) + z) : ((z - t) + s1[e]);
+                    s1[e] = t;
+                    const double z2 = z * z;
+                    t = s2[e] + z2;
+                    c2[e] += (s2[e] >= z2) ? ((s2[e] - t) + z2) : ((z2 - t) + s2[e]);
+                    s2[e] = t;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        sh[0][tid * 4 + e] = s1[e];
+        sh[1][tid * 4 + e] = c1[e];
+        sh[2][tid * 4 + e] = s2[e];
+        sh[3][tid * 4 + e] = c2[e];
+    }
+    __syncthreads();
+    if (active && lane == 0) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            double S = s1[e], C = c1[e], T = s2[e], D = c2[e];
+            for (int l = 1; l < lanes; ++l) {
+                const int ix = (l * cg + g) * 4 + e;
+                double a = sh[0][ix], t = S + a;
+                C += ((fabs(S) >= fabs(a)) ? ((S - t) + a) : ((a - t) + S)) + sh[1][ix];
+                S = t;
+                a = sh[2][ix];
+                t = T + a;
+                D += ((T >= a) ? ((T - t) + a) : ((a - t) + T)) + sh[3][ix];
+                T = t;
+            }
+            const int c = 4 * g + e;
+            part1[((int64_t)blockIdx.x * d + c) * 2 + 0] = S;
+            part1[((int64_t)blockIdx.x * d + c) * 2 + 1] = C;
+            part2[((int64_t)blockIdx.x * d + c) * 2 + 0] = T;
+            part2[((int64_t)blockIdx.x * d + c) * 2 + 1] = D;
+        }
+    }
+}
+// shift = K + S1 / n, scale = sqrt(max(S2 / n - (S1 / n)^2, 0)) (0 -> 1); on entry shift = S1,
+// scale = S2 (combined over the blocks)
+__global__ void norm_post_moments_kernel(int d, double n_total, const double* __restrict__ kbuf,
+                                         double* shift, double* scale) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= d) return;
+    const double m1 = shift[c] / n_total;
+    const double var = fmax(scale[c] / n_total - m1 * m1, 0.0);
+    const double sigma = sqrt(var);
+    shift[c] = kbuf[c] + m1;
+    scale[c] = (sigma == 0.0) ? 1.0 : sigma;
+}
+
 // Combine the per-block partials of one column in block order.
 // mode 0: compensated sum (-> a), mode 2: min (-> a) and max (-> b).
 __global__ void norm_combine_kernel(int mode, const double* __restrict__ partials, int nblocks,
@@ -456,6 +561,21 @@ cudaError_t launch_norm_stats(int work, int norm, const void* X, int64_t n, int 
         norm_col_stats_kernel<float><<<nblocks, kStatThreads, 0, s>>>(mode, (const float*)X, n,
                                                                       d, nullptr, partials);
     norm_combine_kernel<<<(d + 127) / 128, 128, 0, s>>>(mode, partials, nblocks, d, a, b);
+    return cudaGetLastError();
+}
+
+bool norm_moments_ok(int work, const void* X, int d) {
+    return work == KMEANS_FP32 && stats_vec_ok(X, d);
+}
+cudaError_t launch_norm_moments(const void* X, int64_t n, int d, double* part1, double* part2,
+                                int nblocks, double* kbuf, double* shift, double* scale,
+                                double n_total, cudaStream_t s) {
+    launches_add(4);
+    norm_moments_vec_kernel<<<nblocks, kStatThreads, 0, s>>>((const float*)X, n, d, part1, part2,
+                                                             kbuf);
+    norm_combine_kernel<<<(d + 127) / 128, 128, 0, s>>>(0, part1, nblocks, d, shift, nullptr);
+    norm_combine_kernel<<<(d + 127) / 128, 128, 0, s>>>(0, part2, nblocks, d, scale, nullptr);
+    norm_post_moments_kernel<<<(d + 127) / 128, 128, 0, s>>>(d, n_total, kbuf, shift, scale);
     return cudaGetLastError();
 }
 

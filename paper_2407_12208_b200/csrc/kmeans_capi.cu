@@ -307,7 +307,8 @@ int create_impl(int64_t n, int32_t d, int32_t k, int work, int dist, int flags,
     CA(dalloc(&h->shift, (size_t)d * sizeof(double)));
     CA(dalloc(&h->scale, (size_t)d * sizeof(double)));
     h->npartials = norm_stats_blocks(n, d);
-    CA(dalloc(&h->partials, (size_t)h->npartials * d * 2 * sizeof(double)));
+    // two partial sets (the one-pass z-score moments) + K per column
+    CA(dalloc(&h->partials, ((size_t)h->npartials * d * 4 + d) * sizeof(double)));
     CA(dalloc(&h->census, 4 * sizeof(unsigned long long)));
     CA(dalloc(&h->sse_dev, 4 * sizeof(double)));
     CA(dalloc(&h->fbc, 4 * sizeof(int)));
@@ -360,6 +361,15 @@ int normalise_stats(kmeans_ctx* h, const void* Xsrc, int64_t rows) {
         CKN(ncclAllReduce(tmp, tmp, 1, ncclDouble, ncclSum, h->comm, s));
         CK(cudaMemcpyAsync(&n_total, tmp, sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
+    }
+    if (h->norm == KMEANS_NORM_ZSCORE && !h->comm && !getenv("MPK_TWO_PASS_ZSCORE") &&
+        norm_moments_ok(h->work, Xsrc, h->d)) {
+        // one read of X: moments about row 0 (R4)
+        double* part2 = h->partials + (size_t)h->npartials * h->d * 2;
+        double* kbuf = part2 + (size_t)h->npartials * h->d * 2;
+        CK(launch_norm_moments(Xsrc, rows, h->d, h->partials, part2, nb, kbuf, h->shift,
+                               h->scale, n_total, s));
+        return 0;
     }
     CK(launch_norm_stats(h->work, h->norm, Xsrc, rows, h->d, h->partials, nb, h->shift,
                          h->scale, s));

@@ -412,3 +412,41 @@ def test_fx_centres_are_the_rounded_exact_means():
     ulps = np.abs(C.view(np.int32).astype(np.int64) - want.view(np.int32).astype(np.int64))
     assert ulps.max() <= 1
     assert np.mean(ulps == 0) >= 0.999
+
+
+def test_one_pass_zscore_matches_two_pass_and_oracle():
+    """R4: the one-pass z-score moments (about row 0) give eq:z-norm's mu and sigma (PAPER.md:
+    119-126) like the two-pass statistics and the oracle's — the same fp32 transform (the
+    handle reports it in the working type) — even with means 1000 sigma away from 0 (the shift
+    by a data value removes that cancellation)."""
+    rng = np.random.default_rng(3)
+    n, d = 50000, 64
+    X = (rng.standard_normal((n, d)) * rng.uniform(0.5, 3.0, d) + 1000.0 * rng.uniform(-1, 1, d))
+    X = X.astype(np.float32)
+    C0 = synth.init_rows(X, 16, 1)
+    out = {}
+    for name, env in (("one", {}), ("two", {"MPK_TWO_PASS_ZSCORE": "1"})):
+        import os
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        try:
+            km = mpk.KMeans(n, d, 16, "fp32", "fp16", norm="zscore")
+            km.fit(dev(X), dev(C0), max_iter=1, tol=-1.0)
+            sh, sc = np.empty(d, np.float32), np.empty(d, np.float32)   # working type
+            mpk.kmeans_get_transform(km.h, sh, sc)
+            km.close()
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        out[name] = (sh, sc)
+    ref = oracle.fit(X, C0, work="fp32", dist="fp16", norm="zscore", max_iter=1, tol=-1.0)
+    def ulps(a, b):
+        return np.abs(a.view(np.int32).astype(np.int64) - b.view(np.int32).astype(np.int64))
+    want_sh = np.asarray(ref["shift"], np.float64).astype(np.float32)
+    want_sc = np.asarray(ref["scale"], np.float64).astype(np.float32)
+    for sh, sc in out.values():      # the fp64 statistics agree far below fp32's rounding
+        assert ulps(sh, want_sh).max() <= 1 and ulps(sc, want_sc).max() <= 1
+        assert np.mean(ulps(sh, want_sh) == 0) >= 0.95 and np.mean(ulps(sc, want_sc) == 0) >= 0.95
