@@ -884,7 +884,7 @@ cudaError_t launch_finalize(int work, int64_t k, int d, const double* acc, AccLa
 // have_amax skips the pass over X here)
 cudaError_t launch_fx_prepare(const float* Xw, int64_t n, int d, FxState& fx, bool have_amax,
                               cudaStream_t s) {
-    launches_add(2);
+    launches_add(have_amax ? 1 : 2);
     if (have_amax) {
     } else if (d % 4 == 0 && d <= 1024 && ((uintptr_t)Xw & 15) == 0) {
         fx_colmax_vec_kernel<<<kNumSMs * 8, 256, 0, s>>>(Xw, n, d, fx.amax, fx.gate);
@@ -900,7 +900,7 @@ cudaError_t launch_fx_prepare(const float* Xw, int64_t n, int d, FxState& fx, bo
 cudaError_t launch_update_fx(const float* Xw, int64_t n, int d, int k, const int32_t* labels,
                              int* cnt, int* offs, int* cursor, int* perm, const UpdateScratch& us,
                              FxState& fx, cudaStream_t s) {
-    launches_add(9);
+    launches_add(8);     // diff, 6 gated full-path kernels, incremental
     // gate[0] = changed rows (reset), gate[1] = capacity (kept)
     cudaError_t e = cudaMemsetAsync(fx.gate, 0, sizeof(int), s);
     if (e != cudaSuccess) return e;
