@@ -191,17 +191,21 @@ struct FxState {
     long long* part = nullptr;  // piece totals of multi-piece clusters (hi d, lo d per slot)
     int32_t* prev = nullptr;    // n: labels of the previous iteration
     int3* list = nullptr;       // changed rows (row, old, new), capacity gate[1]
+    long long* gShi = nullptr;  // several ranks: the allreduced totals and counts
+    long long* gSlo = nullptr;
+    int* gcnt = nullptr;
     int* gate = nullptr;        // [0] changed rows, [1] capacity, [2] non-finite X flag
     int cap = 0;
 };
-cudaError_t launch_fx_prepare(const float* Xw, int64_t n, int d, FxState& fx, bool have_amax,
-                              cudaStream_t s);
+cudaError_t launch_fx_colmax(const float* Xw, int64_t n, int d, FxState& fx, bool have_amax,
+                             cudaStream_t s);
+cudaError_t launch_fx_scale(int d, FxState& fx, cudaStream_t s);
 cudaError_t launch_update_fx(const float* Xw, int64_t n, int d, int k, const int32_t* labels,
                              int* cnt, int* offs, int* cursor, int* perm, const UpdateScratch& us,
                              FxState& fx, cudaStream_t s);
-cudaError_t launch_finalize_fx(int64_t k, int d, const FxState& fx, const int* cnt,
-                               const double* acc, AccLayout L, float* Cw, IterRec* rec,
-                               cudaStream_t s);
+cudaError_t launch_finalize_fx(int64_t k, int d, const FxState& fx, const long long* Shi,
+                               const long long* Slo, const int* cnt, const double* acc,
+                               AccLayout L, float* Cw, IterRec* rec, cudaStream_t s);
 size_t fx_part_bytes(int64_t n, int d);
 
 // K8: finalize: C = round_u(sum / count) (empty -> keep), shift^2, empty count, trace record.

@@ -882,17 +882,23 @@ cudaError_t launch_finalize(int work, int64_t k, int d, const double* acc, AccLa
 // ---- FX public entry points (internal.h) ---------------------------------------------------
 // amax and gate are zeroed by the caller before the point prep (which may fill amax itself:
 // have_amax skips the pass over X here)
-cudaError_t launch_fx_prepare(const float* Xw, int64_t n, int d, FxState& fx, bool have_amax,
-                              cudaStream_t s) {
-    launches_add(have_amax ? 1 : 2);
-    if (have_amax) {
-    } else if (d % 4 == 0 && d <= 1024 && ((uintptr_t)Xw & 15) == 0) {
+cudaError_t launch_fx_colmax(const float* Xw, int64_t n, int d, FxState& fx, bool have_amax,
+                             cudaStream_t s) {
+    if (have_amax) return cudaSuccess;
+    launches_add(1);
+    if (d % 4 == 0 && d <= 1024 && ((uintptr_t)Xw & 15) == 0) {
         fx_colmax_vec_kernel<<<kNumSMs * 8, 256, 0, s>>>(Xw, n, d, fx.amax, fx.gate);
     } else {
         int g = (int)std::min<int64_t>((n + 7) / 8, kNumSMs * 8);
         if (g < 1) g = 1;
         fx_colmax_kernel<<<g, 256, sizeof(unsigned) * d, s>>>(Xw, n, d, fx.amax, fx.gate);
     }
+    return cudaGetLastError();
+}
+// (several ranks: amax and gate[2] are max-allreduced between the two calls, so every rank
+// uses the same grid)
+cudaError_t launch_fx_scale(int d, FxState& fx, cudaStream_t s) {
+    launches_add(1);
     fx_scale_kernel<<<(d + 127) / 128, 128, 0, s>>>(fx.amax, d, fx.sc, fx.isc, fx.gate);
     return cudaGetLastError();
 }
@@ -938,13 +944,13 @@ cudaError_t launch_update_fx(const float* Xw, int64_t n, int d, int k, const int
     return cudaGetLastError();
 }
 
-cudaError_t launch_finalize_fx(int64_t k, int d, const FxState& fx, const int* cnt,
-                               const double* acc, AccLayout L, float* Cw, IterRec* rec,
-                               cudaStream_t s) {
+cudaError_t launch_finalize_fx(int64_t k, int d, const FxState& fx, const long long* Shi,
+                               const long long* Slo, const int* cnt, const double* acc,
+                               AccLayout L, float* Cw, IterRec* rec, cudaStream_t s) {
     launches_add(1);
     int g = (int)std::min<int64_t>((k + 7) / 8, kNumSMs * 2);
     if (g < 1) g = 1;
-    finalize_fx_kernel<<<g, 256, 0, s>>>(k, d, fx.Shi, fx.Slo, cnt, fx.isc, acc, L, Cw, rec);
+    finalize_fx_kernel<<<g, 256, 0, s>>>(k, d, Shi, Slo, cnt, fx.isc, acc, L, Cw, rec);
     return cudaGetLastError();
 }
 

@@ -177,7 +177,8 @@ void free_all(kmeans_ctx* h) {
                     h->sc, h->labels, h->acc, h->cnt, h->offs, h->cursor, h->perm, h->trace,
                     h->shift, h->scale, h->partials, h->census, h->sse_dev, h->us.cb,
                     h->us.part, h->us.mpo, h->fx.amax, h->fx.sc, h->fx.isc, h->fx.Shi,
-                    h->fx.Slo, h->fx.part, h->fx.prev, h->fx.list, h->fx.gate};
+                    h->fx.Slo, h->fx.part, h->fx.prev, h->fx.list, h->fx.gate, h->fx.gShi,
+                    h->fx.gSlo, h->fx.gcnt};
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
@@ -286,8 +287,8 @@ int create_impl(int64_t n, int32_t d, int32_t k, int work, int dist, int flags,
         CA(dalloc(&h->us.part, b_part));
         CA(dalloc(&h->us.mpo, b_pid));
     }
-    h->fx_ok = work == KMEANS_FP32 && nranks == 1 && k <= 12288 && d <= 8192 &&
-               h->dist_kernel != DK_SMALLD && !getenv("MPK_NO_FX");
+    h->fx_ok = work == KMEANS_FP32 && k <= 12288 && d <= 8192 && h->dist_kernel != DK_SMALLD &&
+               !getenv("MPK_NO_FX");
     if (h->fx_ok) {
         // list capacity n/16 rows: beyond it the full re-summation is the cheaper path.
         // MPK_FX_CAP overrides (tests: 0 = always the full path, n = always incremental)
@@ -302,6 +303,11 @@ int create_impl(int64_t n, int32_t d, int32_t k, int work, int dist, int flags,
         CA(dalloc(&h->fx.prev, (size_t)n * sizeof(int32_t)));
         CA(dalloc(&h->fx.list, (size_t)h->fx.cap * sizeof(int3)));
         CA(dalloc(&h->fx.gate, 4 * sizeof(int)));
+        if (nccl_id) {          // sharded: each rank keeps its shard's totals; A6 sums them
+            CA(dalloc(&h->fx.gShi, (size_t)k * d * sizeof(long long)));
+            CA(dalloc(&h->fx.gSlo, (size_t)k * d * sizeof(long long)));
+            CA(dalloc(&h->fx.gcnt, (size_t)k * sizeof(int)));
+        }
     }
     CA(dalloc(&h->trace, (size_t)KMEANS_MAX_TRACE * sizeof(IterRec)));
     CA(dalloc(&h->shift, (size_t)d * sizeof(double)));
@@ -633,7 +639,14 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
         // FX state for this fit: per-feature grids from max |x|, zero totals and counts, previous
         // labels -1 (every row is "changed" in iteration 1). One host read: a non-finite X
         // disables FX for the fit (the grid needs finite values).
-        CK(launch_fx_prepare((const float*)h->Xw, n, d, h->fx, h->fx_amax_done, s));
+        CK(launch_fx_colmax((const float*)h->Xw, n, d, h->fx, h->fx_amax_done, s));
+        if (h->comm) {          // one grid for all ranks; any rank's non-finite X disables FX
+            ncclGroupStart();
+            CKN(ncclAllReduce(h->fx.amax, h->fx.amax, d, ncclUint32, ncclMax, h->comm, s));
+            CKN(ncclAllReduce(h->fx.gate + 2, h->fx.gate + 2, 1, ncclInt32, ncclMax, h->comm, s));
+            ncclGroupEnd();
+        }
+        CK(launch_fx_scale(d, h->fx, s));
         CK(cudaMemsetAsync(h->fx.Shi, 0, (size_t)k * d * sizeof(long long), s));
         CK(cudaMemsetAsync(h->fx.Slo, 0, (size_t)k * d * sizeof(long long), s));
         CK(cudaMemsetAsync(h->cnt, 0, (size_t)k * sizeof(int), s));
@@ -678,11 +691,25 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
                                  h->perm, h->acc, h->L, h->us, s));          // A5
             if (timing) CK(cudaEventRecord(t2, s));
         }
-        if (h->comm)                                                         // A6
+        if (h->comm && fx_on)        // A6: the FX totals are reduced below; here SSE_t, changed
+            CKN(ncclAllReduce(h->acc + h->L.sse(), h->acc + h->L.sse(), h->L.total() - h->L.sse(),
+                              ncclDouble, ncclSum, h->comm, s));
+        else if (h->comm)                                                    // A6
             CKN(ncclAllReduce(h->acc, h->acc, h->L.total(), ncclDouble, ncclSum, h->comm, s));
         if (timing) CK(cudaEventRecord(t3, s));
-        if (fx_on)
-            CK(launch_finalize_fx(k, d, h->fx, h->cnt, h->acc, h->L, (float*)h->Cw, rec, s));
+        if (fx_on && h->comm) {
+            // A6 for the exact totals: integer sums, so the allreduce is exact and every rank
+            // finalises the same centres
+            ncclGroupStart();
+            CKN(ncclAllReduce(h->fx.Shi, h->fx.gShi, (size_t)k * d, ncclInt64, ncclSum, h->comm, s));
+            CKN(ncclAllReduce(h->fx.Slo, h->fx.gSlo, (size_t)k * d, ncclInt64, ncclSum, h->comm, s));
+            CKN(ncclAllReduce(h->cnt, h->fx.gcnt, k, ncclInt32, ncclSum, h->comm, s));
+            ncclGroupEnd();
+            CK(launch_finalize_fx(k, d, h->fx, h->fx.gShi, h->fx.gSlo, h->fx.gcnt, h->acc, h->L,
+                                  (float*)h->Cw, rec, s));
+        } else if (fx_on)
+            CK(launch_finalize_fx(k, d, h->fx, h->fx.Shi, h->fx.Slo, h->cnt, h->acc, h->L,
+                                  (float*)h->Cw, rec, s));
         else
             CK(launch_finalize(h->work, k, d, h->acc, h->L, h->Cw, rec, s));    // A7
         if (timing) { CK(cudaEventRecord(t4, s)); kev.insert(kev.end(), {t0, t1, t2, t3, t4}); }
