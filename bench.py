@@ -317,6 +317,12 @@ def main():
             "algorithmic_per_launch": f"2*n*k*d = {flops:.4e} flop",
             "avg_launch_ms": t_launch_ms,
             "share_of_step": (t_dist / ms) if ms > 0 else None}
+    if kern == "tcgen05" and achieved:
+        # second denominator: the sustained (power-capped, seconds-long) GEMM peak
+        sus = peaks.get("bf16_tflops_sustained")
+        if sus:
+            roof["peak_sustained"] = sus * (2.0 if dist == "e5m2" else 1.0)
+            roof["frac_sustained"] = achieved / roof["peak_sustained"]
 
     # ---- end-to-end through the C ABI with host buffers -----------------------------------
     e2e = None
