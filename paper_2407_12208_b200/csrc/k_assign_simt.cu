@@ -928,10 +928,17 @@ final_sse_vec_kernel(const float* __restrict__ X, int64_t n, int d, const float*
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     constexpr int RW = 8 / V;
     double acc = 0.0;
+    // the labels of the next row group are fetched one group ahead (the centre loads depend on
+    // them); lane r < RW holds label r of a group, broadcast by shuffles
+    int nlab = (warp * RW + lane < n && lane < RW) ? __ldg(labels + warp * RW + lane) : 0;
     for (int64_t i0 = warp * RW; i0 < n; i0 += nwarps * RW) {
         int lab[RW];
 #pragma unroll
-        for (int r = 0; r < RW; ++r) lab[r] = (i0 + r < n) ? __ldg(labels + i0 + r) : 0;
+        for (int r = 0; r < RW; ++r) lab[r] = __shfl_sync(0xffffffffu, nlab, r);
+        {
+            const int64_t j = i0 + nwarps * RW + lane;
+            nlab = (lane < RW && j < n) ? __ldg(labels + j) : 0;
+        }
         float4 xv[V][RW], cv[V][RW];
 #pragma unroll
         for (int w = 0; w < V; ++w)

@@ -622,27 +622,53 @@ MPK_DEV void fx_q(float x, float2 c, int& i1, int& i2) {
 // Rows whose label changed since the previous iteration -> list (row, old, new); prev <- labels.
 // gate[0] counts them; when gate[0] > gate[1] (capacity) the list is incomplete and the full
 // re-summation runs instead.
-__global__ void fx_diff_kernel(const int32_t* __restrict__ labels, int32_t* __restrict__ prev,
-                               int64_t n, int3* __restrict__ list, int* __restrict__ gate) {
-    const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(256)
+fx_diff_kernel(const int32_t* __restrict__ labels, int32_t* __restrict__ prev, int64_t n,
+               int3* __restrict__ list, int* __restrict__ gate) {
+    // one list-counter atomic per block and sweep (a single hot counter serialised the warps'
+    // atomics when many rows change); any order of the list is fine (integer updates)
+    constexpr int R = 4;                                  // rows per thread in flight
+    __shared__ int wcount[8], wbase[8], bbase;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int cap = gate[1];
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n;
-         base += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = base + threadIdx.x;
-        int l = 0, o = 0;
-        bool ch = false;
-        if (i < n) {
-            l = labels[i];
-            o = prev[i];
-            ch = l != o;
-            if (ch) prev[i] = l;
+    const int64_t span = (int64_t)blockDim.x * R;
+    for (int64_t base = (int64_t)blockIdx.x * span; base < n; base += (int64_t)gridDim.x * span) {
+        int l[R], o[R];
+        unsigned m[R];
+        int tot = 0;
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            const int64_t i = base + u * blockDim.x + threadIdx.x;
+            l[u] = i < n ? __ldg(labels + i) : 0;
+            o[u] = i < n ? prev[i] : 0;
         }
-        const unsigned m = __ballot_sync(0xffffffffu, ch);
-        if (!m) continue;
-        int slot = 0;
-        if (lane == 0) slot = atomicAdd(&gate[0], __popc(m));
-        slot = __shfl_sync(0xffffffffu, slot, 0) + __popc(m & ((1u << lane) - 1u));
-        if (ch && slot < cap) list[slot] = make_int3((int)i, o, l);
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            const int64_t i = base + u * blockDim.x + threadIdx.x;
+            const bool ch = i < n && l[u] != o[u];
+            m[u] = __ballot_sync(0xffffffffu, ch);
+            tot += __popc(m[u]);
+            if (ch) prev[i] = l[u];
+        }
+        if (lane == 0) wcount[warp] = tot;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int run = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { wbase[w] = run; run += wcount[w]; }
+            bbase = run ? atomicAdd(&gate[0], run) : 0;
+        }
+        __syncthreads();
+        int slot = bbase + wbase[warp];
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            if (m[u] & (1u << lane)) {
+                const int sl = slot + __popc(m[u] & ((1u << lane) - 1u));
+                if (sl < cap)
+                    list[sl] = make_int3((int)(base + u * blockDim.x + threadIdx.x), o[u], l[u]);
+            }
+            slot += __popc(m[u]);
+        }
+        __syncthreads();                                  // wcount / wbase reused next sweep
     }
 }
 // Incremental update from the changed-row list: a warp per row, lanes over columns.
@@ -910,7 +936,7 @@ cudaError_t launch_update_fx(const float* Xw, int64_t n, int d, int k, const int
     // gate[0] = changed rows (reset), gate[1] = capacity (kept)
     cudaError_t e = cudaMemsetAsync(fx.gate, 0, sizeof(int), s);
     if (e != cudaSuccess) return e;
-    int g = (int)std::min<int64_t>((n + 255) / 256, kNumSMs * 8);
+    int g = (int)std::min<int64_t>((n + 1023) / 1024, kNumSMs * 8);
     if (g < 1) g = 1;
     fx_diff_kernel<<<g, 256, 0, s>>>(labels, fx.prev, n, fx.list, fx.gate);
     const int* gate = fx.gate;
