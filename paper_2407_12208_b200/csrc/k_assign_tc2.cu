@@ -13,13 +13,18 @@
 //     ahead of the epilogue; tcgen05.commit multicasts "accumulator full" / "slot free" to both
 //     CTAs;
 //   * two epilogue warpgroups (2 warps per SM sub-partition) split the NB columns of every
-//     accumulator and fold them into per-point argmin chains (chain_step, 2 alu-pipe ops per
-//     distance); per tile they meet at a named barrier and one thread arrives remotely on the
-//     leader's "accumulator empty" barrier;
+//     accumulator and fold them into per-point argmin chains. ASSIGN and FINAL visit the columns
+//     in DECREASING order (tiles, chunks, groups reversed), which turns the first-index tie rule
+//     into a non-strict improvement and lets one chain step take two columns with a 3-input
+//     minimum (tc_common.cuh chain_pair_x2: 1.5 alu ops per distance; chain_pair_t2 for FINAL's
+//     top-2); CAND keeps the forward order. Each warp releases an accumulator with its own
+//     remote arrival on the leader's "accumulator empty" barrier (fp16 ASSIGN: through warp 2,
+//     as soon as its last TMEM load of the tile has landed);
 //   * the row-block end is OFF the epilogue's critical path: each warpgroup only merges its
-//     chains and hands a (value, column) partial per point to warp 3 through double-buffered
-//     shared memory; warp 3 merges the two partials and does the label store, the changed
-//     count and the SSE (or, in FINAL mode, the certification).
+//     chains (exact float keys 8 v + c) and hands a (value, column) partial per point to warp 3
+//     through double-buffered shared memory (released by an mbarrier); warp 3 merges the two
+//     partials and does the label store, the changed count and the SSE (or, in FINAL mode, the
+//     certification).
 // DESIGN.md "pair kernel" has the measured per-tile budget this layout comes from.
 // FINAL mode: certified top-2 filter for Alg 3 step 7, as in k_assign_tc.cu; each uncertified
 // row also gets its candidate threshold T = v^(1) + 2 (E + B32) (rounded up).
@@ -424,7 +429,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 const uint32_t col0 = tmem_base + lane_addr + (uint32_t)buf * NB + col_off;
                 const int jbase = (REV ? NT - 1 - t : t) * NB + col_off;
                 if (!(dbg & 1)) {
-                    // 32-column chunks (double-buffering the TMEM loads measured slower)
+                    // 32-column chunks
                     const int nch = wcols >> 5;
                     const int c = nch << 5;
                     auto fold = [&](const uint32_t (&vr)[32], int cc) {
