@@ -8,7 +8,11 @@
  *           PAPER.md:193-196) whose dot products run in the low precision u_l (fp16, bf16 or
  *           q52 = OCP FP8 E5M2) with fp32 accumulation, fused with the argmin;
  *   step 4  centroid update mu_j = (1/|S_j|) sum_{x in S_j} x (eq:center) in
- *           the working precision u (fp32 or fp64);
+ *           the working precision u (fp32 or fp64). fp32 work: the sums are exact integer totals
+ *           on a per-feature grid (2^-45 of the feature's max |x|), updated from the rows whose
+ *           label changed, so mu_j = round_u(exact mean) up to that grid and depends only on
+ *           S_j (bit-reproducible, also across ranks); fp64 work: fp64 sums in a fixed order
+ *           (R7, R9);
  *   step 6  stop at max_iter or when the cluster sets converge;
  *   step 7  final assignment "computed in precision u".
  * Optional: z-score (eq:z-norm) or min-max (image /255)
