@@ -570,7 +570,9 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 // thread signals the leader's "accumulator empty"
                 tc_fence_before();
                 if (fwd) {
-                    // released through warp 2 before the last chunk's fold
+                    // released through warp 2 before the last chunk's fold (debug mode without
+                    // the fold: here)
+                    if (dbg & 1) named_bar_arrive(BAR_REL + buf, P_EPI * 32 + 32);
                 } else if (MPK_PAIR_WARP_ARRIVE) {
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&t_empty[buf]), 0));
