@@ -58,6 +58,9 @@ constexpr int P_NON_EPI = 4;
 #ifndef MPK_PAIR_FWD
 #define MPK_PAIR_FWD 1                   // ASSIGN NB=256: release accumulators via warp 2 (below)
 #endif
+#ifndef MPK_PAIR_HOT_RING
+#define MPK_PAIR_HOT_RING 1              // X~ ring waits (producer, MMA warp) spin too
+#endif
 #ifndef MPK_PAIR_HOT_WAIT
 #define MPK_PAIR_HOT_WAIT 1              // epilogue: test_wait before a bare try_wait loop
 #endif
@@ -223,7 +226,8 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
         int slot = 0;
         uint32_t ph = 0;
         for (int64_t rb = pair; rb < num_rb; rb += npairs) {
-            mbar_wait(smem_u32(&a_empty[slot]), ph ^ 1);
+            if (MPK_PAIR_HOT_RING) mbar_wait_hot(smem_u32(&a_empty[slot]), ph ^ 1);
+            else mbar_wait(smem_u32(&a_empty[slot]), ph ^ 1);
             if (elect_one()) {
                 const uint32_t fb = smem_u32(&a_full[slot]);
                 if (leader) mbar_expect_tx(fb, 2u * a_tile);
@@ -255,7 +259,8 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             int slot = 0, buf = 0;
             uint32_t aph = 0, tph = 0, ai = 0;
             for (int64_t rb = pair; rb < num_rb; rb += npairs) {
-                mbar_wait(smem_u32(&a_full[slot]), aph);
+                if (MPK_PAIR_HOT_RING) mbar_wait_hot(smem_u32(&a_full[slot]), aph);
+                else mbar_wait(smem_u32(&a_full[slot]), aph);
                 tc_fence_after();
                 const uint32_t a_lo = a_lo0 + slot * a_tile16;
                 for (int t = 0; t < NT; ++t, ++ai) {
