@@ -61,6 +61,9 @@ constexpr int P_NON_EPI = 4;
 #ifndef MPK_PAIR_HOT_RING
 #define MPK_PAIR_HOT_RING 1              // X~ ring waits (producer, MMA warp) spin too
 #endif
+#ifndef MPK_PAIR_HSPLIT
+#define MPK_PAIR_HSPLIT 1                // ASSIGN NB=256: four 128-column accumulators (below)
+#endif
 #ifndef MPK_PAIR_HOT_WAIT
 #define MPK_PAIR_HOT_WAIT 1              // epilogue: test_wait before a bare try_wait loop
 #endif
@@ -151,7 +154,19 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
     // and warp 2 (idle once C~ is resident) turns the completed barrier into the one remote
     // "accumulator empty" arrival of its CTA. The MMA for tile t+2 then starts a quarter of a
     // fold earlier than with the arrival after the fold.
-    const bool fwd = MODE == PAIR_ASSIGN && MPK_PAIR_FWD && p.NB == 256 && p.nacc == 2 && (P_EWG == 2 || P_EWG == 4) &&
+    // Half split (ASSIGN, 256-column tiles): each tile is issued as two N = 128 MMAs into
+    // separate 128-column accumulators — half h takes rows h*64 .. h*64+63 of each CTA's resident
+    // centroid half, i.e. centroids t*256 + {h*64 + [0,64)} u {128 + h*64 + [0,64)} — and
+    // warpgroup h folds half h of every tile. Four accumulators (two per warpgroup) let the MMA
+    // refill one while the warpgroup folds the other, and a warpgroup releases its half on its
+    // own. (The accumulator columns of a half map increasingly onto its centroids, so the reverse
+    // scan and the merge keys carry over.)
+    // Measured: e5m2 2.15 -> 2.05 ms (the fold bounds it; decoupling the warpgroups helps), fp16
+    // 2.42 -> 2.68 ms (twice the MMA instructions, commits and waits per tile where the MMA
+    // pipeline already binds), so fp16 keeps one 256-column MMA per tile.
+    const bool hsplit = MODE == PAIR_ASSIGN && MPK_PAIR_HSPLIT && p.NB == 256 && P_EWG == 2 &&
+                        p.tmem_cols >= 512 && p.is_f8;
+    const bool fwd = !hsplit && MODE == PAIR_ASSIGN && MPK_PAIR_FWD && p.NB == 256 && p.nacc == 2 && (P_EWG == 2 || P_EWG == 4) &&
                      !p.is_f8 &&
                      MPK_PAIR_ACC_DBUF && !p.guard;
 
@@ -164,10 +179,11 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
         mbar_init(smem_u32(b_full), 1);
         mbar_init(smem_u32(&part_free[0]), 1);
         mbar_init(smem_u32(&part_free[1]), 1);
-        for (int i = 0; i < p.nacc; ++i) {
+        for (int i = 0; i < (hsplit ? 4 : p.nacc); ++i) {
             mbar_init(smem_u32(&t_full[i]), 1);
-            // one arrival per CTA (named barrier first), or one per epilogue warp
-            mbar_init(smem_u32(&t_empty[i]), (fwd || !MPK_PAIR_WARP_ARRIVE) ? 2 : 2 * P_EPI);
+            // one arrival per CTA (named barrier first), one per epilogue warp, or (half split)
+            // one per warp of the owning warpgroup
+            mbar_init(smem_u32(&t_empty[i]), hsplit ? 8 : ((fwd || !MPK_PAIR_WARP_ARRIVE) ? 2 : 2 * P_EPI));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x)) : "memory");
@@ -258,7 +274,42 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             tc_fence_after();
             int slot = 0, buf = 0;
             uint32_t aph = 0, tph = 0, ai = 0;
-            for (int64_t rb = pair; rb < num_rb; rb += npairs) {
+            if (hsplit) {
+                const uint32_t idesc128 = (idesc & ~(0x3Fu << 17)) | ((128u >> 3) << 17);
+                const uint32_t h16 = (64u * (uint32_t)p.SWZ) >> 4;   // 64 centroid rows
+                for (int64_t rb = pair; rb < num_rb; rb += npairs) {
+                    mbar_wait_hot(smem_u32(&a_full[slot]), aph);
+                    tc_fence_after();
+                    const uint32_t a_lo = a_lo0 + slot * a_tile16;
+                    for (int t = 0; t < NT; ++t, ++ai) {
+                        const int tb = NT - 1 - t;
+                        for (int h = 0; h < 2; ++h) {
+                            const int hb = (int)(ai & 1u) * 2 + h;
+                            mbar_wait_hot(smem_u32(&t_empty[hb]), ((ai >> 1) & 1u) ^ 1u);
+                            tc_fence_after();
+                            if (elect_one()) {
+                                const uint32_t d_tmem = tmem_base + (uint32_t)hb * 128u;
+                                const uint32_t b_lo = b_lo0 + tb * b_half16 + (uint32_t)h * h16;
+                                if (!(dbg & 2)) {
+                                    for (int kb = 0; kb < KB; ++kb)
+                                        for (int ks = 0; ks < ksteps; ++ks) {
+                                            const uint64_t ad = desc_join(dhi, a_lo + kb * kb_a16 + ks * 2);
+                                            const uint64_t bd = desc_join(dhi, b_lo + kb * kb_b16 + ks * 2);
+                                            const uint32_t accum = (kb | ks) ? 1u : 0u;
+                                            if (f8) mma2_f8(d_tmem, ad, bd, idesc128, accum);
+                                            else mma2_f16(d_tmem, ad, bd, idesc128, accum);
+                                        }
+                                }
+                                tc_commit_pair(smem_u32(&t_full[hb]));
+                                if (t == NT - 1 && h == 1) tc_commit_pair(smem_u32(&a_empty[slot]));
+                            }
+                            __syncwarp();
+                        }
+                    }
+                    if (++slot == SA) { slot = 0; aph ^= 1; }
+                }
+            }
+            for (int64_t rb = pair; rb < num_rb && !hsplit; rb += npairs) {
                 if (MPK_PAIR_HOT_RING) mbar_wait_hot(smem_u32(&a_full[slot]), aph);
                 else mbar_wait(smem_u32(&a_full[slot]), aph);
                 tc_fence_after();
@@ -419,6 +470,71 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             const int64_t row = rb * rows_per_rb + rank * P_BM + q;
             const float m2 = (guard && row < n) ? -2.0f * p.sx[row] : -2.0f;
             const float T = (CAND && row < n) ? p.thr[row] : NAN;          // CAND threshold
+            if (REV && hsplit) {
+                float cv[NCH], c2[NCH], cs[NCH];
+                chains_init(cv, cs, c2);
+                uint64_t s2[NCH / 2];
+#pragma unroll
+                for (int m = 0; m < NCH / 2; ++m) s2[m] = pack2(-1.0f, -1.0f);
+                for (int t = 0; t < NT; ++t, ++ai) {
+                    const int hb = (int)(ai & 1u) * 2 + wg;
+                    mbar_wait_hot(smem_u32(&t_full[hb]), (ai >> 1) & 1u);
+                    tc_fence_after();
+                    const uint32_t col0 = tmem_base + lane_addr + (uint32_t)hb * 128u;
+                    // chunk i of half wg holds centroids jb(i) .. jb(i) + 31
+                    const int tb = NT - 1 - t;
+                    auto jb = [&](int i) { return tb * 256 + (i >= 2 ? 128 : 0) + wg * 64 + (i & 1) * 32; };
+                    auto half = [&](auto guard_tag) {
+                        constexpr bool GD = decltype(guard_tag)::value;
+                        uint32_t va[32], vb[32];
+                        ChunkCn<4, GD> q;
+                        tmem_ld32(col0 + 96, va);
+                        tmem_wait_ld_dep(va);
+                        tmem_ld32(col0 + 64, vb);
+                        load_chunk_cn<4, GD>(cn_s, sc_s, jb(3), q);
+                        fold_rev_m3<4, GD>(va, q, m2, cv, s2);
+                        tmem_wait_ld_dep(vb);
+                        tmem_ld32(col0 + 32, va);
+                        load_chunk_cn<4, GD>(cn_s, sc_s, jb(2), q);
+                        fold_rev_m3<4, GD>(vb, q, m2, cv, s2);
+                        tmem_wait_ld_dep(va);
+                        tmem_ld32(col0, vb);
+                        load_chunk_cn<4, GD>(cn_s, sc_s, jb(1), q);
+                        fold_rev_m3<4, GD>(va, q, m2, cv, s2);
+                        tmem_wait_ld_dep(vb);
+                        load_chunk_cn<4, GD>(cn_s, sc_s, jb(0), q);
+                        fold_rev_m3<4, GD>(vb, q, m2, cv, s2);
+                    };
+                    if (!(dbg & 1)) {
+                        if (guard) half(std::true_type{});
+                        else half(std::false_type{});
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&t_empty[hb]), 0));
+                }
+#pragma unroll
+                for (int m = 0; m < NCH / 2; ++m) unpack2(s2[m], cs[2 * m], cs[2 * m + 1]);
+                float b1 = cv[0], k1 = fmaf(cs[0], -8.0f, -8.0f);
+#pragma unroll
+                for (int c = 1; c < NCH; ++c) {
+                    const float kc = fmaf(cs[c], -8.0f, (float)(c - 8));
+                    if (cv[c] < b1 || (cv[c] == b1 && kc < k1)) { b1 = cv[c]; k1 = kc; }
+                }
+                // key = 8 v + c, v = forward ordinal: tile v >> 4, accumulator column
+                // 8 (v & 15) + c of this half -> centroid
+                const int key = (int)k1, v = key >> 3, tt = v >> 4;
+                const int cc = 8 * (v & 15) + (key & 7);
+                int j1 = tt * 256 + (cc < 64 ? wg * 64 + cc : 128 + wg * 64 + (cc - 64));
+                if (!(b1 < INFINITY)) j1 = 0;          // the forward scan's default column 0
+                const int par = (int)(rbi & 1);
+                if (rbi >= 2) mbar_wait_hot(smem_u32(&part_free[par]), (uint32_t)((rbi >> 1) - 1) & 1u);
+                const int slot = (par * P_EWG + wg) * P_BM + q;
+                part_v[slot] = b1;
+                part_j[slot] = j1;
+                named_bar_arrive(BAR_PART + par, P_EPI * 32 + 32);
+                continue;
+            }
             if (trace_me && ai < TRACE_T) trace[ai * 8 + 5] = clock64();   // row-block top
             float cv[NCH], c2[NCH], cs[NCH];
             chains_init(cv, cs, c2);
