@@ -117,6 +117,12 @@ typedef struct kmeans_stats {
                                             still cannot stall the iteration (+inf: none moved)*/
     int32_t n_update_prec_short;         /* iterations with u_bound_t below the working
                                             precision's unit roundoff (2^-24 / 2^-53)          */
+    int32_t tc_variant;                  /* tcgen05 kernel of the loop: 0 = none (CUDA cores),
+                                            1 = streaming centroid tiles (k_assign_tc.cu),
+                                            2 = CTA pair with resident centroids (k_assign_tc2) */
+    int32_t n_ranks;                     /* ranks of the fit (1, or the NCCL / virtual group)  */
+    double eta;                          /* n_dist_low / n_dist (eq:xi-low-prec-ratio,
+                                            PAPER.md:666-668); 1 without kmeans_set_delta     */
 } kmeans_stats;
 
 /*
@@ -168,11 +174,15 @@ int kmeans_get_centroids(kmeans_handle h, void* C);
  * x_normalised = round_u((x - shift) / scale). Identity (0, 1) without normalisation. */
 int kmeans_get_transform(kmeans_handle h, void* shift, void* scale);
 
-/* kmeans_get_stats — copy the last fit's statistics (see kmeans_stats). */
+/* kmeans_get_stats — copy the last fit's statistics (see kmeans_stats): the per-iteration
+ * traces of Alg 3's loop (SSE_t of eq:sse PAPER.md:130-133, the shift and changed counts of the
+ * stopping rule PAPER.md:549, Thm 5.3's bound PAPER.md:487-493), eta of eq:xi-low-prec-ratio
+ * and timings. EINVAL on a NULL handle or out. */
 int kmeans_get_stats(kmeans_handle h, kmeans_stats* out);
 
 /* kmeans_set_stream — run all of the handle's work on this cudaStream_t (NULL = the handle's
- * own stream). The caller keeps ownership of the stream. */
+ * own stream). The caller keeps ownership of the stream. Plumbing only: no passage of the paper
+ * (which runs on one CPU thread) defines streams. EINVAL on a NULL handle. */
 int kmeans_set_stream(kmeans_handle h, void* cuda_stream);
 
 /* kmeans_seed_d2 — seeding by D^2 weighting (Alg 1) with the distances of
@@ -217,16 +227,41 @@ const char* kmeans_last_error(kmeans_handle h);
 int kmeans_cast(int src_prec, int dst_prec, const void* src, int64_t count, void* dst);
 
 /*
- * kmeans_create_dist — like kmeans_create for one rank of a point-sharded run: this rank holds
- * n_local rows; all ranks hold the same C0. nccl_unique_id points to the 128-byte ncclUniqueId
- * created by rank 0 and broadcast by the caller. Each iteration the packed partial sums,
- * counts, SSE and changed-label count are combined with ONE ncclAllReduce over NVLink, so every
- * rank computes identical centroids. kmeans_fit must be called collectively; X/labels are the
- * local shard; centroids, sse and iters are identical on every rank (sse is global).
+ * kmeans_create_dist — like kmeans_create for one rank of a point-sharded run (the
+ * paper has parallel k-means only as related work): this rank holds n_local
+ * rows; all ranks hold the same C0. nccl_unique_id points to the 128-byte ncclUniqueId created
+ * by rank 0 and broadcast by the caller (nranks = 1 with an id still builds a 1-rank NCCL
+ * communicator, so every collective call site runs). Per Lloyd iteration the ranks combine
+ * their shard's share of eq:center: with fp32 work, the exact fixed-point
+ * totals (two int64 k x d arrays) and the int32 counts in one NCCL group of three allreduces
+ * (integer sums: exact and order-free) plus one fp64 allreduce of [SSE_t, #changed]; with fp64
+ * work, one fp64 allreduce of the packed [sums | counts | SSE_t | #changed]. Every rank then
+ * finalises identical centroids. Once per fit: the normalisation statistics (eq:z-norm,
+ * PAPER.md:119-126) and the fixed-point grid (a max-allreduce); at the end the final SSE.
+ * kmeans_fit must be called collectively; X/labels are the local shard; centroids, sse and iters
+ * are identical on every rank (sse is global). Errors: EINVAL on a NULL id with nranks > 1 or a
+ * bad rank; ENCCL if the communicator cannot be built.
  */
 int kmeans_create_dist(int64_t n_local, int32_t d, int32_t k, int work_prec, int dist_prec,
                        int flags, const void* nccl_unique_id, int nranks, int rank,
                        kmeans_handle* out);
+
+/*
+ * Virtual ranks — the point-sharded path of kmeans_create_dist with g ranks inside ONE process
+ * on ONE GPU (a test / validation transport; SURVEY §4 "fake multi-GPU"). kmeans_vgroup_create
+ * makes a group of nranks (1..64) on the current device; kmeans_create_virtual makes rank
+ * `rank`'s handle for its n_local-row shard (same arguments and semantics as
+ * kmeans_create_dist). Each rank's kmeans_fit must run on its OWN host thread, all ranks
+ * collectively, exactly like one process per GPU: every per-rank step is the NCCL path's code;
+ * at each collective the last rank to arrive sums the ranks' buffers on the device in rank
+ * order. The ranks' kernels are serialised on one stream of the group (they never wait on each
+ * other on the device). kmeans_vgroup_destroy returns EINVAL while handles of the group live.
+ */
+typedef struct kmeans_vgroup_s* kmeans_vgroup;
+int kmeans_vgroup_create(int nranks, kmeans_vgroup* out);
+int kmeans_create_virtual(int64_t n_local, int32_t d, int32_t k, int work_prec, int dist_prec,
+                          int flags, kmeans_vgroup group, int rank, kmeans_handle* out);
+int kmeans_vgroup_destroy(kmeans_vgroup group);
 
 /* kmeans_nccl_unique_id — write a fresh 128-byte ncclUniqueId (call on rank 0 only). */
 int kmeans_nccl_unique_id(void* out128);

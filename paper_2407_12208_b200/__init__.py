@@ -34,7 +34,8 @@ EXPORTS = ["kmeans_create", "kmeans_fit", "kmeans_assign", "kmeans_set_centroids
            "kmeans_set_stream", "kmeans_set_timing", "kmeans_set_delta", "kmeans_seed_d2",
            "kmeans_destroy",
            "kmeans_last_error",
-           "kmeans_cast", "kmeans_create_dist", "kmeans_nccl_unique_id", "kmeans_version"]
+           "kmeans_cast", "kmeans_create_dist", "kmeans_nccl_unique_id", "kmeans_version",
+           "kmeans_vgroup_create", "kmeans_create_virtual", "kmeans_vgroup_destroy"]
 
 
 class kmeans_stats(ct.Structure):
@@ -52,7 +53,8 @@ class kmeans_stats(ct.Structure):
                 ("n_kernel_launches", ct.c_int64), ("n_final_fallback", ct.c_int64),
                 ("n_final_uncertified", ct.c_int64), ("n_dist", ct.c_int64),
                 ("n_dist_low", ct.c_int64), ("u_bound_t", ct.c_double * KMEANS_MAX_TRACE),
-                ("n_update_prec_short", ct.c_int32)]
+                ("n_update_prec_short", ct.c_int32), ("tc_variant", ct.c_int32),
+                ("n_ranks", ct.c_int32), ("eta", ct.c_double)]
 
 
 def _load():
@@ -78,6 +80,9 @@ def _load():
         "kmeans_cast": (i32, [i32, i32, P, i64, P]),
         "kmeans_create_dist": (i32, [i64, i32, i32, i32, i32, i32, P, i32, i32, ct.POINTER(P)]),
         "kmeans_nccl_unique_id": (i32, [P]),
+        "kmeans_vgroup_create": (i32, [i32, ct.POINTER(P)]),
+        "kmeans_create_virtual": (i32, [i64, i32, i32, i32, i32, i32, P, i32, ct.POINTER(P)]),
+        "kmeans_vgroup_destroy": (i32, [P]),
         "kmeans_version": (ct.c_char_p, []),
     }
     for name, (res, args) in sig.items():
@@ -138,6 +143,24 @@ def kmeans_create_dist(n_local, d, k, work_prec, dist_prec, flags, nccl_id: byte
                                    _prec(dist_prec), int(flags), buf, int(nranks), int(rank),
                                    ct.byref(h)), None)
     return h
+
+
+def kmeans_vgroup_create(nranks):
+    g = ct.c_void_p()
+    _check(_lib.kmeans_vgroup_create(int(nranks), ct.byref(g)), None)
+    return g
+
+
+def kmeans_create_virtual(n_local, d, k, work_prec, dist_prec, flags, group, rank):
+    h = ct.c_void_p()
+    _check(_lib.kmeans_create_virtual(int(n_local), int(d), int(k), _prec(work_prec),
+                                      _prec(dist_prec), int(flags), group, int(rank),
+                                      ct.byref(h)), None)
+    return h
+
+
+def kmeans_vgroup_destroy(group):
+    _check(_lib.kmeans_vgroup_destroy(group), None)
 
 
 def kmeans_nccl_unique_id() -> bytes:
@@ -230,8 +253,8 @@ def stats_dict(st: kmeans_stats) -> dict:
                 u_bound_t=list(st.u_bound_t[:t]), n_update_prec_short=st.n_update_prec_short,
                 n_kernel_launches=st.n_kernel_launches, n_final_fallback=st.n_final_fallback,
                 n_final_uncertified=st.n_final_uncertified, n_dist=st.n_dist,
-                n_dist_low=st.n_dist_low,
-                eta=(st.n_dist_low / st.n_dist) if st.n_dist else None)
+                n_dist_low=st.n_dist_low, eta=st.eta, tc_variant=st.tc_variant,
+                n_ranks=st.n_ranks)
 
 
 class KMeans:

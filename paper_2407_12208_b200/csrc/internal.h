@@ -152,6 +152,7 @@ cudaError_t launch_final_tc(TcPlan* plan, const Problem& p, const float* xn, con
 // layout as the plan's rows) with thresholds thr, append every column j with v^_j <= thr[r] to
 // cand[r * cand_q ...] (count in cand_cnt[r], which may exceed cand_q: overflow).
 bool tc_plan_has_cand(const TcPlan* plan);
+int tc_plan_kind(const TcPlan* plan);   // 1 = streaming, 2 = CTA pair
 const void* tc_plan_operands(const TcPlan* plan, int* row_bytes);
 cudaError_t launch_cand_tc(TcPlan* plan, const void* Xc, int64_t nc, int guard, const float* sxc,
                            const float* cn, const float* sc, const float* thr, int* cand_cnt,
@@ -207,6 +208,44 @@ cudaError_t launch_finalize_fx(int64_t k, int d, const FxState& fx, const long l
                                const long long* Slo, const int* cnt, const double* acc,
                                AccLayout L, float* Cw, IterRec* rec, cudaStream_t s);
 size_t fx_part_bytes(int64_t n, int d);
+
+// A6 transport (coll.cu): allreduce over the ranks of a point-sharded fit. NCCL (one process
+// per GPU) or virtual ranks (several handles of one process on one GPU, kmeans_vgroup_*).
+enum CollType { CT_F64 = 0, CT_I64 = 1, CT_I32 = 2, CT_U32 = 3 };
+enum CollOp { CO_SUM = 0, CO_MAX = 1, CO_MIN = 2 };
+struct Coll {
+    int nranks = 1, rank = 0;
+    bool virtual_ranks = false;
+    virtual ~Coll() {}
+    // in-place allowed (send == recv); returns 0 or a KMEANS_E* code with *err set
+    virtual int allreduce(const void* send, void* recv, size_t count, int type, int op,
+                          cudaStream_t s, std::string* err) = 0;
+    virtual void group_start() {}
+    virtual int group_end(std::string*) { return 0; }
+    // the stream every handle of the group must run on (virtual ranks share one), or null
+    virtual cudaStream_t shared_stream() { return nullptr; }
+};
+struct VGroup;
+Coll* coll_create_nccl(const void* nccl_id, int nranks, int rank, std::string* err);
+Coll* coll_create_virtual(VGroup* g, int rank, std::string* err);
+VGroup* vgroup_create(int nranks, std::string* err);
+int vgroup_destroy(VGroup* g);   // KMEANS_EINVAL while handles of the group are alive
+int vgroup_size(const VGroup* g);
+
+// cudaFuncSetAttribute is per device: remember per (call site, device) that it was done.
+struct PerDeviceOnce {
+    unsigned long long mask = 0;   // benign race: a duplicate call is idempotent
+    bool need() {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        return dev >= 64 || !((__atomic_load_n(&mask, __ATOMIC_RELAXED) >> dev) & 1ull);
+    }
+    void done() {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 64) __atomic_fetch_or(&mask, 1ull << dev, __ATOMIC_RELAXED);
+    }
+};
 
 // K8: finalize: C = round_u(sum / count) (empty -> keep), shift^2, empty count, trace record.
 cudaError_t launch_finalize(int work, int64_t k, int d, const double* acc, AccLayout L,

@@ -583,6 +583,7 @@ cudaError_t launch_final_tc(TcPlan* pl, const Problem& pb, const float* xn, cons
 }
 
 bool tc_plan_has_cand(const TcPlan* pl) { return pl && pl->kind == 2; }
+int tc_plan_kind(const TcPlan* pl) { return pl ? pl->kind : 0; }
 const void* tc_plan_operands(const TcPlan* pl, int* row_bytes) {
     *row_bytes = pl->d_pad * pl->esize;
     return pl->Xl;

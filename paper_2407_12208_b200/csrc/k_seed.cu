@@ -178,13 +178,13 @@ cudaError_t seed_rounds(const void* Xl, int64_t n, int d, int d_pad, const void*
     const unsigned pb = (unsigned)((n + 255) / 256);
     seed_init_kernel<<<pb, 256, 0, s>>>(D2, n);
     const size_t sm = ((size_t)d + kSeedBlock) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    if (attr.need()) {
         cudaFuncSetAttribute(seed_update_kernel<LT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              200 * 1024);
         cudaFuncSetAttribute(seed_pick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              180 * 1024);
-        attr = true;
+        attr.done();
     }
     // the pick stages the nb block totals in shared memory when they fit (n <= ~73M rows)
     const int staged = (size_t)nb * sizeof(double) <= 140 * 1024 ? 1 : 0;

@@ -492,11 +492,11 @@ cudaError_t update_dispatch(const W* X, int64_t n, int d, int k, const int32_t* 
     const int64_t P = kPiece;
     scan_kernel<<<1, 1024, 0, s>>>(cnt, k, P, offs, cursor, us.mpo, acc + L.counts());
     if (det) {
-        static bool attr = false;
-        if (!attr) {
+        static PerDeviceOnce attr;
+        if (attr.need()) {
             cudaFuncSetAttribute(scatter_det_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kDetHistBytes + kDetRows * (int)sizeof(int));
-            attr = true;
+            attr.done();
         }
         scatter_det_kernel<<<(unsigned)nb, 32 * scatter_warps(k), scatter_smem(k), s>>>(
             labels, n, k, offs, us.cb, perm);
@@ -946,11 +946,11 @@ cudaError_t launch_update_fx(const float* Xw, int64_t n, int d, int k, const int
     block_scan_kernel<<<(unsigned)((k + 31) / 32), 1024, 0, s>>>(us.cb, nb, k, cnt, gate);
     const int64_t P = kPiece;
     scan_kernel<<<1, 1024, 0, s>>>(cnt, k, P, offs, cursor, us.mpo, nullptr, gate);
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    if (attr.need()) {
         cudaFuncSetAttribute(scatter_det_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kDetHistBytes + kDetRows * (int)sizeof(int));
-        attr = true;
+        attr.done();
     }
     scatter_det_kernel<<<(unsigned)nb, 32 * scatter_warps(k), scatter_smem(k), s>>>(
         labels, n, k, offs, us.cb, perm, gate);

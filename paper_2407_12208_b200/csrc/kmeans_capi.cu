@@ -86,8 +86,8 @@ struct kmeans_ctx {
     bool fx_amax_done = false;     // this fit's prep computed the column maxima
     FxState fx;
 
-    // distributed
-    ncclComm_t comm = nullptr;
+    // distributed (A6): NCCL or virtual ranks; null on a single-rank handle
+    Coll* comm = nullptr;
     int nranks = 1, rank = 0;
 
     kmeans_stats stats{};
@@ -115,12 +115,15 @@ int fail(kmeans_ctx* h, int code, const std::string& msg) {
             return fail(h, KMEANS_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
     } while (0)
 
-#define CKN(call)                                                                         \
+// A6 collectives through the handle's transport (coll.cu)
+#define CKC(call)                                                                         \
     do {                                                                                  \
-        ncclResult_t _r = (call);                                                         \
-        if (_r != ncclSuccess)                                                            \
-            return fail(h, KMEANS_ENCCL, std::string(#call) + ": " + ncclGetErrorString(_r)); \
+        std::string _m;                                                                   \
+        int _r = (call);                                                                  \
+        if (_r != 0) return fail(h, _r, _m);                                              \
     } while (0)
+#define AR(send, recv, count, type, op) \
+    h->comm->allreduce((send), (recv), (count), (type), (op), h->stream, &_m)
 
 int elem_size(int prec) {
     switch (prec) {
@@ -182,11 +185,14 @@ void free_all(kmeans_ctx* h) {
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
-    if (h->comm) ncclCommDestroy(h->comm);
+    delete h->comm;
+    h->comm = nullptr;
 }
 
 int create_impl(int64_t n, int32_t d, int32_t k, int work, int dist, int flags,
-                kmeans_handle* out, const void* nccl_id, int nranks, int rank) {
+                kmeans_handle* out, const void* nccl_id, int nranks, int rank,
+                VGroup* vgroup = nullptr) {
+    const bool sharded = nccl_id != nullptr || vgroup != nullptr;
     kmeans_ctx* h = nullptr;
     if (!out) return fail(nullptr, KMEANS_EINVAL, "out is NULL");
     *out = nullptr;
@@ -303,7 +309,7 @@ int create_impl(int64_t n, int32_t d, int32_t k, int work, int dist, int flags,
         CA(dalloc(&h->fx.prev, (size_t)n * sizeof(int32_t)));
         CA(dalloc(&h->fx.list, (size_t)h->fx.cap * sizeof(int3)));
         CA(dalloc(&h->fx.gate, 4 * sizeof(int)));
-        if (nccl_id) {          // sharded: each rank keeps its shard's totals; A6 sums them
+        if (sharded) {          // sharded: each rank keeps its shard's totals; A6 sums them
             CA(dalloc(&h->fx.gShi, (size_t)k * d * sizeof(long long)));
             CA(dalloc(&h->fx.gSlo, (size_t)k * d * sizeof(long long)));
             CA(dalloc(&h->fx.gcnt, (size_t)k * sizeof(int)));
@@ -328,12 +334,14 @@ int create_impl(int64_t n, int32_t d, int32_t k, int work, int dist, int flags,
             return bail(KMEANS_ECUDA, "tcgen05 plan: " + e);
         }
     }
-    if (nranks > 1) {
-        ncclUniqueId id;
-        memcpy(&id, nccl_id, sizeof(id));
-        ncclResult_t r = ncclCommInitRank(&h->comm, nranks, id, rank);
-        if (r != ncclSuccess) return bail(KMEANS_ENCCL, std::string("ncclCommInitRank: ") +
-                                                            ncclGetErrorString(r));
+    if (sharded) {
+        // A6 transport: an NCCL communicator (also for one rank, so that every collective call
+        // site runs), or a rank of a virtual group on this device
+        std::string e;
+        h->comm = vgroup ? coll_create_virtual(vgroup, rank, &e)
+                         : coll_create_nccl(nccl_id, nranks, rank, &e);
+        if (!h->comm) return bail(vgroup ? KMEANS_EINVAL : KMEANS_ENCCL, e);
+        if (cudaStream_t ss = h->comm->shared_stream()) h->stream = ss;
     }
     // identity transform until a normalising fit
     std::vector<double> zero(d, 0.0), one(d, 1.0);
@@ -364,7 +372,7 @@ int normalise_stats(kmeans_ctx* h, const void* Xsrc, int64_t rows) {
     if (h->comm) {
         double* tmp = h->sse_dev + 2;
         CK(cudaMemcpyAsync(tmp, &n_total, sizeof(double), cudaMemcpyHostToDevice, s));
-        CKN(ncclAllReduce(tmp, tmp, 1, ncclDouble, ncclSum, h->comm, s));
+        CKC(AR(tmp, tmp, 1, CT_F64, CO_SUM));
         CK(cudaMemcpyAsync(&n_total, tmp, sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
     }
@@ -380,15 +388,15 @@ int normalise_stats(kmeans_ctx* h, const void* Xsrc, int64_t rows) {
     CK(launch_norm_stats(h->work, h->norm, Xsrc, rows, h->d, h->partials, nb, h->shift,
                          h->scale, s));
     if (h->norm == KMEANS_NORM_ZSCORE) {
-        if (h->comm) CKN(ncclAllReduce(h->shift, h->shift, h->d, ncclDouble, ncclSum, h->comm, s));
+        if (h->comm) CKC(AR(h->shift, h->shift, h->d, CT_F64, CO_SUM));
         CK(launch_norm_post(0, h->d, n_total, h->shift, h->scale, s));
         CK(launch_norm_ssq(h->work, Xsrc, rows, h->d, h->partials, nb, h->shift, h->scale, s));
-        if (h->comm) CKN(ncclAllReduce(h->scale, h->scale, h->d, ncclDouble, ncclSum, h->comm, s));
+        if (h->comm) CKC(AR(h->scale, h->scale, h->d, CT_F64, CO_SUM));
         CK(launch_norm_post(1, h->d, n_total, h->shift, h->scale, s));
     } else {
         if (h->comm) {
-            CKN(ncclAllReduce(h->shift, h->shift, h->d, ncclDouble, ncclMin, h->comm, s));
-            CKN(ncclAllReduce(h->scale, h->scale, h->d, ncclDouble, ncclMax, h->comm, s));
+            CKC(AR(h->shift, h->shift, h->d, CT_F64, CO_MIN));
+            CKC(AR(h->scale, h->scale, h->d, CT_F64, CO_MAX));
         }
         CK(launch_norm_post(2, h->d, n_total, h->shift, h->scale, s));
     }
@@ -641,10 +649,10 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
         // disables FX for the fit (the grid needs finite values).
         CK(launch_fx_colmax((const float*)h->Xw, n, d, h->fx, h->fx_amax_done, s));
         if (h->comm) {          // one grid for all ranks; any rank's non-finite X disables FX
-            ncclGroupStart();
-            CKN(ncclAllReduce(h->fx.amax, h->fx.amax, d, ncclUint32, ncclMax, h->comm, s));
-            CKN(ncclAllReduce(h->fx.gate + 2, h->fx.gate + 2, 1, ncclInt32, ncclMax, h->comm, s));
-            ncclGroupEnd();
+            h->comm->group_start();
+            CKC(AR(h->fx.amax, h->fx.amax, d, CT_U32, CO_MAX));
+            CKC(AR(h->fx.gate + 2, h->fx.gate + 2, 1, CT_I32, CO_MAX));
+            CKC(h->comm->group_end(&_m));
         }
         CK(launch_fx_scale(d, h->fx, s));
         CK(cudaMemsetAsync(h->fx.Shi, 0, (size_t)k * d * sizeof(long long), s));
@@ -692,19 +700,19 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
             if (timing) CK(cudaEventRecord(t2, s));
         }
         if (h->comm && fx_on)        // A6: the FX totals are reduced below; here SSE_t, changed
-            CKN(ncclAllReduce(h->acc + h->L.sse(), h->acc + h->L.sse(), h->L.total() - h->L.sse(),
-                              ncclDouble, ncclSum, h->comm, s));
+            CKC(AR(h->acc + h->L.sse(), h->acc + h->L.sse(), h->L.total() - h->L.sse(), CT_F64,
+                   CO_SUM));
         else if (h->comm)                                                    // A6
-            CKN(ncclAllReduce(h->acc, h->acc, h->L.total(), ncclDouble, ncclSum, h->comm, s));
+            CKC(AR(h->acc, h->acc, h->L.total(), CT_F64, CO_SUM));
         if (timing) CK(cudaEventRecord(t3, s));
         if (fx_on && h->comm) {
             // A6 for the exact totals: integer sums, so the allreduce is exact and every rank
             // finalises the same centres
-            ncclGroupStart();
-            CKN(ncclAllReduce(h->fx.Shi, h->fx.gShi, (size_t)k * d, ncclInt64, ncclSum, h->comm, s));
-            CKN(ncclAllReduce(h->fx.Slo, h->fx.gSlo, (size_t)k * d, ncclInt64, ncclSum, h->comm, s));
-            CKN(ncclAllReduce(h->cnt, h->fx.gcnt, k, ncclInt32, ncclSum, h->comm, s));
-            ncclGroupEnd();
+            h->comm->group_start();
+            CKC(AR(h->fx.Shi, h->fx.gShi, (size_t)k * d, CT_I64, CO_SUM));
+            CKC(AR(h->fx.Slo, h->fx.gSlo, (size_t)k * d, CT_I64, CO_SUM));
+            CKC(AR(h->cnt, h->fx.gcnt, k, CT_I32, CO_SUM));
+            CKC(h->comm->group_end(&_m));
             CK(launch_finalize_fx(k, d, h->fx, h->fx.gShi, h->fx.gSlo, h->fx.gcnt, h->acc, h->L,
                                   (float*)h->Cw, rec, s));
         } else if (fx_on)
@@ -732,7 +740,7 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
         CK(cudaMemsetAsync(h->sse_dev, 0, sizeof(double), s));
         CK(launch_final_sse(h->work, h->Xw, n, d, h->Cw, h->labels, h->sse_dev, s));
         if (h->comm)
-            CKN(ncclAllReduce(h->sse_dev, h->sse_dev, 1, ncclDouble, ncclSum, h->comm, s));
+            CKC(AR(h->sse_dev, h->sse_dev, 1, CT_F64, CO_SUM));
     }
     CK(cudaEventRecord(e3, s));
 
@@ -798,6 +806,9 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
     h->last_n_low = h->delta > 0.0 ? (int64_t)n_low_h : h->last_n_dist;
     st.n_dist_low = h->last_n_low;
     st.n_dist = h->last_n_dist;
+    st.eta = st.n_dist > 0 ? (double)st.n_dist_low / (double)st.n_dist : 1.0;
+    st.tc_variant = (h->dist_kernel == DK_TCGEN05 && h->delta <= 0.0) ? tc_plan_kind(h->tc) : 0;
+    st.n_ranks = h->nranks;
     int warn = 0;
     if (st.n_nonfinite > 0) warn |= KMEANS_WARN_NONFINITE;
     if (any_empty) warn |= KMEANS_WARN_EMPTY;
@@ -825,6 +836,33 @@ int kmeans_create_dist(int64_t n_local, int32_t d, int32_t k, int work_prec, int
     if (!nccl_unique_id && nranks > 1) return fail(nullptr, KMEANS_EINVAL, "nccl id is NULL");
     return create_impl(n_local, d, k, work_prec, dist_prec, flags, out, nccl_unique_id, nranks,
                        rank);
+}
+
+int kmeans_vgroup_create(int nranks, kmeans_vgroup* out) {
+    if (!out) return fail(nullptr, KMEANS_EINVAL, "out is NULL");
+    *out = nullptr;
+    int dev = check_device(nullptr);
+    if (dev < 0) return dev;
+    std::string e;
+    VGroup* g = vgroup_create(nranks, &e);
+    if (!g) return fail(nullptr, KMEANS_EINVAL, e);
+    *out = reinterpret_cast<kmeans_vgroup>(g);
+    return KMEANS_OK;
+}
+
+int kmeans_create_virtual(int64_t n_local, int32_t d, int32_t k, int work_prec, int dist_prec,
+                          int flags, kmeans_vgroup group, int rank, kmeans_handle* out) {
+    if (!group) return fail(nullptr, KMEANS_EINVAL, "group is NULL");
+    VGroup* g = reinterpret_cast<VGroup*>(group);
+    return create_impl(n_local, d, k, work_prec, dist_prec, flags, out, nullptr,
+                       vgroup_size(g), rank, g);
+}
+
+int kmeans_vgroup_destroy(kmeans_vgroup group) {
+    if (!group) return KMEANS_OK;
+    if (vgroup_destroy(reinterpret_cast<VGroup*>(group)) != 0)
+        return fail(nullptr, KMEANS_EINVAL, "destroy the group's handles first");
+    return KMEANS_OK;
 }
 
 int kmeans_nccl_unique_id(void* out128) {
@@ -891,6 +929,9 @@ int kmeans_assign(kmeans_handle h, const void* X, int64_t m, int32_t* labels, do
     h->last_n_low = h->delta > 0.0 ? (int64_t)n_low_h : h->last_n_dist;
     h->stats.n_dist = h->last_n_dist;
     h->stats.n_dist_low = h->last_n_low;
+    h->stats.eta = h->last_n_dist > 0 ? (double)h->last_n_low / (double)h->last_n_dist : 1.0;
+    h->stats.tc_variant =
+        (h->dist_kernel == DK_TCGEN05 && h->delta <= 0.0) ? tc_plan_kind(h->tc) : 0;
     return KMEANS_OK;
 }
 

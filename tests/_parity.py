@@ -51,3 +51,15 @@ def check_labels_admissible(lab_gpu, lab_ref, D, B, slack=2.0):
         assert ok.all(), (f"{(~ok).sum()} inadmissible labels, e.g. row {i[~ok][0]}: "
                           f"gap {gap[~ok][0]:.3e} > tol {tolr[~ok][0]:.3e}")
     return bad.size / max(1, len(lab_ref))
+
+
+def check_admissible_rows(X, C, lab_gpu, lab_ref, work, dist, guard, slack=2.0):
+    """check_labels_admissible for large n: D and B are formed only for the rows whose labels
+    differ (each row's distances depend on that row alone). Returns the mismatch fraction."""
+    lab_gpu = np.asarray(lab_gpu)
+    lab_ref = np.asarray(lab_ref)
+    bad = np.nonzero(lab_gpu != lab_ref)[0]
+    if bad.size:
+        D, B = distances_on_rounded_operands(np.asarray(X)[bad], C, work, dist, guard)
+        check_labels_admissible(lab_gpu[bad], lab_ref[bad], D, B, slack)
+    return bad.size / max(1, len(lab_ref))

@@ -130,9 +130,20 @@ def test_step_parity(work, dist, guard, force_simt):
     km.fit(dev(Xn), dev(C), max_iter=1, tol=-1.0, centroids=cent)
     cg = cent.cpu().numpy().astype(np.float64)
     if frac == 0:
+        assert np.array_equal(np.bincount(lab, minlength=k), ref["counts"])
         m = np.maximum(ref["counts"], 1)[:, None]
         tolr = (m * U[work] * 4 + 4 * U[work]) * np.abs(ref["centroids"]) + 1e-30
         assert np.all(np.abs(cg - ref["centroids"]) <= tolr)
+    # whatever the labels, the update is eq:center on the GPU's OWN labels (Alg 3 step 4,
+    # PAPER.md:547): round_u(mean of the rows labelled j), empty clusters keep c_j — so the
+    # counts behind the centres are exactly the label counts, never checked only "on agreement"
+    cnt = np.bincount(lab, minlength=k)
+    sums = np.zeros((k, d))
+    np.add.at(sums, lab, Xn.astype(np.float64))
+    want = np.where(cnt[:, None] > 0, sums / np.maximum(cnt, 1)[:, None], C.astype(np.float64))
+    want = want.astype(NP[work]).astype(np.float64)
+    tolr = (np.maximum(cnt, 1)[:, None] * 2.0 ** -52 + 4 * U[work]) * np.abs(want) + 1e-30
+    assert np.all(np.abs(cg - want) <= tolr), np.abs(cg - want).max()
     km.close()
 
 

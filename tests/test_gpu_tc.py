@@ -8,7 +8,8 @@ import torch
 
 import oracle
 import synth
-from tests._parity import check_labels_admissible, dev, distances_on_rounded_operands
+from tests._parity import (check_admissible_rows, check_labels_admissible, dev,
+                           distances_on_rounded_operands)
 
 pytestmark = pytest.mark.gpu
 mpk = pytest.importorskip("paper_2407_12208_b200")
@@ -25,12 +26,18 @@ SHAPES = [  # (n, d, k)
 ]
 
 
-@pytest.mark.parametrize("dist", ["fp16", "bf16", "e5m2"])
-@pytest.mark.parametrize("shape", SHAPES)
-@pytest.mark.parametrize("guard", [False, True])
-def test_tc_assign_matches_oracle(dist, shape, guard):
-    n, d, k = shape
-    X, _ = synth.blobs(n, d, max(2, k // 3), sigma=1.5, seed=n + d + k, dtype=np.float32)
+def _set_kind(monkeypatch, kind):
+    """kind 2: the CTA-pair kernel (k_assign_tc2.cu) wherever its resident centroid halves fit;
+    kind 1: the streaming kernel (k_assign_tc.cu), forced with MPK_TC_KIND=1 (it is selected
+    on its own when k is too large for the pair kernel, see test_tc_large_k_streaming)."""
+    if kind == 1:
+        monkeypatch.setenv("MPK_TC_KIND", "1")
+    else:
+        monkeypatch.delenv("MPK_TC_KIND", raising=False)
+
+
+def _assign_vs_oracle(n, d, k, dist, guard, seed, want_variant=None, max_frac=2e-3):
+    X, _ = synth.blobs(n, d, max(2, k // 3), sigma=1.5, seed=seed, dtype=np.float32)
     Xn, _, _ = oracle.normalize(X, "zscore", work="fp32")
     Xn = Xn.astype(np.float32)
     C = synth.init_rows(Xn, k, 3)
@@ -38,13 +45,47 @@ def test_tc_assign_matches_oracle(dist, shape, guard):
     mpk.kmeans_set_centroids(km.h, dev(C))
     lab = torch.empty(n, dtype=torch.int32, device="cuda")
     sse = km.assign(dev(Xn), lab)
+    st = km.stats()
     km.close()
+    assert st["dist_kernel"] == "tcgen05"
+    if want_variant is not None:
+        assert st["tc_variant"] == want_variant
     ref, dmin, _ = oracle.assign(Xn, C, work="fp32", dist=dist, guard=guard)
-    D, B = distances_on_rounded_operands(Xn, C, "fp32", dist, guard)
-    frac = check_labels_admissible(lab.cpu().numpy(), ref, D, B)
-    assert frac <= 2e-3
+    frac = check_admissible_rows(Xn, C, lab.cpu().numpy(), ref, "fp32", dist, guard)
+    assert frac <= max_frac
     want = np.maximum(dmin, 0).sum()
     assert abs(sse - want) <= 1e-4 * want
+    return frac
+
+
+@pytest.mark.parametrize("kind", [2, 1])
+@pytest.mark.parametrize("dist", ["fp16", "bf16", "e5m2"])
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("guard", [False, True])
+def test_tc_assign_matches_oracle(dist, shape, guard, kind, monkeypatch):
+    _set_kind(monkeypatch, kind)
+    n, d, k = shape
+    _assign_vs_oracle(n, d, k, dist, guard, n + d + k, want_variant=kind if kind == 1 else None)
+
+
+@pytest.mark.parametrize("dist", ["fp16", "bf16", "e5m2"])
+@pytest.mark.parametrize("guard", [False, True])
+def test_tc_deep_row_blocks_c5_shape(dist, guard, monkeypatch):
+    """The C5 shape (d = 128, k = 1024) with n = 200 003: every CTA pair of the 74 runs >= 10
+    row-blocks of 256 rows, so the X~ ring wraps (SA slots, phase flips) and the partial
+    buffers are reused (part_free, row-block index >= 2) many times, as at the bench size —
+    against the oracle label by label (admissible under 2 B_acc), with a ragged tail."""
+    _set_kind(monkeypatch, 2)
+    _assign_vs_oracle(200_003, 128, 1024, dist, guard, 77, want_variant=2)
+
+
+@pytest.mark.parametrize("dist,k,variant", [("fp16", 2048, 1), ("bf16", 2048, 1),
+                                            ("e5m2", 2048, 2), ("e5m2", 4096, 1)])
+def test_tc_large_k_streaming(dist, k, variant, monkeypatch):
+    """k beyond the pair kernel's resident centroid halves (d = 128: k > ~1300 at fp16, > ~2600
+    at E5M2) selects the streaming kernel without any override; parity as above."""
+    _set_kind(monkeypatch, 2)
+    _assign_vs_oracle(20_011, 128, k, dist, False, k + 5, want_variant=variant)
 
 
 def test_tc_kernel_is_selected():
@@ -74,12 +115,14 @@ def test_tc_vs_simt_same_fit(dist):
     assert np.mean(res[0][1] == res[1][1]) > 0.995
 
 
+@pytest.mark.parametrize("kind", [2, 1])
 @pytest.mark.parametrize("dist,guard", [("fp16", False), ("bf16", False), ("e5m2", False),
                                         ("fp16", True), ("e5m2", True)])
-def test_final_pass_certified_filter(dist, guard):
+def test_final_pass_certified_filter(dist, guard, kind, monkeypatch):
     """Alg 3 step 7 via the certified tensor-core filter: the final labels equal the
     working-precision argmin for the returned centroids (checked against an fp64 evaluation,
     mismatches allowed only within the fp32 evaluation error), with few CUDA-core fallbacks."""
+    _set_kind(monkeypatch, kind)
     X, _, C0 = synth.make("c3_blobs_1m_d64", n=25000, seed=3)
     C0 = C0[:96].copy()
     km = mpk.KMeans(len(X), 64, 96, "fp32", dist, norm="zscore", guard=guard)
@@ -91,7 +134,7 @@ def test_final_pass_certified_filter(dist, guard):
     scale = np.empty(64, np.float32)
     mpk.kmeans_get_transform(km.h, shift, scale)
     km.close()
-    assert st["dist_kernel"] == "tcgen05"
+    assert st["dist_kernel"] == "tcgen05" and st["tc_variant"] == kind
     assert 0 <= st["n_final_fallback"] <= 0.01 * len(X)
     ref = oracle.fit(X, C0, work="fp32", dist=dist, norm="zscore", guard=guard, max_iter=6,
                      tol=-1.0)

@@ -224,6 +224,55 @@ def test_k1_mean_and_sse_closed_form():
     assert abs(r["sse"] - want) <= 1e-12 * want
 
 
+@pytest.mark.parametrize("work,dist", [("fp64", "fp64"), ("fp32", "fp16"), ("fp32", "e5m2")])
+def test_iteration_sse_k1_closed_form(work, dist):
+    """O6 (SSE_t = sum_i max(0, min_j D^_ij), eq:sse PAPER.md:130-133) pinned by value with
+    k = 1: from C0 = x_0, SSE_1 = sum_i ||x_i - x_0||^2 and then SSE_2 = sum_i ||x_i - mu||^2
+    (mu the mean, eq:center). The data are small integers (exact in fp16 and E5M2, every
+    product and sum exact), so the expanded formula of O4 equals the direct one exactly and
+    SSE_1 is an exact integer. A dropped ||x||^2 or ||c||^2 term, a wrong sign of the cross
+    term or a missing clamp changes SSE_1."""
+    rng = np.random.default_rng(21)
+    X = rng.integers(-3, 4, size=(64, 5)).astype(np.float64)
+    X[0] = [1, -2, 0, 3, -1]
+    # column sums divisible by 64 make mu an exact dyadic value
+    X[-1] -= X.sum(0) - 64 * np.round(X.sum(0) / 64)
+    X[-1] = np.clip(X[-1], -3, 3)
+    r = oracle.fit(X, X[:1], work=work, dist=dist, max_iter=2, tol=-1.0)
+    exact1 = sum(sum((Fraction(a) - Fraction(b)) ** 2 for a, b in zip(x, X[0])) for x in X)
+    assert r["sse_t"][0] == float(exact1)
+    mu = [sum(Fraction(v) for v in X[:, t]) / len(X) for t in range(X.shape[1])]
+    exact2 = sum(sum((Fraction(a) - m) ** 2 for a, m in zip(x, mu)) for x in X)
+    # the centroid is mu rounded to the working precision; SSE_2 from the low-precision
+    # operand c~ = round_l(mu): bound the effect of both roundings on the sum
+    u = U[dist]
+    slack = 4 * u * float(sum(sum(abs(Fraction(a)) + abs(m) for a, m in zip(x, mu)) for x in X)) \
+        * max(1.0, float(max(abs(m) for m in mu)))
+    assert abs(r["sse_t"][1] - float(exact2)) <= slack + 1e-12 * float(exact2)
+    if dist == "fp64":
+        assert abs(r["sse_t"][1] - float(exact2)) <= 1e-12 * float(exact2)
+    assert r["changed_t"].tolist() == [64, 0]
+
+
+def test_guard_scale_by_value():
+    """Alg 4 lines 1-5: s = ||x||_inf and x~ = round_l(x / s). Pinned by
+    value: (3, -4, 1) -> s = 4, x~ = (0.75, -1, 0.25); (3, 1, -2) -> s = 3 (not the 2-norm
+    sqrt(14), not a power of two), x~ = fp16(1, 1/3, -2/3); a zero row -> s = 1 (Z10). Norms are
+    the unscaled ||x||^2."""
+    X = np.array([[3.0, -4.0, 1.0], [3.0, 1.0, -2.0], [0.0, 0.0, 0.0], [-0.5, 0.25, 0.125]])
+    xl, nrm, sc = oracle.prep(X, work="fp32", dist="fp16", guard=True)
+    assert sc.tolist() == [4.0, 3.0, 1.0, 0.5]
+    assert nrm.tolist() == [26.0, 14.0, 0.0, 0.328125]
+    want = np.array([[0.75, -1.0, 0.25],
+                     [1.0, float(np.float16(1.0 / 3.0)), float(np.float16(-2.0 / 3.0))],
+                     [0.0, 0.0, 0.0], [-1.0, 0.5, 0.25]])
+    assert np.array_equal(xl, want)
+    # unguarded: s = 1, x~ = round_l(x)
+    xl0, _, sc0 = oracle.prep(X, work="fp32", dist="e5m2", guard=False)
+    assert sc0.tolist() == [1.0] * 4
+    assert np.array_equal(xl0, X)   # every value is exact in E5M2
+
+
 def test_k_equals_n_zero_sse():
     rng = np.random.default_rng(10)
     X = rng.standard_normal((50, 3))
