@@ -240,13 +240,15 @@ assign_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                                 fold32<false, FINAL>(v1, cn_s, sc_s, m2[h], j0 + 32, cv[h], cs[h], c2[h]);
                             }
                         }
-                    } else if ((p.BN & 31) == 0) {
-                        uint32_t v0[32];
-                        tmem_ld32(col0, v0);
-                        tmem_wait_ld();
-                        const int j0 = t * p.BN;
-                        if (p.guard) fold32<true, FINAL>(v0, cn_s, sc_s, m2[h], j0, cv[h], cs[h], c2[h]);
-                        else fold32<false, FINAL>(v0, cn_s, sc_s, m2[h], j0, cv[h], cs[h], c2[h]);
+                    } else if ((p.BN & 31) == 0) {   // BN = 32, 96: 32-column chunks
+                        for (int c = 0; c < p.BN; c += 32) {
+                            uint32_t v0[32];
+                            tmem_ld32(col0 + c, v0);
+                            tmem_wait_ld();
+                            const int j0 = t * p.BN + c;
+                            if (p.guard) fold32<true, FINAL>(v0, cn_s, sc_s, m2[h], j0, cv[h], cs[h], c2[h]);
+                            else fold32<false, FINAL>(v0, cn_s, sc_s, m2[h], j0, cv[h], cs[h], c2[h]);
+                        }
                     } else {   // BN == 16
                         uint32_t v[32];
                         tmem_ld16(col0, v);
@@ -357,11 +359,22 @@ int tc_dpad(int dist, int d) {
     return rb / es;
 }
 
+// The streaming kernel keeps 2R (R >= 2) row-block slots of 128 rows: 4 x 128 x RB bytes must
+// leave room for at least two centroid stages, which holds for rows of at most 256 bytes.
+static bool stream_plan_fits(int rb) { return rb <= 256; }
+
 bool tc_supported(int dist, int d_pad, int k) {
     if (dist != KMEANS_FP16 && dist != KMEANS_BF16 && dist != KMEANS_E5M2) return false;
     int rb = d_pad * esize_of(dist);
     if (rb > 512) return false;    // A tile <= 64 KB
     if (k < 16) return false;      // tiny k: the CUDA-core kernels are the right tool
+    if (!stream_plan_fits(rb)) {
+        // 512-byte rows (fp16/bf16, 192 < d <= 256): only the CTA-pair kernel, and only while
+        // its resident centroid halves fit; beyond that the CUDA-core kernel serves
+        tcdev::PairParams pp;
+        size_t smem = 0;
+        return tcdev::pair_plan(dist, d_pad, d_pad, k, &pp, &smem);
+    }
     return true;
 }
 
@@ -423,7 +436,8 @@ TcPlan* tc_plan_create(int dist, int64_t n, int d, int d_pad, int k, const void*
     pl->esize = es;
     // Preferred: CTA pairs with the centroid tiles resident in shared memory (k_assign_tc2.cu).
     const char* force = getenv("MPK_TC_KIND");
-    if (!(force && force[0] == '1')) {
+    // MPK_TC_KIND=1 (tests, experiments) forces the streaming kernel where its plan fits
+    if (!(force && force[0] == '1' && stream_plan_fits(d_pad * es))) {
         size_t smem = 0;
         if (tcdev::pair_plan(dist, d, d_pad, k, &pl->pp, &smem)) {
             const int swz = pl->pp.SWZ;

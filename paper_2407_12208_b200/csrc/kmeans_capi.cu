@@ -930,6 +930,7 @@ int kmeans_assign(kmeans_handle h, const void* X, int64_t m, int32_t* labels, do
     h->stats.n_dist = h->last_n_dist;
     h->stats.n_dist_low = h->last_n_low;
     h->stats.eta = h->last_n_dist > 0 ? (double)h->last_n_low / (double)h->last_n_dist : 1.0;
+    h->stats.dist_kernel = h->dist_kernel;
     h->stats.tc_variant =
         (h->dist_kernel == DK_TCGEN05 && h->delta <= 0.0) ? tc_plan_kind(h->tc) : 0;
     return KMEANS_OK;

@@ -23,6 +23,7 @@ SHAPES = [  # (n, d, k)
     (777, 200, 130),
     (5000, 8, 16),
     (129, 64, 17),
+    (3001, 64, 96),     # streaming kernel: a 96-column tile (three 32-column chunks)
 ]
 
 
@@ -65,7 +66,19 @@ def _assign_vs_oracle(n, d, k, dist, guard, seed, want_variant=None, max_frac=2e
 def test_tc_assign_matches_oracle(dist, shape, guard, kind, monkeypatch):
     _set_kind(monkeypatch, kind)
     n, d, k = shape
-    _assign_vs_oracle(n, d, k, dist, guard, n + d + k, want_variant=kind if kind == 1 else None)
+    es = 1 if dist == "e5m2" else 2
+    variant = None
+    if kind == 1:
+        # the streaming kernel holds rows of at most 256 bytes; 512-byte rows stay on the pair
+        # kernel even when kind 1 is requested
+        variant = 1 if mpk_row_bytes(d, es) <= 256 else 2
+    _assign_vs_oracle(n, d, k, dist, guard, n + d + k, want_variant=variant)
+
+
+def mpk_row_bytes(d, es):
+    """Padded operand row length in bytes (k_assign_tc.cu tc_dpad)."""
+    rb = (d * es + 31) // 32 * 32
+    return (rb + 127) // 128 * 128 if rb > 64 else rb
 
 
 @pytest.mark.parametrize("dist", ["fp16", "bf16", "e5m2"])
@@ -86,6 +99,26 @@ def test_tc_large_k_streaming(dist, k, variant, monkeypatch):
     at E5M2) selects the streaming kernel without any override; parity as above."""
     _set_kind(monkeypatch, 2)
     _assign_vs_oracle(20_011, 128, k, dist, False, k + 5, want_variant=variant)
+
+
+def test_wide_rows_large_k_use_cuda_cores():
+    """fp16 rows of 512 bytes (d = 256) with k = 1024: neither tcgen05 plan fits in shared
+    memory, so the handle takes the CUDA-core low-precision kernel (same arithmetic model) —
+    created without error and parity-green."""
+    n, d, k = 3001, 256, 1024
+    X, _ = synth.blobs(n, d, 50, sigma=1.5, seed=3, dtype=np.float32)
+    Xn, _, _ = oracle.normalize(X, "zscore", work="fp32")
+    Xn = Xn.astype(np.float32)
+    C = synth.init_rows(Xn, k, 3)
+    km = mpk.KMeans(n, d, k, "fp32", "fp16")
+    mpk.kmeans_set_centroids(km.h, dev(C))
+    lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    km.assign(dev(Xn), lab)
+    st = km.stats()
+    km.close()
+    assert st["dist_kernel"] == "simt_low" and st["tc_variant"] == 0
+    ref, _, _ = oracle.assign(Xn, C, work="fp32", dist="fp16", guard=False)
+    assert check_admissible_rows(Xn, C, lab.cpu().numpy(), ref, "fp32", "fp16", False) <= 2e-3
 
 
 def test_tc_kernel_is_selected():
@@ -135,7 +168,13 @@ def test_final_pass_certified_filter(dist, guard, kind, monkeypatch):
     mpk.kmeans_get_transform(km.h, shift, scale)
     km.close()
     assert st["dist_kernel"] == "tcgen05" and st["tc_variant"] == kind
-    assert 0 <= st["n_final_fallback"] <= 0.01 * len(X)
+    if kind == 2:
+        # uncertified rows are resolved from their candidate columns (R2)
+        assert 0 <= st["n_final_fallback"] <= 0.01 * len(X)
+    else:
+        # the streaming kernel has no candidate mode: every uncertified row is re-evaluated
+        # over all k centroids on CUDA cores
+        assert st["n_final_fallback"] == st["n_final_uncertified"] <= 0.3 * len(X)
     ref = oracle.fit(X, C0, work="fp32", dist=dist, norm="zscore", guard=guard, max_iter=6,
                      tol=-1.0)
     Xn = oracle.apply_normalization(X, ref["shift"], ref["scale"], "fp32")
