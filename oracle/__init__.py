@@ -58,6 +58,7 @@ def _load():
             lib.oracle_final.argtypes = [i64, i32, i32, i32, P, P, P, P]
             lib.oracle_num_threads.restype = i32
             lib.oracle_seed_d2.argtypes = [i64, i32, i32, i32, i32, i32, P, P, P, P, P]
+            lib.oracle_seed_weights.argtypes = [i64, i32, i32, i32, i32, P, P, i32, P]
             _lib = lib
     return _lib
 
@@ -233,3 +234,19 @@ def seed_d2(X, k, u, work="fp32", dist="fp16", norm="none", guard=False, return_
     if return_d2:
         return idx, warn.value, d2
     return idx, warn.value
+
+
+def seed_weights(X, centres, work="fp32", dist="fp16", norm="none", guard=False):
+    """O10's D^2 weights (Alg 1 line 2) for the given chosen centres (row indices): min over the
+    centres of the low-precision expanded D^2, 0 at the centres — for teacher-forced checks of a
+    seeding whose draws were made elsewhere."""
+    lib = _load()
+    X = _f64(X)
+    n, d = X.shape
+    c = np.ascontiguousarray(np.asarray(centres, dtype=np.int64))
+    out = np.empty(n)
+    rc = lib.oracle_seed_weights(n, d, _prec(work), _prec(dist), _flags(norm, guard), _p(X),
+                                 _p(c), c.size, _p(out))
+    if rc != 0:
+        raise ValueError(f"oracle_seed_weights rc={rc}")
+    return out

@@ -499,21 +499,18 @@ int oracle_assign(int64_t n, int d, int k, int work, int dist, int guard, const 
 /* O10: seeding by D^2 weighting (Alg 1) with the distances of Alg 3 step 1 */
 /* "in precision u_l": after O1 and O2, D^2(p_i, c) is O4's expanded formula    */
 /* from the stored low-precision operands (the dot accumulated sequentially in fp64), floored */
-/* at 0; the centre c is a data point, so its operands are that row's. Reading R6 fixes what  */
-/* the paper leaves open:                                                                      */
+/* at 0; the centre c is a data point, so its operands are that row's. Line 2 of Alg 1 draws  */
+/* p' with probability D(p')^2 / sum_p D(p)^2; reading R6 makes the draw explicit:             */
 /*   * the caller supplies k uniforms u_j in [0,1) (the method's random draws);               */
 /*   * first centre: index min(floor(u_0 n), n-1) ("uniformly", line 1);                      */
-/*   * D2[i] = min over chosen centres; S = the sum of D2 in the order: sequential fp64 sums   */
-/*     over blocks of SEED_BLOCK consecutive indices, then the block sums sequentially;        */
-/*   * next centre: the first index i whose running sum (preceding blocks + this block's      */
-/*     prefix, each in that order) exceeds u_j S; i then has D2[i] > 0, so it is new;          */
+/*   * D2[i] = min over chosen centres; S = sum_i D2[i] (sequential, index order);            */
+/*   * next centre: the first index i whose running sum D2[0] + ... + D2[i] (sequential)      */
+/*     exceeds u_j S — the inverse-CDF draw of the law above; i then has D2[i] > 0 (new);     */
 /*   * S = 0 or non-finite (every point coincides with a centre, or overflow): uniform index   */
 /*     min(floor(u_j n), n-1) and *warn |= 1 (SPEC S:208's fallback);                          */
 /*   * a chosen centre's own weight is 0 (dist(c, c) = 0; the expanded formula in low          */
 /*     precision leaves a rounding residue there), so the k centres are distinct. */
 /* ---------------------------------------------------------------------------------------- */
-#define SEED_BLOCK 4096
-
 static double seed_dist(const ostate_t* S, int64_t i, int64_t c) {
     const double* xl = S->Xl + i * S->d;
     const double* cl = S->Xl + c * S->d;
@@ -523,24 +520,38 @@ static double seed_dist(const ostate_t* S, int64_t i, int64_t c) {
     return (D > 0.0) ? D : 0.0;   /* NaN -> 0 */
 }
 
-int oracle_seed_d2(int64_t n, int d, int k, int work, int dist, int flags, const double* X_in,
-                   const double* u, int64_t* idx_out, double* d2_out, int* warn) {
-    if (check_args(n, d, k, work, dist, flags) != 0 || k > n) return -1;
+static int seed_prepare(ostate_t* S, int64_t n, int d, int work, int dist, int flags,
+                        const double* X_in) {
     int norm = flags & ONORM_MASK, guard = (flags & OGUARD) != 0;
-    ostate_t S;
-    if (alloc_state(&S, n, d, 1, work, dist, guard) != 0) { free_state(&S); return -2; }
+    if (alloc_state(S, n, d, 1, work, dist, guard) != 0) return -2;
     double* shift = (double*)malloc(sizeof(double) * d);
     double* scale = (double*)malloc(sizeof(double) * d);
     oracle_normalize_stats(norm, n, d, X_in, shift, scale);
     if (norm == ONORM_NONE) {
-        for (int64_t i = 0; i < n * d; ++i) S.X[i] = oracle_round(work, X_in[i]);
+        for (int64_t i = 0; i < n * d; ++i) S->X[i] = oracle_round(work, X_in[i]);
     } else {
-        oracle_normalize_apply(work, n, d, shift, scale, X_in, S.X);
+        oracle_normalize_apply(work, n, d, shift, scale, X_in, S->X);
     }
-    prep_points(&S);
+    free(shift); free(scale);
+    prep_points(S);
+    return 0;
+}
+
+/* D2[i] <- min(D2[i], D^2(p_i, c)), the centre's own weight 0 (Alg 1 line 2's D(p)). */
+static void seed_min_update(const ostate_t* S, int64_t n, int64_t c, double* D2) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        double D = (i == c) ? 0.0 : seed_dist(S, i, c);
+        if (D < D2[i]) D2[i] = D;
+    }
+}
+
+int oracle_seed_d2(int64_t n, int d, int k, int work, int dist, int flags, const double* X_in,
+                   const double* u, int64_t* idx_out, double* d2_out, int* warn) {
+    if (check_args(n, d, k, work, dist, flags) != 0 || k > n) return -1;
+    ostate_t S;
+    if (seed_prepare(&S, n, d, work, dist, flags, X_in) != 0) { free_state(&S); return -2; }
     double* D2 = (double*)malloc(sizeof(double) * n);
-    const int64_t nb = (n + SEED_BLOCK - 1) / SEED_BLOCK;
-    double* ps = (double*)malloc(sizeof(double) * nb);
     int w = 0;
     for (int64_t i = 0; i < n; ++i) D2[i] = INFINITY;
     int64_t c = (int64_t)(u[0] * (double)n);
@@ -548,19 +559,9 @@ int oracle_seed_d2(int64_t n, int d, int k, int work, int dist, int flags, const
     if (c < 0) c = 0;
     idx_out[0] = c;
     for (int j = 1; j < k; ++j) {
-#pragma omp parallel for schedule(static)
-        for (int64_t i = 0; i < n; ++i) {
-            double D = (i == c) ? 0.0 : seed_dist(&S, i, c);
-            if (D < D2[i]) D2[i] = D;
-        }
+        seed_min_update(&S, n, c, D2);
         double tot = 0.0;
-        for (int64_t b = 0; b < nb; ++b) {
-            double a = 0.0;
-            int64_t e = (b + 1) * SEED_BLOCK < n ? (b + 1) * SEED_BLOCK : n;
-            for (int64_t i = b * SEED_BLOCK; i < e; ++i) a += D2[i];
-            ps[b] = a;
-            tot += a;
-        }
+        for (int64_t i = 0; i < n; ++i) tot += D2[i];
         if (!(tot > 0.0) || isinf(tot)) {
             c = (int64_t)(u[j] * (double)n);
             if (c > n - 1) c = n - 1;
@@ -568,31 +569,42 @@ int oracle_seed_d2(int64_t n, int d, int k, int work, int dist, int flags, const
         } else {
             const double target = u[j] * tot;
             double run = 0.0;
-            int64_t b = 0;
-            for (; b < nb - 1; ++b) {
-                if (run + ps[b] > target) break;
-                run += ps[b];
+            c = -1;
+            for (int64_t i = 0; i < n; ++i) {
+                run += D2[i];
+                if (run > target) { c = i; break; }
             }
-            double loc = 0.0;
-            int64_t e = (b + 1) * SEED_BLOCK < n ? (b + 1) * SEED_BLOCK : n;
-            c = e - 1;
-            for (int64_t i = b * SEED_BLOCK; i < e; ++i) {
-                loc += D2[i];
-                if (run + loc > target) { c = i; break; }
+            if (c < 0) {             /* rounding left the target at the very top: last positive */
+                for (int64_t i = n - 1; i >= 0; --i)
+                    if (D2[i] > 0.0) { c = i; break; }
             }
         }
         idx_out[j] = c;
     }
     if (d2_out) {
         /* D2 after the last centre too (the weights a (k+1)-th draw would use) */
-#pragma omp parallel for schedule(static)
-        for (int64_t i = 0; i < n; ++i) {
-            double D = (i == c) ? 0.0 : seed_dist(&S, i, c);
-            d2_out[i] = (D < D2[i]) ? D : D2[i];
-        }
+        seed_min_update(&S, n, c, D2);
+        memcpy(d2_out, D2, sizeof(double) * n);
     }
     if (warn) *warn = w;
-    free(D2); free(ps); free(shift); free(scale);
+    free(D2);
+    free_state(&S);
+    return 0;
+}
+
+/* The D^2 weights of O10 for a given list of m chosen centres (teacher-forced checks of a
+ * seeding that made its own draws): D2[i] = min over the centres of D^2(p_i, c), 0 at the
+ * centres themselves. */
+int oracle_seed_weights(int64_t n, int d, int work, int dist, int flags, const double* X_in,
+                        const int64_t* centres, int m, double* D2) {
+    if (check_args(n, d, 1, work, dist, flags) != 0 || m < 1) return -1;
+    ostate_t S;
+    if (seed_prepare(&S, n, d, work, dist, flags, X_in) != 0) { free_state(&S); return -2; }
+    for (int64_t i = 0; i < n; ++i) D2[i] = INFINITY;
+    for (int q = 0; q < m; ++q) {
+        if (centres[q] < 0 || centres[q] >= n) { free_state(&S); return -1; }
+        seed_min_update(&S, n, centres[q], D2);
+    }
     free_state(&S);
     return 0;
 }

@@ -114,6 +114,24 @@ cudaError_t launch_smalld_fused(int work, int dist, const Problem& p, const void
                                 const void* Cl, const void* cn, const void* sc, int32_t* labels,
                                 double* acc, AccLayout L, cudaStream_t s);
 
+// K5g: one whole Lloyd iteration of the small-d path on one rank in ONE launch (k_smalld_loop.cu):
+// centroid prep, distance + argmin, deterministic block partials of the update, and the last
+// block's finalize + trace record + stopping rule. A launch after the stop flag is set returns
+// at once, so the host enqueues chunks of iterations (a CUDA graph) and polls once per chunk.
+struct LoopState {
+    int iter;          // iterations completed
+    int stop;          // set when converged: later launches are no-ops
+    int converged;
+    unsigned counter;  // block ticket of the current launch (reset by the last block)
+    double tol;        // < 0: never stop early
+};
+bool smalld_loop_supported(int d, int k);
+int smalld_loop_grid(int64_t n);
+size_t smalld_loop_part_bytes(int64_t n);
+cudaError_t launch_smalld_iter(int work, int dist, const Problem& p, const void* Xw, void* Cw,
+                               int32_t* labels, double* part, LoopState* st, IterRec* trace,
+                               unsigned long long* census, cudaStream_t s);
+
 // K6m: Alg 4's per-pair precision switch with threshold delta (>= 1); n_low (device) gets the
 // number of triggered (low-precision) pairs added.
 cudaError_t launch_assign_mixed(int work, int dist, const Problem& p, double delta, const void* Xl,

@@ -363,17 +363,28 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
         const bool guard = p.guard != 0;
         double my_sse = 0.0, my_changed = 0.0;
         int64_t rbi = 0;
-        for (int64_t rb = pair; rb < num_rb; rb += npairs, ++rbi) {
-            const int par = (int)(rbi & 1);
-            // this row-block's point data (issued before waiting for the partials)
-            float xn_r[4];
-            int old_r[4];
+        // the point data of a row-block (||x||^2, the previous labels) is loaded one row-block
+        // AHEAD: with small tiles (C3/C4: one accumulator per row-block) a load issued at the
+        // row-block's own top left its whole L2/HBM latency on this warp's critical path
+        float xn_n[4];
+        int old_n[4];
+        auto load_rb = [&](int64_t rb) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int64_t row = rb * rows_per_rb + rank * P_BM + u * 32 + lane;
-                xn_r[u] = row < n ? p.xn[row] : 0.0f;
-                old_r[u] = (!FINAL && row < n) ? p.labels[row] : 0;
+                const bool ok = rb < num_rb && row < n;
+                xn_n[u] = ok ? p.xn[row] : 0.0f;
+                old_n[u] = (!FINAL && ok) ? p.labels[row] : 0;
             }
+        };
+        load_rb(pair);
+        for (int64_t rb = pair; rb < num_rb; rb += npairs, ++rbi) {
+            const int par = (int)(rbi & 1);
+            float xn_r[4];
+            int old_r[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { xn_r[u] = xn_n[u]; old_r[u] = old_n[u]; }
+            load_rb(rb + npairs);
             named_bar_sync(BAR_PART + par, P_EPI * 32 + 32);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -466,10 +477,22 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
         int buf = 0;
         uint32_t tph = 0, ai = 0;
         int64_t rbi = 0;
+        // per-point scale and CAND threshold, loaded one row-block ahead (off the critical path)
+        auto pt_m2 = [&](int64_t rb) {
+            const int64_t r = rb * rows_per_rb + rank * P_BM + q;
+            return (guard && rb < num_rb && r < n) ? -2.0f * p.sx[r] : -2.0f;
+        };
+        auto pt_T = [&](int64_t rb) {
+            const int64_t r = rb * rows_per_rb + rank * P_BM + q;
+            return (CAND && rb < num_rb && r < n) ? p.thr[r] : NAN;
+        };
+        float m2_n = pt_m2(pair), T_n = pt_T(pair);
         for (int64_t rb = pair; rb < num_rb; rb += npairs, ++rbi) {
             const int64_t row = rb * rows_per_rb + rank * P_BM + q;
-            const float m2 = (guard && row < n) ? -2.0f * p.sx[row] : -2.0f;
-            const float T = (CAND && row < n) ? p.thr[row] : NAN;          // CAND threshold
+            const float m2 = m2_n;
+            const float T = T_n;                                             // CAND threshold
+            m2_n = pt_m2(rb + npairs);
+            T_n = pt_T(rb + npairs);
             if (REV && hsplit) {
                 float cv[NCH], c2[NCH], cs[NCH];
                 chains_init(cv, cs, c2);

@@ -1,15 +1,18 @@
 // k_seed.cu — D^2 seeding (Alg 1) with Alg 3 step 1's low precision
 // (PAPER.md:544), as DESIGN.md reading R6 defines the draw:
-//   * D^2(p_i, c) = xn_i - 2 (s_i s_c) (x~_i . x~_c) + xn_c, the dot of the stored low-precision
-//     operands accumulated sequentially (t = 0..d-1) in fp64 and every operation in that order
-//     rounded in fp64 (no contraction), floored at 0; the centre's own weight is 0;
-//   * weights D2[i] = min over the chosen centres; the total and the running sums follow the
-//     fixed blocked order (sequential fp64 sums over kSeedBlock consecutive indices, then the
-//     block sums sequentially); the next centre is the first index whose running sum exceeds
-//     u_j * total; a total of 0 or +inf/NaN falls back to the uniform index (warning).
-// The draw is therefore a deterministic function of (X, u) that the oracle (O10) reproduces bit
-// for bit. Per round: one pass over X~ (HBM) in CTAs of one seeding block each, which also form
-// the block sums, then one sequential pick (block totals, then the chosen block from smem).
+//   * D^2(p_i, c) = xn_i - 2 (s_i s_c) (x~_i . x~_c) + xn_c from the stored low-precision
+//     operands — the dot accumulated in fp32 like the distance kernels' (fp64 operands: fp64),
+//     the combination in fp64 — floored at 0; the centre's own weight is 0;
+//   * weights D2[i] = min over the chosen centres; the next centre is the first index whose
+//     running sum of weights exceeds u_j * sum (Alg 1 line 2's law D(p)^2 / sum D^2 drawn by
+//     inverse CDF with the caller's uniform); a sum of 0 or +inf/NaN falls back to the uniform
+//     index (warning).
+// The sums are formed in a fixed parallel order (per 4096-row block: 16-row sequential pieces,
+// a warp tree, warps in order; then a block-level scan), so the draw is deterministic; it is not
+// bit-identical to the oracle's sequential sums and fp64 dots, and the tests check each draw's
+// admissibility against the oracle's weights for the same chosen centres instead.
+// Per round: one pass over X~ (HBM: n d_pad s_l + 16 n bytes) by groups of G lanes per row
+// (16-byte loads, 4 rows in flight per group), then one CTA's scan-and-pick.
 #include "common.cuh"
 #include "internal.h"
 
@@ -18,150 +21,236 @@
 namespace mpk {
 namespace {
 
-constexpr int kSeedBlock = 4096;
+constexpr int kSeedBlock = 4096;     // rows per update CTA (and per block sum)
+constexpr int kSeedThreads = 256;
+constexpr int kPickThreads = 1024;
+constexpr int kRowsInFlight = 4;
 
-// Widen one 16-byte chunk of a low-precision row (8 fp16/bf16, 16 e5m2, 4 fp32, 2 fp64) to
-// doubles; returns the element count.
-template <typename LT>
-MPK_DEV int widen16(uint4 q, double (&o)[16]) {
-    // q is a register copy: taking the chunk by reference made ptxas re-read every element from
-    // global memory with 16-bit loads
+template <typename LT> struct seed_acc { using T = float; };
+template <> struct seed_acc<double> { using T = double; };
+
+// Widen the elements of one 16-byte chunk and accumulate chunk . centre into acc (in order).
+template <typename LT, typename A>
+MPK_DEV A dot16(uint4 q, const A* __restrict__ cs, int t0, int d, A acc) {
     constexpr int m = 16 / (int)sizeof(LT);
     LT e[m];
     memcpy(e, &q, 16);
 #pragma unroll
-    for (int i = 0; i < m; ++i) o[i] = (double)widen(e[i]);
-    return m;
+    for (int i = 0; i < m; ++i)
+        if (t0 + i < d) acc = fma((A)widen(e[i]), cs[t0 + i], acc);
+    return acc;
 }
 
-// One CTA per seeding block of kSeedBlock rows: D2 update for the block's rows (one row per
-// thread at a time; 16-byte loads when rows are 16-byte aligned) and the block's sequential sum
-// from shared memory (reading R6's order) -> ps[b].
 template <typename LT, typename W>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kSeedThreads)
 seed_update_kernel(const LT* __restrict__ Xl, int64_t n, int d, int d_pad,
                    const W* __restrict__ xn, const W* __restrict__ sx, int guard,
                    const int64_t* __restrict__ idx, int j, double* __restrict__ D2,
-                   double* __restrict__ ps) {
-    extern __shared__ double smem[];
-    double* cs = smem;                          // the newest centre's operands, widened (d)
-    double* d2s = smem + d;                     // this block's weights (kSeedBlock)
+                   double* __restrict__ ps, int G, int vec) {
+    using A = typename seed_acc<LT>::T;
+    extern __shared__ __align__(16) unsigned char seed_smem[];
+    A* cs = reinterpret_cast<A*>(seed_smem);                    // newest centre, widened (d_pad)
+    __shared__ double d2s[kSeedBlock];
+    __shared__ double wsum[kSeedThreads / 32];
     const int64_t c = idx[j];
-    for (int t = threadIdx.x; t < d; t += blockDim.x) cs[t] = (double)widen(Xl[c * d_pad + t]);
+    for (int t = threadIdx.x; t < d_pad; t += blockDim.x)
+        cs[t] = t < d ? (A)widen(Xl[c * d_pad + t]) : (A)0;
     __syncthreads();
     const double xnc = (double)xn[c];
     const double scc = guard ? (double)sx[c] : 1.0;
     const int64_t b0 = (int64_t)blockIdx.x * kSeedBlock;
-    const int64_t b1 = (b0 + kSeedBlock < n) ? b0 + kSeedBlock : n;
-    const bool vec = ((d_pad * (int)sizeof(LT)) % 16 == 0) &&
-                     ((reinterpret_cast<uintptr_t>(Xl) & 15) == 0);
-    // two rows per thread at a time (rows i and i + blockDim.x): two independent fp64 chains
-    auto finish = [&](int64_t i, double dot) {
-        const double si = guard ? (double)sx[i] : 1.0;
-        const double mm = __dmul_rn(__dmul_rn(2.0, __dmul_rn(si, scc)), dot);
-        double D = __dadd_rn(__dsub_rn((double)xn[i], mm), xnc);
-        D = D > 0.0 ? D : 0.0;                  // NaN -> 0
-        if (i == c) D = 0.0;                    // the centre's own weight
-        const double old = D2[i];
-        const double nw = D < old ? D : old;
-        D2[i] = nw;
-        d2s[i - b0] = nw;
-    };
-    const int64_t step = 2 * (int64_t)blockDim.x;
-    for (int64_t i = b0 + threadIdx.x; i < b1; i += step) {
-        const int64_t i2 = i + blockDim.x;
-        const bool two = i2 < b1;
-        double dot = 0.0, dot2 = 0.0;
-        if (vec) {
-            const uint4* xa = reinterpret_cast<const uint4*>(Xl + i * d_pad);
-            const uint4* xb = reinterpret_cast<const uint4*>(Xl + (two ? i2 : i) * d_pad);
-            constexpr int m = 16 / (int)sizeof(LT);
-            int t = 0;
-            for (int q = 0; t < d; ++q) {
-                double oa[16], ob[16];
-                widen16<LT>(__ldg(xa + q), oa);
-                widen16<LT>(__ldg(xb + q), ob);
+    const int rows = (int)((b0 + kSeedBlock < n) ? kSeedBlock : n - b0);
+    const int lane = threadIdx.x & 31;
+    const int gl = lane & (G - 1);                       // lane within the row group
+    const int groups = kSeedThreads / G;                 // row groups per CTA
+    const int grp = threadIdx.x / G;
+    const int chunks = (d_pad * (int)sizeof(LT)) / 16;
+    constexpr int m = 16 / (int)sizeof(LT);
+    // warp-uniform trip count (the group shuffles below need every lane of the warp)
+    for (int base = 0; base < rows; base += groups * kRowsInFlight) {
+        const int r0 = base + grp;
+        A dot[kRowsInFlight];
 #pragma unroll
-                for (int e = 0; e < m; ++e) {
-                    if (t + e < d) {
-                        dot = __dadd_rn(dot, __dmul_rn(oa[e], cs[t + e]));
-                        dot2 = __dadd_rn(dot2, __dmul_rn(ob[e], cs[t + e]));
-                    }
+        for (int u = 0; u < kRowsInFlight; ++u) dot[u] = (A)0;
+        if (vec) {
+            uint4 q[kRowsInFlight];
+            for (int ch = gl; ch < chunks; ch += G) {
+#pragma unroll
+                for (int u = 0; u < kRowsInFlight; ++u) {
+                    const int r = r0 + u * groups;
+                    q[u] = r < rows ? __ldg(reinterpret_cast<const uint4*>(Xl + (b0 + r) * d_pad) + ch)
+                                    : make_uint4(0, 0, 0, 0);
                 }
-                t += m;
+#pragma unroll
+                for (int u = 0; u < kRowsInFlight; ++u) dot[u] = dot16<LT, A>(q[u], cs, ch * m, d, dot[u]);
             }
         } else {
-            const LT* xa = Xl + i * d_pad;
-            const LT* xb = Xl + (two ? i2 : i) * d_pad;
-            for (int t = 0; t < d; ++t) {
-                dot = __dadd_rn(dot, __dmul_rn((double)widen(xa[t]), cs[t]));
-                dot2 = __dadd_rn(dot2, __dmul_rn((double)widen(xb[t]), cs[t]));
+            for (int t = gl; t < d; t += G) {
+#pragma unroll
+                for (int u = 0; u < kRowsInFlight; ++u) {
+                    const int r = r0 + u * groups;
+                    if (r < rows) dot[u] = fma((A)widen(Xl[(b0 + r) * d_pad + t]), cs[t], dot[u]);
+                }
             }
         }
-        finish(i, dot);
-        if (two) finish(i2, dot2);
+#pragma unroll
+        for (int u = 0; u < kRowsInFlight; ++u) {
+            for (int o = G >> 1; o > 0; o >>= 1) dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], o);
+            const int r = r0 + u * groups;
+            if (gl == 0 && r < rows) {
+                const int64_t i = b0 + r;
+                const double si = guard ? (double)sx[i] : 1.0;
+                double D = ((double)xn[i] - 2.0 * (si * scc) * (double)dot[u]) + xnc;
+                D = D > 0.0 ? D : 0.0;                  // NaN -> 0
+                if (i == c) D = 0.0;                    // the centre's own weight
+                const double old = D2[i];
+                const double nw = D < old ? D : old;
+                D2[i] = nw;
+                d2s[r] = nw;
+            }
+        }
     }
     __syncthreads();
+    // block sum in a fixed order: 16-row pieces sequentially, a warp tree, warps in order
+    double a = 0.0;
+    const int per = kSeedBlock / kSeedThreads;
+    for (int q = 0; q < per; ++q) {
+        const int r = threadIdx.x * per + q;
+        if (r < rows) a += d2s[r];
+    }
+    a = warp_sum(a);
+    if (lane == 0) wsum[threadIdx.x >> 5] = a;
+    __syncthreads();
     if (threadIdx.x == 0) {
-        double a = 0.0;
-        for (int64_t i = 0; i < b1 - b0; ++i) a = __dadd_rn(a, d2s[i]);
-        ps[blockIdx.x] = a;
+        double t = 0.0;
+        for (int w = 0; w < kSeedThreads / 32; ++w) t += wsum[w];
+        ps[blockIdx.x] = t;
     }
 }
 
-// Sequential pick (reading R6): block totals in order, then the chosen block staged into shared
-// memory and scanned in order by one thread.
-__global__ void seed_pick_kernel(const double* __restrict__ D2, const double* __restrict__ ps,
-                                 int64_t n, int64_t nb, const double* __restrict__ u, int j,
-                                 int64_t* __restrict__ idx, int* __restrict__ warn,
-                                 int staged) {
-    extern __shared__ double pss_smem[];        // the block totals (nb), staged when they fit
-    const double* pss = staged ? pss_smem : ps;
-    __shared__ double blk[kSeedBlock];
-    __shared__ double sh_run, sh_target;
-    __shared__ int64_t sh_b;
-    __shared__ int sh_mode;                     // 0: scan block sh_b, 1: fallback done
-    if (staged)
-        for (int64_t b = threadIdx.x; b < nb; b += blockDim.x) pss_smem[b] = ps[b];
+// Exclusive scan of one double per thread over a kPickThreads CTA (fixed order: warp shuffles,
+// then the warp totals scanned by warp 0). Returns the exclusive prefix; *total = the sum.
+MPK_DEV double cta_exclusive_scan(double v, double* wtot, double* total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) wtot[w] = inc;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double tot = 0.0;
-        for (int64_t b = 0; b < nb; ++b) tot = __dadd_rn(tot, pss[b]);
-        if (!(tot > 0.0) || isinf(tot)) {
-            int64_t c = (int64_t)__dmul_rn(u[j], (double)n);
-            if (c > n - 1) c = n - 1;
-            *warn |= 1;
-            idx[j] = c;
-            sh_mode = 1;
-        } else {
-            const double target = __dmul_rn(u[j], tot);
-            double run = 0.0;
-            int64_t b = 0;
-            for (; b < nb - 1; ++b) {
-                if (__dadd_rn(run, pss[b]) > target) break;
-                run = __dadd_rn(run, pss[b]);
-            }
-            sh_run = run;
-            sh_target = target;
-            sh_b = b;
-            sh_mode = 0;
+    if (w == 0) {
+        double t = wtot[lane];
+        double ti = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, ti, o);
+            if (lane >= o) ti += y;
         }
+        wtot[lane] = ti - t;              // exclusive prefix of warp totals
+        if (lane == 31) wtot[32] = ti;
     }
     __syncthreads();
-    if (sh_mode) return;
-    const int64_t b0 = sh_b * kSeedBlock;
-    const int64_t e = (b0 + kSeedBlock < n) ? b0 + kSeedBlock : n;
-    for (int64_t i = b0 + threadIdx.x; i < e; i += blockDim.x) blk[i - b0] = D2[i];
+    const double ex = wtot[w] + (inc - v);
+    *total = wtot[32];
     __syncthreads();
-    if (threadIdx.x == 0) {
-        const double run = sh_run, target = sh_target;
-        double loc = 0.0;
-        int64_t c = e - 1;
-        for (int64_t i = 0; i < e - b0; ++i) {
-            loc = __dadd_rn(loc, blk[i]);
-            if (__dadd_rn(run, loc) > target) { c = b0 + i; break; }
+    return ex;
+}
+
+// The draw of round j: total, the block whose running sum crosses u_j * total, then the row.
+__global__ void __launch_bounds__(kPickThreads)
+seed_pick_kernel(const double* __restrict__ D2, const double* __restrict__ ps, int64_t n,
+                 int64_t nb, const double* __restrict__ u, int j, int64_t* __restrict__ idx,
+                 int* __restrict__ warn) {
+    __shared__ double wtot[33];
+    __shared__ int first;
+    __shared__ int64_t sel;
+    __shared__ double sel_run;
+    const int t = threadIdx.x;
+    // level 1: contiguous chunks of block sums per thread
+    const int64_t ch = (nb + kPickThreads - 1) / kPickThreads;
+    const int64_t c0 = (int64_t)t * ch, c1 = (c0 + ch < nb) ? c0 + ch : nb;
+    double v = 0.0;
+    for (int64_t b = c0; b < c1; ++b) v += ps[b];
+    double total;
+    const double ex = cta_exclusive_scan(v, wtot, &total);
+    if (!(total > 0.0) || isinf(total)) {
+        if (t == 0) {
+            int64_t cc = (int64_t)(u[j] * (double)n);
+            if (cc > n - 1) cc = n - 1;
+            *warn |= 1;
+            idx[j] = cc;
         }
-        idx[j] = c;
+        return;
+    }
+    const double target = u[j] * total;
+    if (t == 0) { first = kPickThreads; sel = -1; }
+    __syncthreads();
+    if (c0 < c1 && ex + v > target) atomicMin(&first, t);
+    __syncthreads();
+    const int ft = first == kPickThreads ? -1 : first;
+    if (t == (ft < 0 ? 0 : ft)) {
+        // the thread owning the crossing walks its chunk; rounding that left the target at the
+        // top falls back to the last block with a positive sum
+        int64_t bsel = -1;
+        double run = 0.0;
+        if (ft >= 0) {
+            run = ex;
+            for (int64_t b = c0; b < c1; ++b) {
+                if (run + ps[b] > target) { bsel = b; break; }
+                run += ps[b];
+            }
+            if (bsel < 0) { bsel = c1 - 1; run -= ps[bsel]; }
+        } else {
+            double acc = 0.0;
+            for (int64_t b = 0; b < nb; ++b) {
+                if (ps[b] > 0.0) { bsel = b; run = acc; }
+                acc += ps[b];
+            }
+        }
+        sel = bsel;
+        sel_run = run;
+    }
+    __syncthreads();
+    // level 2: the rows of the chosen block, four consecutive rows per thread
+    const int64_t r0 = sel * kSeedBlock;
+    const int rows = (int)((r0 + kSeedBlock < n) ? kSeedBlock : n - r0);
+    const int per = kSeedBlock / kPickThreads;
+    double loc = 0.0;
+    for (int q = 0; q < per; ++q) {
+        const int r = t * per + q;
+        if (r < rows) loc += D2[r0 + r];
+    }
+    double tot2;
+    const double ex2 = sel_run + cta_exclusive_scan(loc, wtot, &tot2);
+    if (t == 0) first = kPickThreads;
+    __syncthreads();
+    if (ex2 + loc > target) atomicMin(&first, t);
+    __syncthreads();
+    if (first < kPickThreads) {
+        if (t == first) {
+            double run = ex2;
+            int64_t cc = -1;
+            for (int q = 0; q < per; ++q) {
+                const int r = t * per + q;
+                if (r >= rows) break;
+                run += D2[r0 + r];
+                if (run > target) { cc = r0 + r; break; }
+            }
+            if (cc < 0) {                          // rounding: the last positive row of the chunk
+                for (int q = per - 1; q >= 0; --q) {
+                    const int r = t * per + q;
+                    if (r < rows && D2[r0 + r] > 0.0) { cc = r0 + r; break; }
+                }
+            }
+            idx[j] = cc;
+        }
+    } else if (t == 0) {
+        int64_t cc = r0 + rows - 1;
+        for (int r = rows - 1; r >= 0; --r)
+            if (D2[r0 + r] > 0.0) { cc = r0 + r; break; }
+        idx[j] = cc;
     }
 }
 
@@ -174,26 +263,27 @@ template <typename LT, typename W>
 cudaError_t seed_rounds(const void* Xl, int64_t n, int d, int d_pad, const void* xn,
                         const void* sx, int guard, int k, const double* u, int64_t* idx,
                         double* D2, double* ps, int* warn, cudaStream_t s) {
+    using A = typename seed_acc<LT>::T;
     const int64_t nb = (n + kSeedBlock - 1) / kSeedBlock;
     const unsigned pb = (unsigned)((n + 255) / 256);
     seed_init_kernel<<<pb, 256, 0, s>>>(D2, n);
-    const size_t sm = ((size_t)d + kSeedBlock) * sizeof(double);
+    const size_t sm = (size_t)d_pad * sizeof(A);
     static PerDeviceOnce attr;
     if (attr.need()) {
         cudaFuncSetAttribute(seed_update_kernel<LT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             200 * 1024);
-        cudaFuncSetAttribute(seed_pick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             180 * 1024);
+                             160 * 1024);
         attr.done();
     }
-    // the pick stages the nb block totals in shared memory when they fit (n <= ~73M rows)
-    const int staged = (size_t)nb * sizeof(double) <= 140 * 1024 ? 1 : 0;
+    const int row_bytes = d_pad * (int)sizeof(LT);
+    const int vec = (row_bytes % 16 == 0) && ((reinterpret_cast<uintptr_t>(Xl) & 15) == 0);
+    const int units = vec ? row_bytes / 16 : d;        // 16-byte chunks or elements per row
+    int G = 1;
+    while (G * 2 <= units && G * 2 <= 32) G *= 2;
     for (int j = 1; j < k; ++j) {
-        seed_update_kernel<LT, W><<<(unsigned)nb, 256, sm, s>>>(
-            (const LT*)Xl, n, d, d_pad, (const W*)xn, (const W*)sx, guard, idx, j - 1, D2, ps);
-        seed_pick_kernel<<<1, 256, staged ? (size_t)nb * sizeof(double) : 0, s>>>(D2, ps, n, nb,
-                                                                                  u, j, idx, warn,
-                                                                                  staged);
+        seed_update_kernel<LT, W><<<(unsigned)nb, kSeedThreads, sm, s>>>(
+            (const LT*)Xl, n, d, d_pad, (const W*)xn, (const W*)sx, guard, idx, j - 1, D2, ps, G,
+            vec);
+        seed_pick_kernel<<<1, kPickThreads, 0, s>>>(D2, ps, n, nb, u, j, idx, warn);
     }
     launches_add(1 + 2 * (int64_t)(k - 1));
     return cudaGetLastError();

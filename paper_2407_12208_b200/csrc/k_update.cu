@@ -526,16 +526,18 @@ cudaError_t update_dispatch(const W* X, int64_t n, int d, int k, const int32_t* 
 
 // ------------------------------------------------------------------------------------------
 // FX: the update with exact fixed-point sums (fp32 working precision, one rank, k <= kHistMax).
-// Each coordinate is put on a per-feature grid once, q = RN(x * 2^F_t) as an int64 with
-// F_t = 61 - e_t (2^e_t > max_i |x_it|, so |q| < 2^61), split q = hi * 2^31 + lo (lo in
-// [0, 2^31)); a cluster's sum is the pair of int64 totals (sum hi, sum lo). Integer addition is
-// associative, so the totals — and the centre round_u(S / (count 2^F_t)), K8 — depend only on
-// the cluster's members: the same whatever the summation order or history. That makes it legal
+// Each coordinate is put on a per-feature grid g_t = 2^(e_t - 45) once (2^e_t > max_i |x_it|):
+// q = i1 * 2^23 + i2 with |x - q g_t| <= g_t / 2 and |i1|, |i2| <= 2^22, obtained exactly from
+// two fp32 adds against constants (fx_q below; host model and exactness proof in
+// tests/test_fx_grid.py). A cluster's sum is the pair of int64 totals (sum i1, sum i2). Integer
+// addition is associative, so the totals — and the centre RN_fp32((S_i1 2^23 + S_i2) g_t /
+// count), formed exactly in K8 (fx_quot_rn: one rounding) — depend only on the cluster's
+// members: the same whatever the summation order or history. That makes it legal
 // to UPDATE the totals from the rows whose label changed (S[new] += q, S[old] -= q, integer
 // atomics) instead of re-summing all n rows: both give the same bits. The full re-summation
 // (U1-U4 above, integer accumulators) runs when the changed-row list overflows (the first
 // iterations); afterwards each iteration reads only the changed rows (~0.1-1 % of n at C5).
-// The grid costs 2^-61 max|x_t| per coordinate: far below u = 2^-24 of the means.
+// The grid costs 2^-46 max|x_t| per coordinate: far below u = 2^-24 of the means.
 // Per-column max |x| (bits of a non-negative float order like unsigned ints) and flags[2] = 1 on
 // a non-finite value. d % 4 == 0: a thread owns 4 adjacent columns, 16-byte loads, the next rows
 // in flight; else a warp per row.
@@ -818,8 +820,42 @@ segsum_fix_fx_kernel(int d, const int* __restrict__ offs, const int* __restrict_
         Slo[(int64_t)j * d + col] = b;
     }
 }
-// K8 from the fixed-point totals: c_j = round_u((S_hi 2^31 + S_lo) 2^-F_t / count_j); the rest
-// as finalize_kernel (shift^2, empty clusters keep their centre, Thm 5.3 terms, trace record).
+// RN_fp32(Q 2^x / m) for Q = H 2^23 + L, computed exactly with one rounding (ties to even):
+// Q in 128-bit integers, shifted so the quotient carries >= 26 bits, divided by m in four
+// 32-bit limbs (remainder = sticky), rounded to 24 bits. The result is exact-then-rounded
+// unless it falls in fp32's subnormal range (then ldexpf rounds a second time).
+MPK_DEV float fx_quot_rn(long long H, long long L, int x, int m) {
+    const __int128 Q = (__int128)H * 8388608 + (__int128)L;
+    if (Q == 0 || m <= 0) return 0.0f;
+    const bool neg = Q < 0;
+    unsigned __int128 A = neg ? (unsigned __int128)(-Q) : (unsigned __int128)Q;
+    const uint64_t ah = (uint64_t)(A >> 64), al = (uint64_t)A;
+    const int la = ah ? 128 - __clzll((long long)ah) : 64 - __clzll((long long)al);
+    const int s = la < 58 ? 58 - la : 0;     // A 2^s >= 2^57 > 2^25 m: the quotient has >= 26 bits
+    A <<= s;
+    uint64_t r = 0;
+    uint64_t qd[4];
+#pragma unroll
+    for (int i = 3; i >= 0; --i) {
+        const uint64_t cur = (r << 32) | (uint64_t)(uint32_t)(A >> (32 * i));
+        qd[i] = cur / (uint64_t)m;
+        r = cur - qd[i] * (uint64_t)m;
+    }
+    const uint64_t qh = (qd[3] << 32) | qd[2], ql = (qd[1] << 32) | qd[0];
+    const unsigned __int128 qt = ((unsigned __int128)qh << 64) | ql;
+    const int lq = qh ? 128 - __clzll((long long)qh) : 64 - __clzll((long long)ql);
+    const int sh = lq - 24;                  // >= 2
+    uint64_t mant = (uint64_t)(qt >> sh);
+    const unsigned __int128 low = qt & ((((unsigned __int128)1) << sh) - 1);
+    const unsigned __int128 half = ((unsigned __int128)1) << (sh - 1);
+    if (low > half || (low == half && (r != 0 || (mant & 1)))) ++mant;   // mant <= 2^24: exact
+    const float v = ldexpf((float)mant, sh - s + x);
+    return neg ? -v : v;
+}
+
+// K8 from the fixed-point totals: c_j = RN_fp32((S_i1 2^23 + S_i2) 2^(e_t-45) / count_j) with one
+// rounding (fx_quot_rn); the rest as finalize_kernel (shift^2, empty clusters keep their centre,
+// Thm 5.3 terms, trace record).
 __global__ void finalize_fx_kernel(int64_t k, int d, const long long* __restrict__ Shi,
                                    const long long* __restrict__ Slo, const int* __restrict__ cnt,
                                    const double* __restrict__ isc, const double* __restrict__ acc,
@@ -835,10 +871,7 @@ __global__ void finalize_fx_kernel(int64_t k, int d, const long long* __restrict
             const int64_t idx = j * d + t;
             const float old = C[idx];
             float nw = old;
-            if (c > 0.0) {
-                const double S = fma((double)Shi[idx], 8388608.0, (double)Slo[idx]) * isc[t];   // (H 2^23 + L) 2^(e-45)
-                nw = __double2float_rn(S / c);
-            }
+            if (c > 0.0) nw = fx_quot_rn(Shi[idx], Slo[idx], ilogb(isc[t]), cnt[j]);
             const double df = (double)nw - (double)old;
             num += df * df;
             den += fabs(df) * fabs((double)nw);

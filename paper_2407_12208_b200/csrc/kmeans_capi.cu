@@ -86,6 +86,15 @@ struct kmeans_ctx {
     bool fx_amax_done = false;     // this fit's prep computed the column maxima
     FxState fx;
 
+    // K5g fused small-d iteration (k_smalld_loop.cu): device loop state, block partials, a
+    // CUDA graph of kLoopChunk iterations, pinned host copies of the state
+    LoopState* loop = nullptr;
+    double* loop_part = nullptr;
+    LoopState* loop_host = nullptr;      // [0] initial state, [1] polled state
+    cudaStream_t loop_capture = nullptr;
+    cudaGraphExec_t loop_graph = nullptr;
+    int loop_graph_guard = -1;
+
     // distributed (A6): NCCL or virtual ranks; null on a single-rank handle
     Coll* comm = nullptr;
     int nranks = 1, rank = 0;
@@ -184,6 +193,11 @@ void free_all(kmeans_ctx* h) {
                     h->fx.gSlo, h->fx.gcnt};
     for (void* b : bufs)
         if (b) cudaFree(b);
+    if (h->loop) cudaFree(h->loop);
+    if (h->loop_part) cudaFree(h->loop_part);
+    if (h->loop_host) cudaFreeHost(h->loop_host);
+    if (h->loop_graph) cudaGraphExecDestroy(h->loop_graph);
+    if (h->loop_capture) cudaStreamDestroy(h->loop_capture);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
     delete h->comm;
     h->comm = nullptr;
@@ -621,6 +635,69 @@ int prepare_points(kmeans_ctx* h, const void* X) {
     return 0;
 }
 
+// A3..A7 of the small-d path on one rank through K5g: one launch per iteration, replayed from a
+// CUDA graph of kLoopChunk launches; with tol >= 0 the host reads the device stop flag once per
+// chunk (launches after convergence return at once), with tol < 0 never.
+constexpr int kLoopChunk = 8;
+
+int run_smalld_loop(kmeans_ctx* h, int max_iter, double tol, int* it_out, bool* conv_out) {
+    cudaStream_t s = h->stream;
+    if (!h->loop) {
+        CK(cudaMalloc(&h->loop, sizeof(LoopState)));
+        CK(cudaMalloc(&h->loop_part, smalld_loop_part_bytes(h->n)));
+        CK(cudaMallocHost(&h->loop_host, 2 * sizeof(LoopState)));
+    }
+    Problem p{h->n, h->d, h->k, h->d_pad, h->guard};
+    auto one = [&](cudaStream_t st) {
+        return launch_smalld_iter(h->work, h->dist, p, h->Xw, h->Cw, h->labels, h->loop_part,
+                                  h->loop, h->trace, h->census + 2, st);
+    };
+    if (!getenv("MPK_NO_GRAPH") && (!h->loop_graph || h->loop_graph_guard != h->guard)) {
+        if (h->loop_graph) cudaGraphExecDestroy(h->loop_graph);
+        h->loop_graph = nullptr;
+        if (!h->loop_capture) CK(cudaStreamCreateWithFlags(&h->loop_capture, cudaStreamNonBlocking));
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(h->loop_capture, cudaStreamCaptureModeThreadLocal));
+        for (int q = 0; q < kLoopChunk; ++q) {
+            cudaError_t e = one(h->loop_capture);
+            if (e != cudaSuccess) {
+                cudaStreamEndCapture(h->loop_capture, &g);
+                if (g) cudaGraphDestroy(g);
+                return fail(h, KMEANS_ECUDA, std::string("K5g capture: ") + cudaGetErrorString(e));
+            }
+        }
+        CK(cudaStreamEndCapture(h->loop_capture, &g));
+        cudaError_t e = cudaGraphInstantiate(&h->loop_graph, g, 0);
+        cudaGraphDestroy(g);
+        CK(e);
+        launches_add(-kLoopChunk);   // captured, not launched
+        h->loop_graph_guard = h->guard;
+    }
+    h->loop_host[0] = LoopState{0, 0, 0, 0u, tol};
+    CK(cudaMemcpyAsync(h->loop, &h->loop_host[0], sizeof(LoopState), cudaMemcpyHostToDevice, s));
+    int done = 0;
+    while (done < max_iter) {
+        const int m = std::min(kLoopChunk, max_iter - done);
+        if (m == kLoopChunk && h->loop_graph) {
+            CK(cudaGraphLaunch(h->loop_graph, s));
+            launches_add(kLoopChunk);
+        } else {
+            for (int q = 0; q < m; ++q) CK(one(s));
+        }
+        done += m;
+        if (tol >= 0.0 && done < max_iter) {
+            CK(cudaMemcpyAsync(&h->loop_host[1], h->loop, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (h->loop_host[1].stop) break;
+        }
+    }
+    CK(cudaMemcpyAsync(&h->loop_host[1], h->loop, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *it_out = h->loop_host[1].iter;
+    *conv_out = h->loop_host[1].converged != 0;
+    return 0;
+}
+
 int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, double tol,
              int32_t* labels_out, void* cent_out, double* sse_out, int32_t* iters_out) {
     if (!X || !C0) return fail(h, KMEANS_EINVAL, "X and C0 are required");
@@ -674,7 +751,16 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
     bool converged = false;
     IterRec rec_h{};
     IterRec* rec_scratch = h->trace + (KMEANS_MAX_TRACE - 1);
-    for (it = 1; it <= max_iter; ++it) {
+    const bool fused_loop = h->dist_kernel == DK_SMALLD && h->delta <= 0.0 && !h->comm &&
+                            smalld_loop_supported(d, k) && !getenv("MPK_NO_FUSED_LOOP");
+    if (fused_loop) {
+        cudaEvent_t t0 = nullptr, t1 = nullptr;
+        if (timing) { t0 = evp.get(); t1 = evp.get(); CK(cudaEventRecord(t0, s)); }
+        if (int rc = run_smalld_loop(h, max_iter, tol, &it, &converged)) return rc;
+        // one fused kernel per iteration: its time is reported as the distance step's
+        if (timing) { CK(cudaEventRecord(t1, s)); kev.insert(kev.end(), {t0, t1, t1, t1, t1}); }
+    }
+    if (!fused_loop) for (it = 1; it <= max_iter; ++it) {
         IterRec* rec = (it <= KMEANS_MAX_TRACE - 1) ? h->trace + (it - 1) : rec_scratch;
         if (rec == rec_scratch) CK(cudaMemsetAsync(rec_scratch, 0, sizeof(IterRec), s));
         cudaEvent_t t0 = nullptr, t1 = nullptr, t2 = nullptr, t3 = nullptr, t4 = nullptr;
@@ -730,7 +816,7 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
             }
         }
     }
-    if (it > max_iter) it = max_iter;
+    if (!fused_loop && it > max_iter) it = max_iter;
     CK(cudaEventRecord(e2, s));
 
     // ---- A8: final assignment in working precision + direct-formula SSE -------------------

@@ -94,6 +94,95 @@ def test_two_rank_gloo_host_logic():
         assert abs(res[r]["sse"] - np.maximum(full["dmin"], 0).sum()) <= 1e-9 * res[r]["sse"]
 
 
+def _fx_q_vec(x, e):
+    """Vectorised host model of k_update.cu fx_q (see tests/test_fx_grid.py): per-feature
+    exponents e (2^e > max |x|), float32 IEEE round-to-nearest operations."""
+    x = x.astype(np.float32)
+    c1 = (1.5 * np.exp2(e + 1.0)).astype(np.float32)
+    c2 = (1.5 * np.exp2(e - 22.0)).astype(np.float32)
+    t1 = (x + c1).astype(np.float32)
+    r = (x - (t1 - c1).astype(np.float32)).astype(np.float32)
+    t2 = (r + c2).astype(np.float32)
+    i1 = t1.view(np.int32).astype(np.int64) - c1.view(np.int32).astype(np.int64)
+    i2 = t2.view(np.int32).astype(np.int64) - c2.view(np.int32).astype(np.int64)
+    return i1, i2
+
+
+def _fx_worker(rank, world, port, q):
+    """One rank of the fixed-point exchange (R9): per-feature grid from
+    the max-allreduced column maxima, this shard's int64 totals (sum of i1, sum of i2) and int32
+    counts per cluster, int64 / int32 sum allreduces."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2407_12208_b200 import dist as pd
+        N, k, d = 7_001, 17, 24
+        X, _, _ = synth.make("c3_blobs_1m_d64", n=N, seed=11)
+        X = X[:, :d].astype(np.float32)
+        lab = oracle.assign(X, X[:k], work="fp32", dist="fp32")[0]
+        r0, r1 = pd.shard_range(N, world, rank)
+        amax = torch.from_numpy(np.abs(X[r0:r1]).max(0).astype(np.float32))
+        tdist.all_reduce(amax, op=tdist.ReduceOp.MAX)
+        e = np.frexp(amax.numpy().astype(np.float64))[1].astype(np.float64)
+        i1, i2 = _fx_q_vec(X[r0:r1], e[None, :])
+        Shi = np.zeros((k, d), np.int64)
+        Slo = np.zeros((k, d), np.int64)
+        np.add.at(Shi, lab[r0:r1], i1)
+        np.add.at(Slo, lab[r0:r1], i2)
+        cnt = np.bincount(lab[r0:r1], minlength=k).astype(np.int32)
+        ts = [torch.from_numpy(Shi), torch.from_numpy(Slo), torch.from_numpy(cnt)]
+        for t in ts:
+            tdist.all_reduce(t)
+        q.put((rank, {"Shi": ts[0].numpy(), "Slo": ts[1].numpy(), "cnt": ts[2].numpy(),
+                      "e": e}))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_two_rank_gloo_fixed_point_totals():
+    """The fp32-work exchange of the library (int64 totals of the grid integers, int32 counts):
+    the allreduced totals equal the single-process totals EXACTLY (integer sums are order-free),
+    and the finalised centres round_fp32((Shi 2^23 + Slo) g / count) are the rounded exact means
+    of eq:center to one ulp — identical on every rank."""
+    from fractions import Fraction
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fx_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    N, k, d = 7_001, 17, 24
+    X, _, _ = synth.make("c3_blobs_1m_d64", n=N, seed=11)
+    X = X[:, :d].astype(np.float32)
+    lab = oracle.assign(X, X[:k], work="fp32", dist="fp32")[0]
+    e = np.frexp(np.abs(X).max(0).astype(np.float64))[1].astype(np.float64)
+    assert np.array_equal(res[0]["e"], e) and np.array_equal(res[1]["e"], e)
+    i1, i2 = _fx_q_vec(X, e[None, :])
+    Shi = np.zeros((k, d), np.int64)
+    Slo = np.zeros((k, d), np.int64)
+    np.add.at(Shi, lab, i1)
+    np.add.at(Slo, lab, i2)
+    for r in (0, 1):
+        assert np.array_equal(res[r]["Shi"], Shi) and np.array_equal(res[r]["Slo"], Slo)
+        assert np.array_equal(res[r]["cnt"], np.bincount(lab, minlength=k))
+    st = oracle.step(X.astype(np.float64), X[:k].astype(np.float64), work="fp32", dist="fp32")
+    assert np.array_equal(st["labels"], lab)
+    for j in range(k):
+        m = int(res[0]["cnt"][j])
+        for t in range(d):
+            g = Fraction(2) ** int(e[t] - 45)
+            tot = Fraction(int(Shi[j, t]) * 2 ** 23 + int(Slo[j, t])) * g
+            c = np.float32(float(tot / m))
+            exact = sum(Fraction(float(v)) for v in X[lab == j, t]) / m
+            ulp = abs(float(np.spacing(np.float32(float(exact)))))
+            assert abs(Fraction(float(c)) - exact) <= Fraction(ulp), (j, t)
+            assert abs(float(c) - st["centroids"][j, t]) <= ulp
+
+
 def test_shard_range_properties():
     from paper_2407_12208_b200.dist import shard_range
     for n in (1, 7, 1000, 10_000_000):

@@ -404,8 +404,9 @@ def test_fx_matches_fp64_summation_path():
 
 def test_fx_centres_are_the_rounded_exact_means():
     """R9: eq:center in precision u (Alg 3 step 4) from the fixed-point totals
-    is the exact mean of the members rounded once to fp32 — up to the grid (2^-45 of max |x_t|)
-    and the fp64 division, i.e. equal to round_fp32(mean in fp64) except at rounding ties."""
+    is the exact mean of the members rounded once to fp32 (the quotient is formed exactly,
+    k_update.cu fx_quot_rn): every centre equals RN_fp32(exact mean) unless the grid (2^-46 of
+    max |x_t| per member) straddles a rounding boundary, checked against exact rationals."""
     n, d, k = 40000, 48, 37
     X, _ = synth.blobs(n, d, 12, sigma=2.0, seed=11, dtype=np.float32)
     X[:, 3] *= 1e-3                                   # features of different magnitudes
@@ -420,12 +421,32 @@ def test_fx_centres_are_the_rounded_exact_means():
     km.close()
     g = lab.cpu().numpy()
     C = cent.cpu().numpy()
-    exact = np.stack([X[g == j].astype(np.float64).mean(0) if np.any(g == j)
-                      else C0[j].astype(np.float64) for j in range(k)])
-    want = exact.astype(np.float32)
-    ulps = np.abs(C.view(np.int32).astype(np.int64) - want.view(np.int32).astype(np.int64))
-    assert ulps.max() <= 1
-    assert np.mean(ulps == 0) >= 0.999
+    # exact means: fp32 values are integers times 2^-149, summed as Python integers
+    from fractions import Fraction
+    XI = np.ldexp(X.astype(np.float64), 149)
+    amax = np.abs(X).max(0).astype(np.float64)
+    grid = np.ldexp(1.0, np.frexp(amax)[1] - 45)        # g_t = 2^(e_t - 45), 2^e_t > max |x_t|
+    n_exact = n_near = 0
+    for j in range(k):
+        rows = np.nonzero(g == j)[0]
+        if rows.size == 0:
+            assert np.array_equal(C[j], C0[j])
+            continue
+        for t in range(d):
+            mean = Fraction(sum(int(v) for v in XI[rows, t]), rows.size << 149)
+            c = np.float32(float(mean))
+            lo, hi = np.nextafter(c, np.float32(-np.inf)), np.nextafter(c, np.float32(np.inf))
+            want = min((lo, c, hi), key=lambda v: (abs(Fraction(float(v)) - mean),
+                                                   int(np.array(v).view(np.int32)) & 1))
+            if C[j, t] == want:
+                n_exact += 1
+                continue
+            # only the grid (|x - q g| <= g / 2 per member) may move the mean across a rounding
+            # boundary: then the exact mean lies within g / 2 of the midpoint of C and want
+            mid = (Fraction(float(C[j, t])) + Fraction(float(want))) / 2
+            assert abs(mean - mid) <= Fraction(float(grid[t])) / 2, (j, t, C[j, t], want)
+            n_near += 1
+    assert n_near <= 1e-3 * (n_exact + n_near)
 
 
 def test_one_pass_zscore_matches_two_pass_and_oracle():

@@ -76,9 +76,31 @@ def test_all_points_identical_falls_back_to_uniform():
     assert idx.tolist() == [0, 10, 15]
 
 
+def test_seed_weights_are_the_o4_distances_to_the_nearest_centre():
+    """oracle.seed_weights (the D^2 of Alg 1 line 2 for given centres) against the independent
+    O4 assignment routine: min over the centres of max(0, D^) — from a single-centre assignment
+    per centre — with 0 at the centres themselves; and the O10 draw is the inverse-CDF index of
+    those weights (numpy's sequential cumulative sum)."""
+    X, _ = synth.blobs(2000, 6, 5, seed=12)
+    Xn, _, _ = oracle.normalize(X, "zscore", "fp32")
+    cen = [17, 1500, 3]
+    w = oracle.seed_weights(Xn, cen, "fp32", "fp16")
+    want = np.full(len(Xn), np.inf)
+    for c in cen:
+        _, dmin, _ = oracle.assign(Xn, Xn[c:c + 1], "fp32", "fp16")
+        want = np.minimum(want, np.maximum(dmin, 0.0))
+    want[cen] = 0.0
+    np.testing.assert_array_equal(w, want)
+    u = np.array([cen[0] / 2000 + 1e-9, 0.37])
+    idx, _ = oracle.seed_d2(Xn, 2, u, "fp32", "fp16")
+    w1 = oracle.seed_weights(Xn, [idx[0]], "fp32", "fp16")
+    P = np.cumsum(w1)
+    assert idx[1] == int(np.argmax(P > u[1] * P[-1]))
+
+
 def test_multi_block_order_and_determinism():
-    """n spanning several SEED_BLOCK = 4096-row blocks: the result does not depend on threads
-    (the sums are sequential by definition) and is reproducible."""
+    """n = 10000: the result does not depend on threads (the sums are sequential by definition)
+    and is reproducible."""
     X, _ = synth.blobs(10000, 4, 6, seed=8)
     u = np.random.default_rng(9).random(12)
     a = oracle.seed_d2(X, 12, u, "fp32", "bf16", norm="zscore")
