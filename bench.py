@@ -372,11 +372,20 @@ def main():
 
     # ---- roofline of the dominant kernel (distance + argmin) ------------------------------
     peaks, peak_src = load_peaks()
-    kern = st["dist_kernel"] if args.delta is None else "mixed_cuda_core"
+    kern = st["dist_kernel"]
+    if args.delta is not None:
+        # Alg 4 / Alg 5: on tcgen05 the certified filter + candidate evaluation (R10);
+        # otherwise the CUDA-core kernel K6m-b
+        kern = "tcgen05_mixed" if kern == "tcgen05" else "mixed_cuda_core"
     t_launch_ms = t_dist / (args.steps * args.iters)
     flops = 2.0 * n_local * k * d       # one dot product per pair (low or working precision)
     f8 = fp8_peak() if dist == "e5m2" else None
-    if kern == "tcgen05" and f8:
+    if kern == "tcgen05_mixed":
+        peak = peaks["bf16_tflops"]
+        bound = "tensor"
+        peak_note = (f"{peak_src} bf16 burst (fp16/bf16 filter operands); achieved = 2nkd per "
+                     "iteration over the whole Alg 4 step (filter, candidates, trigger counts)")
+    elif kern == "tcgen05" and f8:
         # the measured cuBLASLt FP8 GEMM peak (profiles/fp8_peak.json); every 8-bit format runs
         # at the same kind::f8f6f4 rate
         peak = f8["fp8_e4m3xe4m3_tflops"]
@@ -387,18 +396,32 @@ def main():
         peak = peaks["bf16_tflops"] * ratio
         bound = "tensor"
         peak_note = f"{peak_src} bf16 burst x {ratio} ({dist})"
+    elif kern == "smalld_fused":
+        # the fused small-d iteration (K5g) streams X once: bound by memory, judged in GB/s
+        peak = peaks["hbm_gbs"]
+        bound = "hbm"
+        peak_note = f"{peak_src} HBM copy bandwidth"
     else:
         # CUDA-core FP32 FMA: 148 SMs x 128 lanes x 2 flop x max clock
         peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
         bound = "alu"
         peak_note = "derived: 148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz"
-    achieved = flops / (t_launch_ms / 1e3) / 1e12 if t_launch_ms > 0 else None
+    if bound == "hbm":
+        wsz = 4 if cfg.work == "fp32" else 8
+        bytes_it = n_local * (d * wsz + 8)       # X read once, labels read + written
+        achieved = bytes_it / (t_launch_ms / 1e3) / 1e9 if t_launch_ms > 0 else None
+        unit, alg = "GB/s", f"n*(d*s_w + 8) = {bytes_it:.4e} B per iteration"
+    else:
+        achieved = flops / (t_launch_ms / 1e3) / 1e12 if t_launch_ms > 0 else None
+        unit, alg = "TFLOP/s", f"2*n*k*d = {flops:.4e} flop"
     roof = {"kernel": f"assign_{kern}", "bound": bound, "achieved": achieved, "peak": peak,
-            "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
+            "unit": unit, "frac": (achieved / peak) if achieved else None,
             "traffic": traffic_from_profiles(args.config, dist), "peak_source": peak_note,
-            "algorithmic_per_launch": f"2*n*k*d = {flops:.4e} flop",
+            "algorithmic_per_launch": alg,
             "avg_launch_ms": t_launch_ms,
             "share_of_step": (t_dist / ms) if ms > 0 else None}
+    if bound == "hbm" and n_local * d * 4 < 126e6:
+        roof["note"] = "X fits in L2 (126 MB): the per-iteration reads after the first are L2 hits"
     if kern == "tcgen05" and achieved:
         # second denominator: the sustained (power-capped, seconds-long) GEMM peak
         sus = peaks.get("bf16_tflops_sustained")

@@ -61,8 +61,14 @@ enum kmeans_flags {
     /* Alg 4 lines 1-5: every point and centroid is divided by its own
        infinity norm (zero vector -> 1) in precision u before rounding to u_l, and the dot
        product is rescaled by s_i * s_j (Alg 4 line 6). Applied to all pairs (delta = 1). */
-    KMEANS_FORCE_SIMT = 0x200
+    KMEANS_FORCE_SIMT = 0x200,
     /* Debug/parity: use the CUDA-core distance kernel even where the tcgen05 kernel applies. */
+    KMEANS_GUARD_POW2 = 0x400
+    /* Alg 4's scaling with s = 2^ceil(log2 ||x||_inf) (reading Z9 B; implies GUARD_SCALE): the
+       division by s is exact, so x~ = round_l(x / s) differs from round_l(x) only where x / s
+       is kept out of the low format's subnormal / overflow range. With the row as one block it
+       is an MX (OCP microscaling, UE8M0) block scale; the remedy the survey proposed for the
+       paper's q52 failures. */
 };
 
 enum kmeans_status {

@@ -75,9 +75,17 @@ def _prec(p) -> int:
     return PREC[p] if isinstance(p, str) else int(p)
 
 
+GUARD_POW2 = 0x400
+
+
+def _guard(guard) -> int:
+    """False -> 0; True -> 1 (s = ||x||_inf, reading Z9 A); "pow2" -> 2 (Z9 B)."""
+    return 2 if guard == "pow2" else (1 if guard else 0)
+
+
 def _flags(norm="none", guard=False) -> int:
     f = NORM[norm] if isinstance(norm, str) else int(norm)
-    return f | (GUARD if guard else 0)
+    return f | (GUARD if guard else 0) | (GUARD_POW2 if guard == "pow2" else 0)
 
 
 def num_threads() -> int:
@@ -167,7 +175,7 @@ def step(X, C, work="fp32", dist="fp16", guard=False, delta=None):
     counts = np.empty(k, np.int64)
     cnext = np.empty((k, d))
     n_low = ct.c_int64()
-    rc = lib.oracle_step(n, d, k, _prec(work), _prec(dist), int(guard), _p(X), _p(Cc),
+    rc = lib.oracle_step(n, d, k, _prec(work), _prec(dist), _guard(guard), _p(X), _p(Cc),
                          _p(labels), _p(dmin), _p(d2), _p(sums), _p(counts), _p(cnext),
                          float(delta or 0.0), ct.byref(n_low))
     if rc != 0:
@@ -185,7 +193,7 @@ def assign(X, C, work="fp32", dist="fp16", guard=False, delta=None, return_n_low
     labels = np.empty(n, np.int32)
     dmin, d2 = np.empty(n), np.empty(n)
     n_low = ct.c_int64()
-    rc = lib.oracle_assign(n, d, Cc.shape[0], _prec(work), _prec(dist), int(guard), _p(X),
+    rc = lib.oracle_assign(n, d, Cc.shape[0], _prec(work), _prec(dist), _guard(guard), _p(X),
                            _p(Cc), _p(labels), _p(dmin), _p(d2), float(delta or 0.0),
                            ct.byref(n_low))
     if rc != 0:
@@ -201,7 +209,7 @@ def prep(X, work="fp32", dist="fp16", guard=False):
     X = _f64(X)
     n, d = X.shape
     xl, nrm, sc = np.empty_like(X), np.empty(n), np.empty(n)
-    lib.oracle_prep(n, d, _prec(work), _prec(dist), int(guard), _p(X), _p(xl), _p(nrm), _p(sc))
+    lib.oracle_prep(n, d, _prec(work), _prec(dist), _guard(guard), _p(X), _p(xl), _p(nrm), _p(sc))
     return xl, nrm, sc
 
 

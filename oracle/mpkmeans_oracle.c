@@ -44,7 +44,8 @@
 
 /* precision ids (same numbering as the public C-ABI enums, restated here, not shared) */
 enum { OFMT_FP64 = 0, OFMT_FP32 = 1, OFMT_FP16 = 2, OFMT_BF16 = 3, OFMT_E5M2 = 4 };
-enum { ONORM_NONE = 0, ONORM_MINMAX = 1, ONORM_ZSCORE = 2, ONORM_MASK = 0xff, OGUARD = 0x100 };
+enum { ONORM_NONE = 0, ONORM_MINMAX = 1, ONORM_ZSCORE = 2, ONORM_MASK = 0xff, OGUARD = 0x100,
+       OGUARD_POW2 = 0x400 };
 
 /* ---------------------------------------------------------------------------------------- */
 /* O0: formats. Table 1: t = significand digits incl. implicit bit,          */
@@ -145,6 +146,7 @@ void oracle_normalize_apply(int work, int64_t rows, int d, const double* shift,
 /* O2 / O3: norms, guard scale and low-precision operand of one vector.                     */
 /*   norm = p^T p, fp64 sequential sum, stored in precision u.            */
 /*   guard: s = ||p||_inf (Alg 4 lines 1-2; zero vector -> 1, reading Z10), */
+/*          or (guard 2, reading Z9 B) the smallest power of two >= ||p||_inf,                 */
 /*          p~ = round_l(round_u(p / s)) (Alg 4 lines 4-5 in precision u, then the operand of */
 /*          the low-precision dot, line 6).                                                  */
 /*   no guard: s = 1, p~ = round_l(p).                                                       */
@@ -159,6 +161,12 @@ static void prep_vector(int work, int dist, int guard, int d, const double* p, d
         double m = 0.0;
         for (int t = 0; t < d; ++t) if (fabs(p[t]) > m) m = fabs(p[t]);
         sc = (m == 0.0 || isnan(m)) ? 1.0 : m;
+        if (guard == 2 && sc != 1.0 && isfinite(sc)) {
+            int e;
+            double f = frexp(sc, &e);          /* sc = f 2^e, f in [0.5, 1) */
+            double up = (f == 0.5) ? sc : ldexp(1.0, e);
+            if (isfinite(up) && (work != OFMT_FP32 || up <= 3.4028234663852886e38)) sc = up;
+        }
     }
     *s = sc;
     for (int t = 0; t < d; ++t) {
@@ -366,7 +374,7 @@ static int set_delta(ostate_t* S, double delta) {
     if (delta > 0.0) {
         if (!(delta >= 1.0)) return -1;
         S->delta2 = delta * delta;
-        S->guard = 1;
+        if (!S->guard) S->guard = 1;
     }
     return 0;
 }
@@ -377,7 +385,7 @@ static int check_args(int64_t n, int d, int k, int work, int dist, int flags) {
     if (work != OFMT_FP64 && work != OFMT_FP32) return -1;
     if (dist < OFMT_FP64 || dist > OFMT_E5M2) return -1;
     if (work == OFMT_FP32 && dist == OFMT_FP64) return -1;   /* 0 < u <= u_l */
-    if (norm > ONORM_ZSCORE || (flags & ~(ONORM_MASK | OGUARD))) return -1;
+    if (norm > ONORM_ZSCORE || (flags & ~(ONORM_MASK | OGUARD | OGUARD_POW2))) return -1;
     return 0;
 }
 
@@ -395,7 +403,8 @@ int oracle_fit(int64_t n, int d, int k, int work, int dist, int flags, const dou
                double* scale_out, double* tr_sse, int64_t* tr_changed, double* tr_shift2,
                int32_t* tr_empty, double delta, int64_t* n_trig_out, double* tr_ubound) {
     if (check_args(n, d, k, work, dist, flags) != 0 || max_iter < 1 || k > n) return -1;
-    int norm = flags & ONORM_MASK, guard = (flags & OGUARD) != 0;
+    int norm = flags & ONORM_MASK;
+    int guard = (flags & OGUARD_POW2) ? 2 : ((flags & OGUARD) != 0);
     ostate_t S;
     if (alloc_state(&S, n, d, k, work, dist, guard) != 0) { free_state(&S); return -2; }
     if (set_delta(&S, delta) != 0) { free_state(&S); return -1; }
@@ -522,7 +531,8 @@ static double seed_dist(const ostate_t* S, int64_t i, int64_t c) {
 
 static int seed_prepare(ostate_t* S, int64_t n, int d, int work, int dist, int flags,
                         const double* X_in) {
-    int norm = flags & ONORM_MASK, guard = (flags & OGUARD) != 0;
+    int norm = flags & ONORM_MASK;
+    int guard = (flags & OGUARD_POW2) ? 2 : ((flags & OGUARD) != 0);
     if (alloc_state(S, n, d, 1, work, dist, guard) != 0) return -2;
     double* shift = (double*)malloc(sizeof(double) * d);
     double* scale = (double*)malloc(sizeof(double) * d);

@@ -19,6 +19,7 @@ KMEANS_FP64, KMEANS_FP32, KMEANS_FP16, KMEANS_BF16, KMEANS_E5M2 = 0, 1, 2, 3, 4
 KMEANS_NORM_NONE, KMEANS_NORM_MINMAX, KMEANS_NORM_ZSCORE = 0, 1, 2
 KMEANS_GUARD_SCALE = 0x100
 KMEANS_FORCE_SIMT = 0x200
+KMEANS_GUARD_POW2 = 0x400
 KMEANS_OK, KMEANS_EINVAL, KMEANS_ENOMEM, KMEANS_ECUDA, KMEANS_ENCCL, KMEANS_ENODEV = \
     0, -1, -2, -3, -4, -5
 KMEANS_WARN_NONFINITE, KMEANS_WARN_EMPTY, KMEANS_WARN_MAXITER, KMEANS_WARN_UNDERFLOW = 1, 2, 4, 8
@@ -262,7 +263,9 @@ class KMeans:
 
     def __init__(self, n, d, k, work="fp32", dist="fp16", norm="none", guard=False,
                  force_simt=False, delta=None):
+        # guard: False, True (s = ||x||_inf) or "pow2" (s = 2^ceil(log2 ||x||_inf))
         flags = NORM[norm] | (KMEANS_GUARD_SCALE if guard else 0) | \
+            (KMEANS_GUARD_POW2 if guard == "pow2" else 0) | \
             (KMEANS_FORCE_SIMT if force_simt else 0)
         self.n, self.d, self.k = int(n), int(d), int(k)
         self.work = work

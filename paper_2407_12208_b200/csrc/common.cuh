@@ -99,6 +99,31 @@ MPK_DEV bool is_zero_or_subnormal_low(e5m2_t v) { return (v.bits & 0x7C) == 0; }
 MPK_DEV bool is_zero_or_subnormal_low(float v) { return fabsf(v) < 1.17549435e-38f; }
 MPK_DEV bool is_zero_or_subnormal_low(double v) { return fabs(v) < 2.2250738585072014e-308; }
 
+// Alg 4's operand scale from a vector's infinity norm: guard 1 (reading Z9
+// A) s = ||x||_inf; guard 2 (reading Z9 B, KMEANS_GUARD_POW2) s = 2^ceil(log2 ||x||_inf), the
+// smallest power of two >= the norm, so x / s is exact (an MX / UE8M0 block scale with the row
+// as one block). Zero or NaN norm -> 1 (reading Z10); a power of two that would overflow -> the
+// norm itself.
+MPK_DEV float guard_scale(float amax, int guard) {
+    if (amax == 0.0f || isnan(amax)) return 1.0f;
+    if (guard != 2) return amax;
+    const uint32_t b = __float_as_uint(amax);
+    if ((b & 0x007fffffu) == 0u && (b & 0x7f800000u) != 0u) return amax;   // already 2^e
+    int e;
+    (void)frexpf(amax, &e);                   // amax = m 2^e, m in [0.5, 1)
+    const float s = ldexpf(1.0f, e);
+    return isinf(s) ? amax : s;
+}
+MPK_DEV double guard_scale(double amax, int guard) {
+    if (amax == 0.0 || isnan(amax)) return 1.0;
+    if (guard != 2) return amax;
+    int e;
+    const double m = frexp(amax, &e);
+    if (m == 0.5) return amax;
+    const double s = ldexp(1.0, e);
+    return isinf(s) ? amax : s;
+}
+
 // ------------------------------------------------------------------------------------------
 // Reductions.
 // ------------------------------------------------------------------------------------------

@@ -130,7 +130,8 @@ int smalld_loop_grid(int64_t n);
 size_t smalld_loop_part_bytes(int64_t n);
 cudaError_t launch_smalld_iter(int work, int dist, const Problem& p, const void* Xw, void* Cw,
                                int32_t* labels, double* part, LoopState* st, IterRec* trace,
-                               unsigned long long* census, cudaStream_t s);
+                               unsigned long long* census, cudaStream_t s);   // Xw == nullptr: only set the kernel's
+                                                      // shared-memory attribute (per device)
 
 // K6m: Alg 4's per-pair precision switch with threshold delta (>= 1); n_low (device) gets the
 // number of triggered (low-precision) pairs added.
@@ -187,6 +188,28 @@ cudaError_t launch_cand_exact(const float* Xw, const float* Cw, const float* cn,
                               const int* rows, int nr, const int* cand_cnt, const int* cand,
                               int cand_q, int32_t* labels, int* left_count, int* left_rows,
                               unsigned long long* keys, cudaStream_t s);
+
+// Alg 4 / Alg 5 on the tensor cores (k_final.cu; R10): candidate columns of the
+// certified filter's uncertified rows evaluated with the per-pair switch exactly as K6m-b; the
+// trigger counts per row from the sorted centroid norms; per-row label distance (SSE_t) and the
+// changed count; gathers for the rows left to the full CUDA-core evaluation.
+cudaError_t launch_cand_exact_mixed(int dist, const void* Xl, const float* Xw, const void* Cl,
+                                    const float* Cw, const float* xn, const float* sx,
+                                    const float* cn, const float* sc, int d, int d_pad,
+                                    double delta2, const int* rows, int nr, const int* cand_cnt,
+                                    const int* cand, int cand_q, int32_t* labels, int* left_count,
+                                    int* left_rows, unsigned long long* keys, cudaStream_t s);
+cudaError_t launch_mixed_count(const float* xn, int64_t n, const float* cn, int k, double delta2,
+                               float* sorted_cn, unsigned long long* n_low, cudaStream_t s);
+cudaError_t launch_mixed_label_eval(int dist, const void* Xl, const float* Xw, const void* Cl,
+                                    const float* Cw, const float* xn, const float* sx,
+                                    const float* cn, const float* sc, int64_t n, int d, int d_pad,
+                                    double delta2, const int32_t* labels, const int32_t* prev,
+                                    double* acc_sse, double* acc_changed, cudaStream_t s);
+cudaError_t launch_gather_float_rows(const float* src, int d, const int* rows, int nr, float* dst,
+                                     cudaStream_t s);
+cudaError_t launch_scatter_labels(const int32_t* src, const int* rows, int nr, int32_t* labels,
+                                  cudaStream_t s);
 
 // K7: update = stable bucket sort by label (block counts, scan, scatter) + segmented fp64 sums
 // with an ordered reduction of the chunk-boundary partials: bit-reproducible for k <= 12288.

@@ -732,7 +732,7 @@ smalld_kernel(Problem p, const W* __restrict__ X, const typename low_type<DIST>:
         }
         W xn = rounder<WORK>::from(nrm);
         W s = (W)1;
-        if (p.guard && !same) s = (amax == 0.0 || isnan(amax)) ? (W)1 : (W)amax;
+        if (p.guard && !same) s = (W)guard_scale((W)amax, p.guard);
         AT xl[SD_D];
 #pragma unroll
         for (int t = 0; t < SD_D; ++t) {

@@ -475,7 +475,7 @@ __global__ void prep_kernel(const W* __restrict__ X, int64_t rows, int d, int d_
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
         W s = (W)1;
-        if (guard && !same) s = (amax == (W)0 || isnan(amax)) ? (W)1 : amax;
+        if (guard && !same) s = guard_scale(amax, guard);
         if (lane == 0) {
             norms[i] = rounder<WORK>::from(acc);
             if (scales) scales[i] = s;
@@ -668,7 +668,7 @@ MPK_DEV void prep_row_fast(float (&v)[Q], int64_t i, int lane, int d, int d_pad,
         for (int q = 0; q < Q; ++q) amax = fmaxf(amax, fabsf(v[q]));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-        s = (amax == 0.0f || isnan(amax)) ? 1.0f : amax;
+        s = guard_scale(amax, guard);
     }
     if (lane == 0) {
         norms[i] = __double2float_rn(acc);
@@ -850,7 +850,7 @@ prep_vec_kernel(const float* __restrict__ Xin, int64_t rows, int d, int guard,
                     for (int e = 0; e < 4; ++e) amax = fmaxf(amax, fabsf(v[w][e]));
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-                s = (amax == 0.0f || isnan(amax)) ? 1.0f : amax;
+                s = guard_scale(amax, guard);
                 if (s != 1.0f) {          // warp-uniform: s is the row's
 #pragma unroll
                     for (int w = 0; w < V; ++w)

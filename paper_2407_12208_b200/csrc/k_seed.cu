@@ -11,8 +11,8 @@
 // a warp tree, warps in order; then a block-level scan), so the draw is deterministic; it is not
 // bit-identical to the oracle's sequential sums and fp64 dots, and the tests check each draw's
 // admissibility against the oracle's weights for the same chosen centres instead.
-// Per round: one pass over X~ (HBM: n d_pad s_l + 16 n bytes) by groups of G lanes per row
-// (16-byte loads, 4 rows in flight per group), then one CTA's scan-and-pick.
+// Per round: one pass over X~ (HBM: n d_pad s_l + 16 n bytes), one row per thread with the
+// row's 16-byte chunks all in flight, then one CTA's scan-and-pick.
 #include "common.cuh"
 #include "internal.h"
 
@@ -24,7 +24,6 @@ namespace {
 constexpr int kSeedBlock = 4096;     // rows per update CTA (and per block sum)
 constexpr int kSeedThreads = 256;
 constexpr int kPickThreads = 1024;
-constexpr int kRowsInFlight = 4;
 
 template <typename LT> struct seed_acc { using T = float; };
 template <> struct seed_acc<double> { using T = double; };
@@ -46,7 +45,7 @@ __global__ void __launch_bounds__(kSeedThreads)
 seed_update_kernel(const LT* __restrict__ Xl, int64_t n, int d, int d_pad,
                    const W* __restrict__ xn, const W* __restrict__ sx, int guard,
                    const int64_t* __restrict__ idx, int j, double* __restrict__ D2,
-                   double* __restrict__ ps, int G, int vec) {
+                   double* __restrict__ ps, int vec) {
     using A = typename seed_acc<LT>::T;
     extern __shared__ __align__(16) unsigned char seed_smem[];
     A* cs = reinterpret_cast<A*>(seed_smem);                    // newest centre, widened (d_pad)
@@ -61,54 +60,39 @@ seed_update_kernel(const LT* __restrict__ Xl, int64_t n, int d, int d_pad,
     const int64_t b0 = (int64_t)blockIdx.x * kSeedBlock;
     const int rows = (int)((b0 + kSeedBlock < n) ? kSeedBlock : n - b0);
     const int lane = threadIdx.x & 31;
-    const int gl = lane & (G - 1);                       // lane within the row group
-    const int groups = kSeedThreads / G;                 // row groups per CTA
-    const int grp = threadIdx.x / G;
     const int chunks = (d_pad * (int)sizeof(LT)) / 16;
     constexpr int m = 16 / (int)sizeof(LT);
-    // warp-uniform trip count (the group shuffles below need every lane of the warp)
-    for (int base = 0; base < rows; base += groups * kRowsInFlight) {
-        const int r0 = base + grp;
-        A dot[kRowsInFlight];
-#pragma unroll
-        for (int u = 0; u < kRowsInFlight; ++u) dot[u] = (A)0;
+    constexpr int QB = 16;                          // 16-byte chunks of a row in flight
+    // one row per thread: the whole row's 16-byte chunks are loaded before they are used (a
+    // warp keeps 32 rows, 8 KB at d = 128 fp16, in flight); the dot is the sequential fp32 sum
+    for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+        const int64_t i = b0 + r;
+        const double old = D2[i];
+        const W xni = xn[i];
+        const W si_w = guard ? sx[i] : (W)1;
+        A dot = (A)0;
         if (vec) {
-            uint4 q[kRowsInFlight];
-            for (int ch = gl; ch < chunks; ch += G) {
+            const uint4* xp = reinterpret_cast<const uint4*>(Xl + i * d_pad);
+            for (int q0 = 0; q0 < chunks; q0 += QB) {
+                uint4 buf[QB];
 #pragma unroll
-                for (int u = 0; u < kRowsInFlight; ++u) {
-                    const int r = r0 + u * groups;
-                    q[u] = r < rows ? __ldg(reinterpret_cast<const uint4*>(Xl + (b0 + r) * d_pad) + ch)
-                                    : make_uint4(0, 0, 0, 0);
-                }
+                for (int u = 0; u < QB; ++u)
+                    buf[u] = (q0 + u < chunks) ? __ldg(xp + q0 + u) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-                for (int u = 0; u < kRowsInFlight; ++u) dot[u] = dot16<LT, A>(q[u], cs, ch * m, d, dot[u]);
+                for (int u = 0; u < QB; ++u)
+                    if (q0 + u < chunks) dot = dot16<LT, A>(buf[u], cs, (q0 + u) * m, d, dot);
             }
         } else {
-            for (int t = gl; t < d; t += G) {
-#pragma unroll
-                for (int u = 0; u < kRowsInFlight; ++u) {
-                    const int r = r0 + u * groups;
-                    if (r < rows) dot[u] = fma((A)widen(Xl[(b0 + r) * d_pad + t]), cs[t], dot[u]);
-                }
-            }
+            const LT* xp = Xl + i * d_pad;
+            for (int t = 0; t < d; ++t) dot = fma((A)widen(xp[t]), cs[t], dot);
         }
-#pragma unroll
-        for (int u = 0; u < kRowsInFlight; ++u) {
-            for (int o = G >> 1; o > 0; o >>= 1) dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], o);
-            const int r = r0 + u * groups;
-            if (gl == 0 && r < rows) {
-                const int64_t i = b0 + r;
-                const double si = guard ? (double)sx[i] : 1.0;
-                double D = ((double)xn[i] - 2.0 * (si * scc) * (double)dot[u]) + xnc;
-                D = D > 0.0 ? D : 0.0;                  // NaN -> 0
-                if (i == c) D = 0.0;                    // the centre's own weight
-                const double old = D2[i];
-                const double nw = D < old ? D : old;
-                D2[i] = nw;
-                d2s[r] = nw;
-            }
-        }
+        const double si = (double)si_w;
+        double D = ((double)xni - 2.0 * (si * scc) * (double)dot) + xnc;
+        D = D > 0.0 ? D : 0.0;                      // NaN -> 0
+        if (i == c) D = 0.0;                        // the centre's own weight
+        const double nw = D < old ? D : old;
+        D2[i] = nw;
+        d2s[r] = nw;
     }
     __syncthreads();
     // block sum in a fixed order: 16-row pieces sequentially, a warp tree, warps in order
@@ -276,12 +260,9 @@ cudaError_t seed_rounds(const void* Xl, int64_t n, int d, int d_pad, const void*
     }
     const int row_bytes = d_pad * (int)sizeof(LT);
     const int vec = (row_bytes % 16 == 0) && ((reinterpret_cast<uintptr_t>(Xl) & 15) == 0);
-    const int units = vec ? row_bytes / 16 : d;        // 16-byte chunks or elements per row
-    int G = 1;
-    while (G * 2 <= units && G * 2 <= 32) G *= 2;
     for (int j = 1; j < k; ++j) {
         seed_update_kernel<LT, W><<<(unsigned)nb, kSeedThreads, sm, s>>>(
-            (const LT*)Xl, n, d, d_pad, (const W*)xn, (const W*)sx, guard, idx, j - 1, D2, ps, G,
+            (const LT*)Xl, n, d, d_pad, (const W*)xn, (const W*)sx, guard, idx, j - 1, D2, ps,
             vec);
         seed_pick_kernel<<<1, kPickThreads, 0, s>>>(D2, ps, n, nb, u, j, idx, warn);
     }

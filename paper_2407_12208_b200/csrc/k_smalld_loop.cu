@@ -13,7 +13,10 @@
 // A launch that finds the stop flag set returns at once, so the host can enqueue (or replay as
 // a CUDA graph) a chunk of iterations and poll the flag once per chunk: the iteration costs one
 // launch instead of three launches, a memset and a host round trip.
-// Rows are staged through shared memory in tiles of kTileRows rows with 16-byte loads.
+// Rows (and the previous labels) stream through shared memory in a ring of kStages tiles of
+// kTileRows rows filled by 1-D bulk copies (the TMA engine), so the next tiles' HBM reads overlap
+// this tile's arithmetic; each thread's 8 rows of a tile are summed in fp32 and then added to its
+// fp64 totals (reading R1).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -25,11 +28,45 @@ namespace mpk {
 
 namespace {
 
-constexpr int LD = 4, LK = 8, LT = 256, kTileRows = 1024;
+constexpr int LD = 4, LK = 8, LT = 256;
+#ifndef MPK_SL_TILE
+#define MPK_SL_TILE 2048
+#endif
+#ifndef MPK_SL_MINB
+#define MPK_SL_MINB 1
+#endif
+constexpr int kTileRows = MPK_SL_TILE;   // rows per pipeline stage (8 per thread)
+constexpr int kStages = 3;           // tiles in flight per block (bulk copies)
 constexpr int NV = LK * LD + LK + 2;   // sums, counts, sse, changed
+constexpr int kRedGroups = LT / NV;    // the last block reduces the partials in this many groups
 
-template <typename W, int DIST>
-__global__ void __launch_bounds__(LT)
+MPK_DEV uint32_t sm_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+MPK_DEV void bar_init(uint32_t b, uint32_t c) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(c) : "memory");
+}
+MPK_DEV void bar_expect(uint32_t b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+                 : "memory");
+}
+MPK_DEV void bar_wait(uint32_t b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "W_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra W_%=;\n\t}" ::"r"(b),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on the mbarrier
+MPK_DEV void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+// D: the feature count (exact, 1..4); KT: the centroid loop bound (4 or 8, >= k)
+template <typename W, int DIST, int D, int KT>
+__global__ void __launch_bounds__(LT, MPK_SL_MINB)
 smalld_iter_kernel(Problem p, const W* __restrict__ X, W* __restrict__ C,
                    int32_t* __restrict__ labels, double* __restrict__ part,
                    LoopState* __restrict__ st, IterRec* __restrict__ trace,
@@ -39,13 +76,44 @@ smalld_iter_kernel(Problem p, const W* __restrict__ X, W* __restrict__ C,
     constexpr int WORK = sizeof(W) == 8 ? KMEANS_FP64 : KMEANS_FP32;
     constexpr bool same = (DIST == WORK);
     if (*(volatile int*)&st->stop) return;            // converged: this launch is a no-op
+    extern __shared__ __align__(128) unsigned char dsm[];
+    const int d = p.d, k = p.k;
+    const size_t xbytes = (size_t)kTileRows * d * sizeof(W);
+    W* xs0 = reinterpret_cast<W*>(dsm);                                   // [kStages][rows*d]
+    int32_t* ls0 = reinterpret_cast<int32_t*>(dsm + kStages * xbytes);   // [kStages][rows]
     __shared__ AT cl_s[LK][LD];
     __shared__ W cn_s[LK], sc_s[LK];
-    __shared__ __align__(16) W xs[kTileRows * LD];
     __shared__ double red[LT / 32][NV];
+    __shared__ __align__(8) uint64_t full[kStages];
     __shared__ int is_last;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int d = p.d, k = p.k;
+    const int64_t ntiles = (p.n + kTileRows - 1) / kTileRows;
+    const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    auto tile_rows = [&](int64_t m) {
+        const int64_t r0 = ((int64_t)blockIdx.x + m * gridDim.x) * kTileRows;
+        return (int)std::min<int64_t>(kTileRows, p.n - r0);
+    };
+    // a tile whose X bytes are not a multiple of 16 (only the ragged last one) is read with
+    // plain loads; the others stream through the bulk-copy ring
+    auto bulk_ok = [&](int rows) { return ((size_t)rows * d * sizeof(W)) % 16 == 0 && (rows * 4) % 16 == 0; };
+    auto issue = [&](int64_t m) {
+        const int stg = (int)(m % kStages);
+        const int rows = tile_rows(m);
+        if (!bulk_ok(rows)) return;
+        const int64_t r0 = ((int64_t)blockIdx.x + m * gridDim.x) * kTileRows;
+        const uint32_t xb = (uint32_t)((size_t)rows * d * sizeof(W));
+        const uint32_t fb = sm_u32(&full[stg]);
+        bar_expect(fb, xb + (uint32_t)rows * 4u);
+        bulk_g2s(sm_u32(xs0 + (size_t)stg * kTileRows * d), X + r0 * d, xb, fb);
+        bulk_g2s(sm_u32(ls0 + (size_t)stg * kTileRows), labels + r0, (uint32_t)rows * 4u, fb);
+    };
+    if (tid == 0) {
+        for (int q = 0; q < kStages; ++q) bar_init(sm_u32(&full[q]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int64_t m = 0; m < my_tiles && m < kStages; ++m) issue(m);
 
     // ---- A3: centroid prep (the arithmetic of prep_kernel: exact squares summed in the warp
     // reduction's order, infinity-norm scale, one rounding of c / s) -------------------------
@@ -60,7 +128,7 @@ smalld_iter_kernel(Problem p, const W* __restrict__ X, W* __restrict__ C,
             amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
         }
         W s = (W)1;
-        if (p.guard && !same) s = (amax == (W)0 || isnan(amax)) ? (W)1 : amax;
+        if (p.guard && !same) s = guard_scale(amax, p.guard);
         unsigned long long nf = 0, nu = 0;
         if (lane < LD) {
             AT o = (AT)0;
@@ -87,89 +155,105 @@ smalld_iter_kernel(Problem p, const W* __restrict__ X, W* __restrict__ C,
     }
     __syncthreads();
 
-    double sums[LK][LD];
-    double cnts[LK];
+    double sums[KT][D];
+    double cnts[KT];
 #pragma unroll
-    for (int j = 0; j < LK; ++j) {
+    for (int j = 0; j < KT; ++j) {
         cnts[j] = 0.0;
 #pragma unroll
-        for (int t = 0; t < LD; ++t) sums[j][t] = 0.0;
+        for (int t = 0; t < D; ++t) sums[j][t] = 0.0;
     }
     double my_sse = 0.0, my_changed = 0.0;
 
     // ---- A4 + A5 over this block's tiles -----------------------------------------------------
-    const int64_t ntiles = (p.n + kTileRows - 1) / kTileRows;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t r0 = tile * kTileRows;
-        const int rows = (int)std::min<int64_t>(kTileRows, p.n - r0);
-        const int64_t e0 = r0 * d;
-        const int ne = rows * d;
-        __syncthreads();                               // xs reuse
-        constexpr int VW = 16 / sizeof(W);             // elements per 16-byte load
-        const W* src = X + e0;
-        if ((((uintptr_t)src) & 15) == 0) {
-            const int nv = ne / VW;
-            for (int q = tid; q < nv; q += LT)
-                reinterpret_cast<int4*>(xs)[q] = __ldg(reinterpret_cast<const int4*>(src) + q);
-            for (int q = nv * VW + tid; q < ne; q += LT) xs[q] = src[q];
+    for (int64_t m = 0; m < my_tiles; ++m) {
+        const int stg = (int)(m % kStages);
+        const int rows = tile_rows(m);
+        const int64_t r0 = ((int64_t)blockIdx.x + m * gridDim.x) * kTileRows;
+        W* xs = xs0 + (size_t)stg * kTileRows * d;
+        int32_t* ls = ls0 + (size_t)stg * kTileRows;
+        if (bulk_ok(rows)) {
+            bar_wait(sm_u32(&full[stg]), (uint32_t)((m / kStages) & 1));
         } else {
-            for (int q = tid; q < ne; q += LT) xs[q] = src[q];
+            for (int q = tid; q < rows * d; q += LT) xs[q] = X[r0 * d + q];
+            for (int q = tid; q < rows; q += LT) ls[q] = labels[r0 + q];
+            __syncthreads();
         }
-        __syncthreads();
+        // this tile's sums: partials of the thread's 8 rows in the working precision (fp32
+        // partials of 8 rows, then fp64: reading R1; fp64 work: fp64 throughout)
+        W ps[KT][D], pc[KT];
+#pragma unroll
+        for (int j = 0; j < KT; ++j) {
+            pc[j] = (W)0;
+#pragma unroll
+            for (int t = 0; t < D; ++t) ps[j][t] = (W)0;
+        }
         for (int r = tid; r < rows; r += LT) {
             const int64_t i = r0 + r;
-            W x[LD];
-            double nrm = 0.0, amax = 0.0;
+            W x[D];
+            double nrm = 0.0;
 #pragma unroll
-            for (int t = 0; t < LD; ++t) {
-                x[t] = t < d ? xs[r * d + t] : (W)0;
+            for (int t = 0; t < D; ++t) {
+                x[t] = xs[r * D + t];
                 const double v = (double)x[t];
                 nrm = __dadd_rn(nrm, __dmul_rn(v, v));
-                amax = fmax(amax, fabs(v));
             }
             const W xn = rounder<WORK>::from(nrm);
             W s = (W)1;
-            if (p.guard && !same) s = (amax == 0.0 || isnan(amax)) ? (W)1 : (W)amax;
-            AT xl[LD];
+            if (p.guard && !same) {
+                W amax = (W)0;
 #pragma unroll
-            for (int t = 0; t < LD; ++t) {
+                for (int t = 0; t < D; ++t) amax = fmax(amax, fabs(x[t]));
+                s = guard_scale(amax, p.guard);
+            }
+            AT xl[D];
+#pragma unroll
+            for (int t = 0; t < D; ++t) {
                 const W q = (s == (W)1) ? x[t] : x[t] / s;
                 xl[t] = (AT)widen(rounder<DIST>::from(q));
             }
             W best = (W)INFINITY;
             int bj = 0;
 #pragma unroll
-            for (int j = 0; j < LK; ++j) {
+            for (int j = 0; j < KT; ++j) {
                 if (j < k) {
                     AT dot = (AT)0;
 #pragma unroll
-                    for (int t = 0; t < LD; ++t) dot = fma(xl[t], cl_s[j][t], dot);
+                    for (int t = 0; t < D; ++t) dot = fma(xl[t], cl_s[j][t], dot);
                     const W v = fma((W)-2 * (s * sc_s[j]), (W)dot, cn_s[j]);
                     if (v < best) { best = v; bj = j; }
                 }
             }
-            if (labels[i] != bj) my_changed += 1.0;
+            if (ls[r] != bj) my_changed += 1.0;
             labels[i] = bj;
             const double md = (double)xn + (double)best;
             my_sse += md > 0.0 ? md : 0.0;
 #pragma unroll
-            for (int j = 0; j < LK; ++j) {
-                const bool hit = (bj == j);
-                cnts[j] += hit ? 1.0 : 0.0;
+            for (int j = 0; j < KT; ++j) {
+                const W hit = (bj == j) ? (W)1 : (W)0;
+                pc[j] += hit;
 #pragma unroll
-                for (int t = 0; t < LD; ++t) sums[j][t] += hit ? (double)x[t] : 0.0;
+                for (int t = 0; t < D; ++t) ps[j][t] = fma(hit, x[t], ps[j][t]);
             }
         }
+#pragma unroll
+        for (int j = 0; j < KT; ++j) {
+            cnts[j] += (double)pc[j];
+#pragma unroll
+            for (int t = 0; t < D; ++t) sums[j][t] += (double)ps[j][t];
+        }
+        __syncthreads();                               // every thread is done with this stage
+        if (tid == 0 && m + kStages < my_tiles) issue(m + kStages);
     }
     // ---- block partial (warp shuffles, then warps in order) ---------------------------------
 #pragma unroll
     for (int j = 0; j < LK; ++j) {
 #pragma unroll
         for (int t = 0; t < LD; ++t) {
-            const double v = warp_sum(sums[j][t]);
+            const double v = (j < KT && t < D) ? warp_sum(sums[j < KT ? j : 0][t < D ? t : 0]) : 0.0;
             if (lane == 0) red[w][j * LD + t] = v;
         }
-        const double c = warp_sum(cnts[j]);
+        const double c = j < KT ? warp_sum(cnts[j < KT ? j : 0]) : 0.0;
         if (lane == 0) red[w][LK * LD + j] = c;
     }
     my_sse = warp_sum(my_sse);
@@ -189,25 +273,34 @@ smalld_iter_kernel(Problem p, const W* __restrict__ X, W* __restrict__ C,
     __syncthreads();
     if (!is_last) return;
     __threadfence();
-    // partials of all blocks, summed in block order (thread per value; at most a few hundred
-    // blocks), into red[0][.]
-    if (tid < NV) {
+    // partials of all blocks in a fixed order: group g sums the blocks b = g (mod kRedGroups)
+    // in increasing b (independent loads in flight), then the groups are added in order
+    if (tid < NV * kRedGroups) {
+        const int c = tid % NV, g = tid / NV;
         double a = 0.0;
-        for (unsigned b = 0; b < gridDim.x; ++b) a += __ldcg(part + (size_t)b * NV + tid);
-        red[0][tid] = a;
+#pragma unroll 4
+        for (unsigned b = g; b < gridDim.x; b += kRedGroups) a += __ldcg(part + (size_t)b * NV + c);
+        red[g][c] = a;
     }
     __syncthreads();
+    if (tid < NV) {
+        double a = 0.0;
+        for (int g = 0; g < kRedGroups; ++g) a += red[g][tid];
+        red[LT / 32 - 1][tid] = a;
+    }
+    __syncthreads();
+    const double* tot = red[LT / 32 - 1];
     if (w == 0) {
         // one lane per (cluster, feature): new centre, shift and Thm 5.3 terms
-        double num = 0.0, den = 0.0, sh = 0.0, empty = 0.0, rmax = 0.0;
+        double sh = 0.0, empty = 0.0, rmax = 0.0;
         for (int j = 0; j < k; ++j) {
-            const double c = red[0][LK * LD + j];
+            const double c = tot[LK * LD + j];
             double nm = 0.0, dn = 0.0;
             if (lane < d) {
                 const int idx = j * d + lane;
                 const W old = C[idx];
                 W nw = old;
-                if (c > 0.0) nw = rounder<WORK>::from(red[0][j * LD + lane] / c);
+                if (c > 0.0) nw = rounder<WORK>::from(tot[j * LD + lane] / c);
                 const double df = (double)nw - (double)old;
                 nm = df * df;
                 dn = fabs(df) * fabs((double)nw);
@@ -219,17 +312,16 @@ smalld_iter_kernel(Problem p, const W* __restrict__ X, W* __restrict__ C,
             if (c == 0.0) empty += 1.0;
             if (nm > 0.0 && dn > 0.0) rmax = fmax(rmax, 2.0 * dn / nm);
         }
-        (void)num; (void)den;
         if (lane == 0) {
             const int it = st->iter;
             IterRec* rec = trace + (it < KMEANS_MAX_TRACE - 1 ? it : KMEANS_MAX_TRACE - 1);
-            rec->sse = red[0][NV - 2];
+            rec->sse = tot[NV - 2];
             rec->shift2 = sh;
-            rec->changed = red[0][NV - 1];
+            rec->changed = tot[NV - 1];
             rec->empty = empty;
             rec->ub_inv = rmax;
             st->iter = it + 1;
-            if (st->tol >= 0.0 && (red[0][NV - 1] == 0.0 || sqrt(sh) <= st->tol)) {
+            if (st->tol >= 0.0 && (tot[NV - 1] == 0.0 || sqrt(sh) <= st->tol)) {
                 st->stop = 1;
                 st->converged = 1;
             }
@@ -239,13 +331,39 @@ smalld_iter_kernel(Problem p, const W* __restrict__ X, W* __restrict__ C,
     }
 }
 
+template <typename W>
+size_t smem_bytes_for(int d) {
+    return (size_t)kStages * kTileRows * ((size_t)d * sizeof(W) + sizeof(int32_t));
+}
+
+template <typename W, int DIST, int D, int KT>
+cudaError_t launch_dk(const Problem& p, const void* X, void* C, int32_t* labels, double* part,
+                      int grid, LoopState* st, IterRec* trace, unsigned long long* census,
+                      cudaStream_t s) {
+    const size_t sm = smem_bytes_for<W>(D);
+    if (!X) {   // attribute-only call (before a stream capture: not a stream operation)
+        return cudaFuncSetAttribute(smalld_iter_kernel<W, DIST, D, KT>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    }
+    smalld_iter_kernel<W, DIST, D, KT><<<grid, LT, sm, s>>>(p, (const W*)X, (W*)C, labels, part,
+                                                            st, trace, census);
+    return cudaGetLastError();
+}
+
 template <typename W, int DIST>
 cudaError_t launch_t(const Problem& p, const void* X, void* C, int32_t* labels, double* part,
                      int grid, LoopState* st, IterRec* trace, unsigned long long* census,
                      cudaStream_t s) {
-    smalld_iter_kernel<W, DIST><<<grid, LT, 0, s>>>(p, (const W*)X, (W*)C, labels, part, st, trace,
-                                                    census);
-    return cudaGetLastError();
+#define MPK_DK(Dv) \
+    return p.k <= 4 ? launch_dk<W, DIST, Dv, 4>(p, X, C, labels, part, grid, st, trace, census, s) \
+                    : launch_dk<W, DIST, Dv, 8>(p, X, C, labels, part, grid, st, trace, census, s)
+    switch (p.d) {
+        case 1: MPK_DK(1);
+        case 2: MPK_DK(2);
+        case 3: MPK_DK(3);
+        default: MPK_DK(4);
+    }
+#undef MPK_DK
 }
 
 }  // namespace
@@ -262,7 +380,7 @@ size_t smalld_loop_part_bytes(int64_t n) { return (size_t)smalld_loop_grid(n) * 
 cudaError_t launch_smalld_iter(int work, int dist, const Problem& p, const void* Xw, void* Cw,
                                int32_t* labels, double* part, LoopState* st, IterRec* trace,
                                unsigned long long* census, cudaStream_t s) {
-    launches_add(1);
+    if (Xw) launches_add(1);
     const int g = smalld_loop_grid(p.n);
 #define MPK_SL(W)                                                                                  \
     switch (dist) {                                                                                \

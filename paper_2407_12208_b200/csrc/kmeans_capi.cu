@@ -86,6 +86,16 @@ struct kmeans_ctx {
     bool fx_amax_done = false;     // this fit's prep computed the column maxima
     FxState fx;
 
+    // Alg 4 / Alg 5 on the tensor cores (assign_mixed_tc): previous labels, sorted centroid
+    // norms, and the gathered rows left to the full CUDA-core evaluation (grown on demand)
+    int32_t* mix_prev = nullptr;
+    float* mix_sorted = nullptr;
+    int64_t mix_cap = 0;
+    void* mix_Xl = nullptr;
+    float* mix_Xw = nullptr;
+    float* mix_xn = nullptr;
+    float* mix_sx = nullptr;
+    int32_t* mix_lab = nullptr;
     // K5g fused small-d iteration (k_smalld_loop.cu): device loop state, block partials, a
     // CUDA graph of kLoopChunk iterations, pinned host copies of the state
     LoopState* loop = nullptr;
@@ -193,6 +203,10 @@ void free_all(kmeans_ctx* h) {
                     h->fx.gSlo, h->fx.gcnt};
     for (void* b : bufs)
         if (b) cudaFree(b);
+    void* mix_bufs[] = {h->mix_prev, h->mix_sorted, h->mix_Xl, h->mix_Xw, h->mix_xn, h->mix_sx,
+                        h->mix_lab};
+    for (void* b : mix_bufs)
+        if (b) cudaFree(b);
     if (h->loop) cudaFree(h->loop);
     if (h->loop_part) cudaFree(h->loop_part);
     if (h->loop_host) cudaFreeHost(h->loop_host);
@@ -219,7 +233,8 @@ int create_impl(int64_t n, int32_t d, int32_t k, int work, int dist, int flags,
         return fail(nullptr, KMEANS_EINVAL, "unknown dist_prec");
     if (work == KMEANS_FP32 && dist == KMEANS_FP64)
         return fail(nullptr, KMEANS_EINVAL, "dist_prec must not be more precise than work_prec");
-    if (norm > KMEANS_NORM_ZSCORE || (flags & ~(0xff | KMEANS_GUARD_SCALE | KMEANS_FORCE_SIMT)))
+    if (norm > KMEANS_NORM_ZSCORE ||
+        (flags & ~(0xff | KMEANS_GUARD_SCALE | KMEANS_FORCE_SIMT | KMEANS_GUARD_POW2)))
         return fail(nullptr, KMEANS_EINVAL, "unknown flags");
     if (nranks < 1 || rank < 0 || rank >= nranks)
         return fail(nullptr, KMEANS_EINVAL, "bad rank / nranks");
@@ -228,7 +243,9 @@ int create_impl(int64_t n, int32_t d, int32_t k, int work, int dist, int flags,
 
     h = new kmeans_ctx();
     h->n = n; h->d = d; h->k = k; h->work = work; h->dist = dist; h->flags = flags;
-    h->norm = norm; h->guard = (flags & KMEANS_GUARD_SCALE) ? 1 : 0;
+    h->norm = norm;
+    // guard: 0 off, 1 s = ||x||_inf (reading Z9 A), 2 s = 2^ceil(log2 ||x||_inf) (Z9 B)
+    h->guard = (flags & KMEANS_GUARD_POW2) ? 2 : ((flags & KMEANS_GUARD_SCALE) ? 1 : 0);
     h->force_simt = (flags & KMEANS_FORCE_SIMT) ? 1 : 0;
     h->device = dev;
     h->wsize = elem_size(work);
@@ -436,10 +453,128 @@ struct EventPool {
     }
 };
 
+constexpr int kCandQ = 32;   // candidate columns kept per uncertified row
+
+// Alg 4 / Alg 5 on the tensor cores (R10). The certified filter of the final pass
+// (FINAL mode of the pair kernel) runs on the loop's guarded low-precision operands: a row whose
+// low-precision top-2 gap exceeds 2 (E + B32) has the same argmin under Alg 4's per-pair
+// distances (the triggered pairs' CUDA-core evaluation differs from the tensor core's only by
+// accumulation order, the others by at most E + B32, R2's proof), and for every other row the
+// columns with v^_j <= T contain that argmin and its ties; those candidates are evaluated with
+// the switch exactly as K6m-b does (cand_exact_mixed). Rows with no or too many candidates get
+// the full K6m-b evaluation on gathered copies. eta is counted exactly from the sorted norms.
+bool mixed_tc_ok(const kmeans_ctx* h) {
+    return h->dist_kernel == DK_TCGEN05 && h->work == KMEANS_FP32 &&
+           (h->dist == KMEANS_FP16 || h->dist == KMEANS_BF16) && tc_plan_has_cand(h->tc) &&
+           h->k <= 16384 && !getenv("MPK_MIXED_SIMT");
+}
+
+int ensure_cand_buffers(kmeans_ctx* h, TcPlan* plan, int64_t nfb) {
+    if (nfb <= h->cand_cap) return 0;
+    void* old[] = {h->cand_X, h->cand_sx, h->cand_cnt, h->cand, h->cand_left, h->cand_key};
+    for (void* b : old)
+        if (b) cudaFree(b);
+    h->cand_X = h->cand_sx = nullptr;
+    h->cand_cnt = h->cand = h->cand_left = nullptr;
+    h->cand_key = nullptr;
+    const int64_t cap = std::min<int64_t>(h->n, nfb + nfb / 4 + 1024);
+    int rb = 0;
+    tc_plan_operands(plan, &rb);
+    CK(cudaMalloc(&h->cand_X, (size_t)cap * rb));
+    CK(cudaMalloc(&h->cand_sx, (size_t)cap * 4));
+    CK(cudaMalloc(&h->cand_cnt, (size_t)cap * 4));
+    CK(cudaMalloc(&h->cand, (size_t)cap * kCandQ * 4));
+    CK(cudaMalloc(&h->cand_left, (size_t)cap * 4));
+    CK(cudaMalloc(&h->cand_key, (size_t)cap * 8));
+    h->cand_cap = cap;
+    return 0;
+}
+
+int assign_mixed_tc(kmeans_ctx* h, int64_t rows, double* acc_sse, double* acc_changed) {
+    cudaStream_t s = h->stream;
+    const int d = h->d, k = h->k;
+    const double delta2 = h->delta * h->delta;
+    if (!h->mix_prev) {
+        int kp = 1;
+        while (kp < k) kp <<= 1;
+        CK(cudaMalloc(&h->mix_prev, (size_t)h->n * sizeof(int32_t)));
+        CK(cudaMalloc(&h->mix_sorted, (size_t)kp * sizeof(float)));
+    }
+    if (!h->fb_thr) CK(cudaMalloc(&h->fb_thr, (size_t)std::max<int64_t>(h->n, 1) * 4));
+    if (acc_changed)
+        CK(cudaMemcpyAsync(h->mix_prev, h->labels, (size_t)rows * sizeof(int32_t),
+                           cudaMemcpyDeviceToDevice, s));
+    // eta: the triggered pairs of these rows, exactly
+    CK(launch_mixed_count((const float*)h->xn, rows, (const float*)h->cn, k, delta2,
+                          h->mix_sorted, h->n_low_dev, s));
+    // the certified filter (labels of every row; the uncertified ones listed with thresholds)
+    Problem p{rows, d, k, h->d_pad, h->guard};
+    CK(cudaMemsetAsync(h->fbc, 0, 2 * sizeof(int), s));
+    CK(launch_final_tc(h->tc, p, (const float*)h->xn, (const float*)h->sx, (const float*)h->cn,
+                       (const float*)h->sc, h->labels, h->fbc, h->perm, h->fb_thr, s));
+    int nfb = 0;
+    CK(cudaMemcpyAsync(&nfb, h->fbc, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (nfb > 0) {
+        if (int rc = ensure_cand_buffers(h, h->tc, nfb)) return rc;
+        int rb = 0;
+        const void* ops = tc_plan_operands(h->tc, &rb);
+        CK(launch_gather_rows(ops, rb, h->perm, nfb, h->cand_X, (const float*)h->sx, h->cand_sx, s));
+        CK(cudaMemsetAsync(h->cand_cnt, 0, (size_t)nfb * 4, s));
+        CK(launch_cand_tc(h->tc, h->cand_X, nfb, h->guard, h->cand_sx, (const float*)h->cn,
+                          (const float*)h->sc, h->fb_thr, h->cand_cnt, h->cand, kCandQ, s));
+        CK(launch_cand_exact_mixed(h->dist, h->Xl, (const float*)h->Xw, h->Cl, (const float*)h->Cw,
+                                   (const float*)h->xn, (const float*)h->sx, (const float*)h->cn,
+                                   (const float*)h->sc, d, h->d_pad, delta2, h->perm, nfb,
+                                   h->cand_cnt, h->cand, kCandQ, h->labels, h->fbc + 1,
+                                   h->cand_left, h->cand_key, s));
+        int nleft = 0;
+        CK(cudaMemcpyAsync(&nleft, h->fbc + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (nleft > 0) {
+            // the full K6m-b evaluation of the remaining rows, on gathered copies
+            if (nleft > h->mix_cap) {
+                void* old[] = {h->mix_Xl, h->mix_Xw, h->mix_xn, h->mix_sx, h->mix_lab};
+                for (void* b : old)
+                    if (b) cudaFree(b);
+                const int64_t cap = std::min<int64_t>(h->n, (int64_t)nleft + nleft / 4 + 256);
+                CK(cudaMalloc(&h->mix_Xl, (size_t)cap * rb));
+                CK(cudaMalloc((void**)&h->mix_Xw, (size_t)cap * d * 4));
+                CK(cudaMalloc((void**)&h->mix_xn, (size_t)cap * 4));
+                CK(cudaMalloc((void**)&h->mix_sx, (size_t)cap * 4));
+                CK(cudaMalloc((void**)&h->mix_lab, (size_t)cap * 4));
+                h->mix_cap = cap;
+            }
+            CK(launch_gather_rows(ops, rb, h->cand_left, nleft, h->mix_Xl, (const float*)h->sx,
+                                  h->mix_sx, s));
+            CK(launch_gather_float_rows((const float*)h->Xw, d, h->cand_left, nleft, h->mix_Xw, s));
+            CK(launch_gather_float_rows((const float*)h->xn, 1, h->cand_left, nleft, h->mix_xn, s));
+            Problem pl{nleft, d, k, h->d_pad, h->guard};
+            unsigned long long* discard = nullptr;   // trigger counts come from mixed_count
+            CK(cudaMallocAsync((void**)&discard, sizeof(unsigned long long), s));
+            CK(launch_assign_mixed(h->work, h->dist, pl, h->delta, h->mix_Xl, h->mix_Xw, h->mix_xn,
+                                   h->mix_sx, h->Cl, h->Cw, h->cn, h->sc, h->mix_lab, nullptr,
+                                   nullptr, discard, s));
+            CK(cudaFreeAsync(discard, s));
+            CK(launch_scatter_labels(h->mix_lab, h->cand_left, nleft, h->labels, s));
+        }
+        h->last_fallback = nleft;
+    }
+    // SSE_t and the changed count from the final labels (Alg 4 distances of the labels)
+    if (acc_sse || acc_changed)
+        CK(launch_mixed_label_eval(h->dist, h->Xl, (const float*)h->Xw, h->Cl, (const float*)h->Cw,
+                                   (const float*)h->xn, (const float*)h->sx, (const float*)h->cn,
+                                   (const float*)h->sc, rows, d, h->d_pad, delta2, h->labels,
+                                   acc_changed ? h->mix_prev : nullptr, acc_sse, acc_changed, s));
+    return 0;
+}
+
 // Distance + argmin for the current centroids on h->n rows (loop iteration or assign).
 int run_assign(kmeans_ctx* h, int64_t rows, double* acc_sse, double* acc_changed) {
     Problem p{rows, h->d, h->k, h->d_pad, h->guard};
-    if (h->delta > 0.0) {   // Alg 4: per-pair precision switch (both dot products per pair)
+    if (h->delta > 0.0 && mixed_tc_ok(h)) {
+        if (int rc = assign_mixed_tc(h, rows, acc_sse, acc_changed)) return rc;
+    } else if (h->delta > 0.0) {   // Alg 4 on CUDA cores (both dot products per pair)
         CK(launch_assign_mixed(h->work, h->dist, p, h->delta, h->Xl, h->Xw, h->xn, h->sx, h->Cl,
                                h->Cw, h->cn, h->sc, h->labels, acc_sse, acc_changed,
                                h->n_low_dev, h->stream));
@@ -467,8 +602,6 @@ int prep_centroids(kmeans_ctx* h) {
 // the filter's argmin, which equals the working-precision argmin; the remaining rows are
 // re-evaluated by the CUDA-core kernel in working precision. Otherwise the CUDA-core kernel
 // evaluates every row.
-constexpr int kCandQ = 32;   // candidate columns kept per uncertified row
-
 int final_assign(kmeans_ctx* h, const Problem& pf) {
     cudaStream_t s = h->stream;
     const int64_t n = h->n;
@@ -652,6 +785,8 @@ int run_smalld_loop(kmeans_ctx* h, int max_iter, double tol, int* it_out, bool* 
         return launch_smalld_iter(h->work, h->dist, p, h->Xw, h->Cw, h->labels, h->loop_part,
                                   h->loop, h->trace, h->census + 2, st);
     };
+    CK(launch_smalld_iter(h->work, h->dist, p, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                          nullptr, s));                   // smem attribute, outside any capture
     if (!getenv("MPK_NO_GRAPH") && (!h->loop_graph || h->loop_graph_guard != h->guard)) {
         if (h->loop_graph) cudaGraphExecDestroy(h->loop_graph);
         h->loop_graph = nullptr;
@@ -1130,7 +1265,7 @@ int kmeans_set_delta(kmeans_handle h, double delta) {
         return fail(h, KMEANS_EINVAL, "delta must be 0 (off) or a finite value >= 1");
     h->delta = delta;
     // Alg 4 lines 1-5: the triggered pairs use the infinity-norm scaled operands
-    h->guard = delta > 0.0 ? 1 : h->guard_user;
+    h->guard = delta > 0.0 ? (h->guard_user ? h->guard_user : 1) : h->guard_user;
     return KMEANS_OK;
 }
 

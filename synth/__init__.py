@@ -152,6 +152,10 @@ CONFIGS = {
                              "fp64", ("fp64", "fp16"), ("none", "zscore")),
     "c2_image_512": Config("c2_image_512", "image", 512 * 512, 3, 5, 5, work="fp32",
                            dists=("fp16",), norms=("minmax",)),
+    # supplementary (not a BASELINE config): the C2 image at 4096 x 4096 = 16.8M pixels (201 MB
+    # of fp32), large enough that the small-d kernel streams from HBM instead of L2
+    "c2_image_4096": Config("c2_image_4096", "image", 4096 * 4096, 3, 5, 5, work="fp32",
+                            dists=("fp16",), norms=("minmax",), extra={"h": 4096, "w": 4096}),
     "c3_blobs_1m_d64": Config("c3_blobs_1m_d64", "blobs", 1_000_000, 64, 256, 256,
                               (-10.0, 10.0), 1.0, "fp32", ("fp16", "bf16"), ("zscore",)),
     "c4_blobs_1m_large": Config("c4_blobs_1m_large", "blobs", 1_000_000, 32, 64, 64,
@@ -173,7 +177,8 @@ def make(cfg: Config | str, n: int | None = None, seed: int = 0, dtype=None,
         cfg = CONFIGS[cfg]
     dtype = dtype or (np.float64 if cfg.work == "fp64" else np.float32)
     if cfg.kind == "image":
-        X, y = image(seed=seed, dtype=dtype)
+        X, y = image(h=cfg.extra.get("h", 512), w=cfg.extra.get("w", 512), seed=seed,
+                     dtype=dtype)
         if n is not None:
             X, y = X[:n].copy(), y[:n].copy()
         C0 = init_rows(X, cfg.k, seed)

@@ -271,3 +271,12 @@ def test_tc_nonfinite_rows_match_the_scan(dist):
     ref, _, _ = oracle.assign(X, C, work="fp32", dist=dist, guard=False)
     assert g[0] == 0
     assert np.array_equal(g[:4], ref[:4]), (g[:4], ref[:4])
+
+
+@pytest.mark.parametrize("dist", ["fp16", "e5m2"])
+@pytest.mark.parametrize("shape", [(4099, 128, 1024), (3001, 32, 64), (1500, 16, 40)])
+def test_tc_guard_pow2_matches_oracle(dist, shape):
+    """Reading Z9 B (KMEANS_GUARD_POW2, s = 2^ceil(log2 ||x||_inf)) on the tensor-core kernels,
+    label by label against the oracle's O2 with the same reading."""
+    n, d, k = shape
+    _assign_vs_oracle(n, d, k, dist, "pow2", n + 3 * d + k)

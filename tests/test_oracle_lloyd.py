@@ -360,3 +360,29 @@ def test_iteration_counting_and_tol():
     assert r["iters"] == 2 and r["changed_t"].tolist() == [4, 0]   # no label changed
     r = oracle.fit(X, [[0.5], [10.5]], max_iter=7, tol=-1.0)
     assert r["iters"] == 7
+
+
+def test_guard_pow2_reading_b():
+    """Reading Z9 B (KMEANS_GUARD_POW2): s = 2^ceil(log2 ||x||_inf) — a power of two in
+    [||x||_inf, 2 ||x||_inf) — so x / s is exact and x~ = round_l(x / s). Pins: (1) the scale by
+    value; (2) where every infinity norm is a power of two, B equals A bit for bit; (3) scaling
+    by a power of two commutes with rounding, so away from the format's subnormal and overflow
+    ranges the significands of x~ are those of round_l(x): B changes nothing but the exponent
+    range (the MX block scale's only effect)."""
+    X = np.array([[3.0, -4.0, 1.0], [0.75, 0.5, -0.25], [0.0, 0.0, 0.0], [5.0, 1.0, 1.0]])
+    xl, nrm, sc = oracle.prep(X, work="fp32", dist="fp16", guard="pow2")
+    assert sc.tolist() == [4.0, 1.0, 1.0, 8.0]
+    assert np.array_equal(xl[0], [0.75, -1.0, 0.25])
+    assert np.array_equal(xl[3], [0.625, 0.125, 0.125])
+    rng = np.random.default_rng(31)
+    P = rng.standard_normal((300, 9))
+    P[:, 0] = np.sign(P[:, 0]) * 2.0 ** rng.integers(1, 6, 300)   # the max is a power of 2
+    P[:, 1:] = np.clip(P[:, 1:], -1.9, 1.9)
+    a = oracle.prep(P, work="fp64", dist="e5m2", guard=True)
+    b = oracle.prep(P, work="fp64", dist="e5m2", guard="pow2")
+    assert all(np.array_equal(u, v) for u, v in zip(a, b))
+    Q = rng.uniform(0.05, 1.0, (400, 3)) * rng.choice([-1, 1], (400, 3))
+    ql, _, _ = oracle.prep(Q, work="fp64", dist="e5m2", guard=False)
+    pl, _, ps = oracle.prep(Q, work="fp64", dist="e5m2", guard="pow2")
+    assert np.all(np.log2(ps) == np.round(np.log2(ps)))
+    np.testing.assert_array_equal(pl * ps[:, None], ql)
