@@ -15,8 +15,9 @@
 // launch instead of three launches, a memset and a host round trip.
 // Rows (and the previous labels) stream through shared memory in a ring of kStages tiles of
 // kTileRows rows filled by 1-D bulk copies (the TMA engine), so the next tiles' HBM reads overlap
-// this tile's arithmetic; each thread's 8 rows of a tile are summed in fp32 and then added to its
-// fp64 totals (reading R1).
+// this tile's arithmetic; each thread's rows of up to 4 tiles (<= 32 rows) are summed in fp32, then
+// converted to fp64 and reduced by a warp tree into the warp's fp64 totals (DESIGN.md reading
+// R1 / R11): a fixed order.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -37,6 +38,7 @@ constexpr int LD = 4, LK = 8, LT = 256;
 #endif
 constexpr int kTileRows = MPK_SL_TILE;   // rows per pipeline stage (8 per thread)
 constexpr int kStages = 3;           // tiles in flight per block (bulk copies)
+constexpr int kFlushTiles = 4;       // tiles per per-thread partial (<= 32 rows)
 constexpr int NV = LK * LD + LK + 2;   // sums, counts, sse, changed
 constexpr int kRedGroups = LT / NV;    // the last block reduces the partials in this many groups
 
@@ -82,7 +84,7 @@ smalld_iter_kernel(Problem p, const W* __restrict__ X, W* __restrict__ C,
     W* xs0 = reinterpret_cast<W*>(dsm);                                   // [kStages][rows*d]
     int32_t* ls0 = reinterpret_cast<int32_t*>(dsm + kStages * xbytes);   // [kStages][rows]
     __shared__ AT cl_s[LK][LD];
-    __shared__ W cn_s[LK], sc_s[LK];
+    __shared__ W cn_s[LK], sc_s[LK], m2_s[LK];
     __shared__ double red[LT / 32][NV];
     __shared__ __align__(8) uint64_t full[kStages];
     __shared__ int is_last;
@@ -146,6 +148,7 @@ smalld_iter_kernel(Problem p, const W* __restrict__ X, W* __restrict__ C,
         if (lane == 0) {
             cn_s[w] = rounder<WORK>::from(acc);
             sc_s[w] = s;
+            m2_s[w] = (W)-2 * s;
         }
         if (blockIdx.x == 0 && census) {
             nf = warp_sum(nf);
@@ -155,17 +158,15 @@ smalld_iter_kernel(Problem p, const W* __restrict__ X, W* __restrict__ C,
     }
     __syncthreads();
 
-    double sums[KT][D];
-    double cnts[KT];
-#pragma unroll
-    for (int j = 0; j < KT; ++j) {
-        cnts[j] = 0.0;
-#pragma unroll
-        for (int t = 0; t < D; ++t) sums[j][t] = 0.0;
-    }
+    // the block's running totals per warp (fp64, in shared memory: red[w][.]); each tile's
+    // per-thread partials are converted to fp64 and reduced by a warp tree into them
+    for (int q = lane; q < NV; q += 32) red[w][q] = 0.0;
     double my_sse = 0.0, my_changed = 0.0;
 
     // ---- A4 + A5 over this block's tiles -----------------------------------------------------
+    // per-thread partials of up to kFlushTiles tiles (<= 32 rows) in the working precision, then
+    // fp64 (reading R1; fp64 work: fp64 throughout)
+    W ps[KT][D], pc[KT];
     for (int64_t m = 0; m < my_tiles; ++m) {
         const int stg = (int)(m % kStages);
         const int rows = tile_rows(m);
@@ -179,14 +180,13 @@ smalld_iter_kernel(Problem p, const W* __restrict__ X, W* __restrict__ C,
             for (int q = tid; q < rows; q += LT) ls[q] = labels[r0 + q];
             __syncthreads();
         }
-        // this tile's sums: partials of the thread's 8 rows in the working precision (fp32
-        // partials of 8 rows, then fp64: reading R1; fp64 work: fp64 throughout)
-        W ps[KT][D], pc[KT];
+        if (m % kFlushTiles == 0) {
 #pragma unroll
-        for (int j = 0; j < KT; ++j) {
-            pc[j] = (W)0;
+            for (int j = 0; j < KT; ++j) {
+                pc[j] = (W)0;
 #pragma unroll
-            for (int t = 0; t < D; ++t) ps[j][t] = (W)0;
+                for (int t = 0; t < D; ++t) ps[j][t] = (W)0;
+            }
         }
         for (int r = tid; r < rows; r += LT) {
             const int64_t i = r0 + r;
@@ -207,22 +207,24 @@ smalld_iter_kernel(Problem p, const W* __restrict__ X, W* __restrict__ C,
                 s = guard_scale(amax, p.guard);
             }
             AT xl[D];
+            if (s == (W)1) {                           // no scaling: no division issued
 #pragma unroll
-            for (int t = 0; t < D; ++t) {
-                const W q = (s == (W)1) ? x[t] : x[t] / s;
-                xl[t] = (AT)widen(rounder<DIST>::from(q));
+                for (int t = 0; t < D; ++t) xl[t] = (AT)widen(rounder<DIST>::from(x[t]));
+            } else {
+#pragma unroll
+                for (int t = 0; t < D; ++t) xl[t] = (AT)widen(rounder<DIST>::from(x[t] / s));
             }
             W best = (W)INFINITY;
             int bj = 0;
 #pragma unroll
             for (int j = 0; j < KT; ++j) {
-                if (j < k) {
-                    AT dot = (AT)0;
+                if (j >= k) break;                     // uniform: no predicated columns
+                AT dot = (AT)0;
 #pragma unroll
-                    for (int t = 0; t < D; ++t) dot = fma(xl[t], cl_s[j][t], dot);
-                    const W v = fma((W)-2 * (s * sc_s[j]), (W)dot, cn_s[j]);
-                    if (v < best) { best = v; bj = j; }
-                }
+                for (int t = 0; t < D; ++t) dot = fma(xl[t], cl_s[j][t], dot);
+                // -2 (s s_j) = s (-2 s_j) exactly (a power-of-two factor)
+                const W v = fma(s * m2_s[j], (W)dot, cn_s[j]);
+                if (v < best) { best = v; bj = j; }
             }
             if (ls[r] != bj) my_changed += 1.0;
             labels[i] = bj;
@@ -230,32 +232,30 @@ smalld_iter_kernel(Problem p, const W* __restrict__ X, W* __restrict__ C,
             my_sse += md > 0.0 ? md : 0.0;
 #pragma unroll
             for (int j = 0; j < KT; ++j) {
+                if (j >= k) break;
                 const W hit = (bj == j) ? (W)1 : (W)0;
                 pc[j] += hit;
 #pragma unroll
                 for (int t = 0; t < D; ++t) ps[j][t] = fma(hit, x[t], ps[j][t]);
             }
         }
+        if (m % kFlushTiles == kFlushTiles - 1 || m == my_tiles - 1) {
 #pragma unroll
-        for (int j = 0; j < KT; ++j) {
-            cnts[j] += (double)pc[j];
+            for (int j = 0; j < KT; ++j) {
+                if (j >= k) break;                     // uniform
+                const double c = warp_sum((double)pc[j]);
+                if (lane == 0) red[w][LK * LD + j] += c;
 #pragma unroll
-            for (int t = 0; t < D; ++t) sums[j][t] += (double)ps[j][t];
+                for (int t = 0; t < D; ++t) {
+                    const double v = warp_sum((double)ps[j][t]);
+                    if (lane == 0) red[w][j * LD + t] += v;
+                }
+            }
         }
         __syncthreads();                               // every thread is done with this stage
         if (tid == 0 && m + kStages < my_tiles) issue(m + kStages);
     }
-    // ---- block partial (warp shuffles, then warps in order) ---------------------------------
-#pragma unroll
-    for (int j = 0; j < LK; ++j) {
-#pragma unroll
-        for (int t = 0; t < LD; ++t) {
-            const double v = (j < KT && t < D) ? warp_sum(sums[j < KT ? j : 0][t < D ? t : 0]) : 0.0;
-            if (lane == 0) red[w][j * LD + t] = v;
-        }
-        const double c = j < KT ? warp_sum(cnts[j < KT ? j : 0]) : 0.0;
-        if (lane == 0) red[w][LK * LD + j] = c;
-    }
+    // ---- block partial (the warps' totals in order) ------------------------------------------
     my_sse = warp_sum(my_sse);
     my_changed = warp_sum(my_changed);
     if (lane == 0) { red[w][NV - 2] = my_sse; red[w][NV - 1] = my_changed; }
