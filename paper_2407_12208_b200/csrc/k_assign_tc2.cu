@@ -64,6 +64,12 @@ constexpr int P_NON_EPI = 4;
 #ifndef MPK_PAIR_HSPLIT
 #define MPK_PAIR_HSPLIT 1                // ASSIGN NB=256: four 128-column accumulators (below)
 #endif
+#ifndef MPK_PAIR_CNINIT
+#define MPK_PAIR_CNINIT 0                // fp16/bf16 ASSIGN: accumulators pre-loaded with ||c||^2/2 (slower: DESIGN §7)
+#endif
+#ifndef MPK_PAIR_CNINIT_EARLY
+#define MPK_PAIR_CNINIT_EARLY 1
+#endif
 #ifndef MPK_PAIR_HOT_WAIT
 #define MPK_PAIR_HOT_WAIT 1              // epilogue: test_wait before a bare try_wait loop
 #endif
@@ -132,7 +138,8 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
     uint8_t* a_base = b_base + (size_t)p.NT * p.b_half_bytes;           // X~ ring
     float* cn_s = (float*)(a_base + (size_t)p.SA * p.a_tile_bytes);
     float* sc_s = cn_s + p.k_pad;
-    uint64_t* bars = (uint64_t*)(((uintptr_t)(sc_s + p.k_pad) + 7) & ~(uintptr_t)7);
+    float* cnh_s = sc_s + p.k_pad;                  // ||c||^2 / 2 (the pre-loaded accumulators)
+    uint64_t* bars = (uint64_t*)(((uintptr_t)(cnh_s + p.k_pad) + 7) & ~(uintptr_t)7);
     uint64_t* a_full = bars;
     uint64_t* a_empty = a_full + p.SA;
     uint64_t* b_full = a_empty + p.SA;
@@ -166,13 +173,26 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
     // pipeline already binds), so fp16 keeps one 256-column MMA per tile.
     const bool hsplit = MODE == PAIR_ASSIGN && MPK_PAIR_HSPLIT && p.NB == 256 && P_EWG == 2 &&
                         p.tmem_cols >= 512 && p.is_f8;
-    const bool fwd = !hsplit && MODE == PAIR_ASSIGN && MPK_PAIR_FWD && p.NB == 256 && p.nacc == 2 && (P_EWG == 2 || P_EWG == 4) &&
+    // "cn init" (fp16/bf16 ASSIGN, 256-column tiles, no guard): each accumulator is pre-loaded
+    // with ||c_j||^2 / 2 by the epilogue (tcgen05.st, after it has read the previous tile from
+    // it) and the MMA adds x~ . (-c~) (B negated in the instruction descriptor), so the
+    // accumulator holds v_j / 2 = ||c_j||^2 / 2 - x~.c~_j and the fold needs no per-column fma
+    // with ||c||^2. Measured at C5 fp16: the fold's FFMA2 and ||c||^2 loads are ~11 % of the
+    // kernel (MPK_PAIR_DBG=4 probe: 2.25 vs 2.53 ms), but writing the pre-load back into TMEM
+    // (tcgen05.st, as much TMEM write traffic as the MMA's) costs more: 2.59-2.64 vs 2.47-2.51 ms
+    // with the release before or after the last chunk's fold. Off by default; correct either way
+    // (the parity tests pass with it on).
+    const bool cninit = MPK_PAIR_CNINIT && !hsplit && MODE == PAIR_ASSIGN && p.NB == 256 &&
+                        p.nacc == 2 && P_EWG == 2 && !p.is_f8 && MPK_PAIR_ACC_DBUF && !p.guard &&
+                        !(p.dbg & 7);
+    const bool fwd = !cninit && !hsplit && MODE == PAIR_ASSIGN && MPK_PAIR_FWD && p.NB == 256 && p.nacc == 2 && (P_EWG == 2 || P_EWG == 4) &&
                      !p.is_f8 &&
                      MPK_PAIR_ACC_DBUF && !p.guard;
 
     for (int j = threadIdx.x; j < p.k_pad; j += blockDim.x) {
         cn_s[j] = j < p.k ? p.cn[j] : INFINITY;       // padded centroids never win
         sc_s[j] = (p.guard && j < p.k) ? p.sc[j] : 1.0f;
+        cnh_s[j] = 0.5f * cn_s[j];                 // exact (a power-of-two factor)
     }
     if (threadIdx.x == 0) {
         for (int i = 0; i < p.SA; ++i) { mbar_init(smem_u32(&a_full[i]), 1); mbar_init(smem_u32(&a_empty[i]), 1); }
@@ -183,7 +203,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             mbar_init(smem_u32(&t_full[i]), 1);
             // one arrival per CTA (named barrier first), one per epilogue warp, or (half split)
             // one per warp of the owning warpgroup
-            mbar_init(smem_u32(&t_empty[i]), hsplit ? 8 : ((fwd || !MPK_PAIR_WARP_ARRIVE) ? 2 : 2 * P_EPI));
+            mbar_init(smem_u32(&t_empty[i]), hsplit ? 8 : ((fwd || (!MPK_PAIR_WARP_ARRIVE && !cninit)) ? 2 : 2 * P_EPI));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x)) : "memory");
@@ -273,7 +293,10 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             mbar_wait(smem_u32(b_full), 0);
             tc_fence_after();
             int slot = 0, buf = 0;
-            uint32_t aph = 0, tph = 0, ai = 0;
+            // cn init: the first use of each accumulator waits for the epilogue's pre-load (its
+            // first release), so the phase bit starts flipped
+            uint32_t aph = 0, tph = cninit ? 1u : 0u, ai = 0;
+            const uint32_t idesc_use = cninit ? (idesc | (1u << 14)) : idesc;   // B negated
             if (hsplit) {
                 const uint32_t idesc128 = (idesc & ~(0x3Fu << 17)) | ((128u >> 3) << 17);
                 const uint32_t h16 = (64u * (uint32_t)p.SWZ) >> 4;   // 64 centroid rows
@@ -330,9 +353,9 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                                 for (int ks = 0; ks < ksteps; ++ks) {
                                     const uint64_t ad = desc_join(dhi, a_lo + kb * kb_a16 + ks * 2);
                                     const uint64_t bd = desc_join(dhi, b_lo + kb * kb_b16 + ks * 2);
-                                    const uint32_t accum = (kb | ks) ? 1u : 0u;
-                                    if (f8) mma2_f8(d_tmem, ad, bd, idesc, accum);
-                                    else mma2_f16(d_tmem, ad, bd, idesc, accum);
+                                    const uint32_t accum = (cninit || (kb | ks)) ? 1u : 0u;
+                                    if (f8) mma2_f8(d_tmem, ad, bd, idesc_use, accum);
+                                    else mma2_f16(d_tmem, ad, bd, idesc_use, accum);
                                 }
                             }
                         }
@@ -487,6 +510,34 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             return (CAND && rb < num_rb && r < n) ? p.thr[r] : NAN;
         };
         float m2_n = pt_m2(pair), T_n = pt_T(pair);
+        // cn init: write ||c_j||^2 / 2 of centroid tile tb into this warp's 32-column chunk i of
+        // accumulator b (the same value in all 32 TMEM lanes of the warp)
+        const int64_t my_tiles = my_rbs * (int64_t)NT;
+        auto cn_init_chunk = [&](int b, int tb, int i) {
+            uint32_t r[32];
+            const uint32_t src = smem_u32(cnh_s + tb * NB + col_off + i * 32);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const float4 f = lds_f4(src + 16 * e);
+                r[4 * e + 0] = __float_as_uint(f.x); r[4 * e + 1] = __float_as_uint(f.y);
+                r[4 * e + 2] = __float_as_uint(f.z); r[4 * e + 3] = __float_as_uint(f.w);
+            }
+            tmem_st32(tmem_base + lane_addr + (uint32_t)b * NB + col_off + i * 32, r);
+        };
+        if (cninit) {
+            // the first use of each accumulator: pre-load, then release it (the MMA warp's first
+            // wait on "accumulator empty" is for this release)
+            for (int b = 0; b < nacc; ++b) {
+                if (b < my_tiles) {
+                    const int tb = NT - 1 - (b % NT);
+                    for (int i = 0; i < 4; ++i) cn_init_chunk(b, tb, i);
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&t_empty[b]), 0));
+            }
+        }
         for (int64_t rb = pair; rb < num_rb; rb += npairs, ++rbi) {
             const int64_t row = rb * rows_per_rb + rank * P_BM + q;
             const float m2 = m2_n;
@@ -638,6 +689,58 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                                 fold_rev_m3s<4, GD>(va, q, m2, cv, cs);
                                 return;
                             }
+                            if (!GD && nch == 4 && c == wcols && cninit) {
+                                // pre-loaded accumulators: fold the values as they are and
+                                // pre-load each chunk for this accumulator's next tile (ai + 2)
+                                const bool nxt = ai + nacc < my_tiles;
+                                const int tbn = NT - 1 - (int)((t + nacc) % NT);
+                                uint32_t vb[32];
+                                tmem_ld32(col0 + 96, va);
+                                tmem_wait_ld_dep(va);
+                                tmem_ld32(col0 + 64, vb);
+                                fold_rev_m3_direct<4>(va, cv, s2);
+                                if (nxt) cn_init_chunk(buf, tbn, 3);
+                                tmem_wait_ld_dep(vb);
+                                tmem_ld32(col0 + 32, va);
+                                fold_rev_m3_direct<4>(vb, cv, s2);
+                                if (nxt) cn_init_chunk(buf, tbn, 2);
+                                tmem_wait_ld_dep(va);
+                                tmem_ld32(col0, vb);
+                                fold_rev_m3_direct<4>(va, cv, s2);
+                                if (nxt) cn_init_chunk(buf, tbn, 1);
+                                tmem_wait_ld_dep(vb);
+                                if (nxt) cn_init_chunk(buf, tbn, 0);
+#if MPK_PAIR_CNINIT_EARLY
+                                // release before the last chunk's fold (as the fwd path does)
+                                tmem_wait_st();
+                                tc_fence_before();
+                                __syncwarp();
+                                if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&t_empty[buf]), 0));
+#endif
+                                fold_rev_m3_direct<4>(vb, cv, s2);
+                                return;
+                            }
+                            if (MPK_PAIR_ACC_DBUF && !GD && nch == 4 && c == wcols && (dbg & 4)) {
+                                // timing probe: the fold without ||c||^2 and the -2 factor
+                                uint32_t vb[32];
+                                tmem_ld32(col0 + 96, va);
+                                tmem_wait_ld_dep(va);
+                                tmem_ld32(col0 + 64, vb);
+                                fold_rev_m3_direct<4>(va, cv, s2);
+                                tmem_wait_ld_dep(vb);
+                                tmem_ld32(col0 + 32, va);
+                                fold_rev_m3_direct<4>(vb, cv, s2);
+                                tmem_wait_ld_dep(va);
+                                tmem_ld32(col0, vb);
+                                fold_rev_m3_direct<4>(va, cv, s2);
+                                tmem_wait_ld_dep(vb);
+                                if (fwd) {
+                                    tc_fence_before();
+                                    named_bar_arrive(BAR_REL + buf, P_EPI * 32 + 32);
+                                }
+                                fold_rev_m3_direct<4>(vb, cv, s2);
+                                return;
+                            }
                             if (MPK_PAIR_ACC_DBUF && !GD && nch == 4 && c == wcols) {
                                 // NB = 256: four chunks unrolled, the TMEM load of the next chunk
                                 // in flight while this one folds (the load's ~180-cycle latency
@@ -712,7 +815,11 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 if (tr) trace[ai * 8 + 3] = clock64();
                 // one arrival per CTA: the epilogue warps meet at a named barrier, then a single
                 // thread signals the leader's "accumulator empty"
+                if (cninit) tmem_wait_st();            // the pre-load is in TMEM before the release
                 tc_fence_before();
+                if (cninit && MPK_PAIR_CNINIT_EARLY) {
+                    // released before the last chunk's fold (above)
+                } else
                 if (fwd) {
                     // released through warp 2 before the last chunk's fold (debug mode without
                     // the fold: here)
@@ -775,7 +882,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             const int par = (int)(rbi & 1);
             if (rbi >= 2) mbar_wait_hot(smem_u32(&part_free[par]), (uint32_t)((rbi >> 1) - 1) & 1u);
             const int slot = (par * P_EWG + wg) * P_BM + q;
-            part_v[slot] = b1;
+            part_v[slot] = cninit ? 2.0f * b1 : b1;    // cn init: the chains held v / 2 (exact)
             part_j[slot] = j1;
             if (FINAL) part_v2[slot] = b2;
             named_bar_arrive(BAR_PART + par, P_EPI * 32 + 32);
@@ -809,7 +916,7 @@ bool pair_plan(int dist, int d, int d_pad, int k, PairParams* pp, size_t* smem_b
     const size_t a_tile = (size_t)P_BM * RB;
     // static shared (the warp-3 partial buffers) counts against the same 227 KB
     const size_t stat = 3 * 2 * P_EWG * P_BM * 4;
-    const size_t fixed = 1024 + stat + (size_t)k_pad * 8 + 8 +
+    const size_t fixed = 1024 + stat + (size_t)k_pad * 12 + 8 +
                          (size_t)(2 * 8 + 1 + 2 * P_MAX_ACC) * 8 + 16;
     const size_t bres = (size_t)NT * b_half;
     if (fixed + bres + 2 * a_tile > P_BUDGET) return false;

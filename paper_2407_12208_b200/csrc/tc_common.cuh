@@ -116,6 +116,19 @@ MPK_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[32]) {
         : "r"(taddr));
 }
 MPK_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+MPK_DEV void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+        "%28, %29, %30, %31, %32};"
+        ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+          "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]),
+          "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]),
+          "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+          "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+MPK_DEV void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 // wait::ld that also "defines" r, so the compiler cannot schedule reads of a prefetched
 // tcgen05.ld destination above the wait (needed when loads are double-buffered)
 MPK_DEV void tmem_wait_ld_dep(uint32_t (&r)[32]) {
@@ -366,6 +379,30 @@ MPK_DEV void fold_rev_m3(const uint32_t (&v)[32], const ChunkCn<G, GUARD>& q, fl
                 }
                 x2[h][2 * qq + 0] = fma2(pack2u(v[col + 0], v[col + 1]), s01, pack2(cc.x, cc.y));
                 x2[h][2 * qq + 1] = fma2(pack2u(v[col + 2], v[col + 3]), s23, pack2(cc.z, cc.w));
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < NCH / 2; ++m)
+            chain_pair_x2(x2[0][m], x2[1][m], cv[2 * m], cv[2 * m + 1], s2[m], m1);
+    }
+}
+// Fold of an accumulator that already holds the (halved) distance ||c_j||^2 / 2 - x~.c~_j (the
+// pair kernel's pre-loaded mode, k_assign_tc2.cu "cn init"): the values enter the chains as they
+// are, no fma with ||c||^2 per column.
+template <int G>
+MPK_DEV void fold_rev_m3_direct(const uint32_t (&v)[32], float (&cv)[NCH], uint64_t (&s2)[NCH / 2]) {
+    const uint64_t m1 = pack2(-1.0f, -1.0f);
+#pragma unroll
+    for (int gp = G / 2 - 1; gp >= 0; --gp) {
+        uint64_t x2[2][4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int g = 2 * gp + 1 - h;
+#pragma unroll
+            for (int qq = 0; qq < 2; ++qq) {
+                const int col = 8 * g + 4 * qq;
+                x2[h][2 * qq + 0] = pack2u(v[col + 0], v[col + 1]);
+                x2[h][2 * qq + 1] = pack2u(v[col + 2], v[col + 3]);
             }
         }
 #pragma unroll
