@@ -3,9 +3,12 @@
 One process per GPU. Rows are split into contiguous shards; the library's handles
 (kmeans_create_dist) own an NCCL communicator created from a unique id that rank 0 generates and
 this module broadcasts over the torch.distributed process group. Per Lloyd iteration the library
-issues ONE ncclAllReduce(sum) over a packed fp64 buffer laid out as
+exchanges, with fp32 work (the exact fixed-point update, R9), the int64 totals of the
+grid integers (two k*d arrays) and the int32 counts in one NCCL group, plus [SSE_t, #changed] in
+fp64; with fp64 work one fp64 allreduce of the packed buffer
     [ sums (k*d) | counts (k) | SSE_t | #changed | reserved (2) ]
-(AccLayout in csrc/internal.h), after which every rank finalises identical centroids.
+(AccLayout in csrc/internal.h). Every rank then finalises identical centroids. The same exchange
+can run between virtual ranks on one GPU (kmeans_vgroup_create / kmeans_create_virtual).
 This module only moves bytes and indices; every numeric step runs in the CUDA library.
 """
 from __future__ import annotations
