@@ -266,11 +266,15 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             else mbar_wait(smem_u32(&a_empty[slot]), ph ^ 1);
             if (elect_one()) {
                 const uint32_t fb = smem_u32(&a_full[slot]);
-                if (leader) mbar_expect_tx(fb, 2u * a_tile);
-                const uint32_t dst = a0 + slot * a_tile;
-                const int row0 = (int)(rb * rows_per_rb + rank * P_BM);
-                for (int kb = 0; kb < KB; ++kb)
-                    tma_load_2d_pair(dst + kb * kb_a, &tmap_x, kb * eps, row0, fb);
+                if (dbg & 8) {                         // debug timing: no X~ loads
+                    if (leader) mbar_arrive(fb);
+                } else {
+                    if (leader) mbar_expect_tx(fb, 2u * a_tile);
+                    const uint32_t dst = a0 + slot * a_tile;
+                    const int row0 = (int)(rb * rows_per_rb + rank * P_BM);
+                    for (int kb = 0; kb < KB; ++kb)
+                        tma_load_2d_pair(dst + kb * kb_a, &tmap_x, kb * eps, row0, fb);
+                }
             }
             __syncwarp();
             if (++slot == SA) { slot = 0; ph ^= 1; }
@@ -411,6 +415,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             named_bar_sync(BAR_PART + par, P_EPI * 32 + 32);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
+                if (dbg & 16) break;                   // debug timing: no row-block end work
                 const int q = u * 32 + lane;
                 const int s0 = (par * P_EWG + 0) * P_BM + q;
                 float b1 = part_v[s0], b2 = FINAL ? part_v2[s0] : INFINITY;

@@ -277,9 +277,17 @@ smalld_iter_kernel(Problem p, const W* __restrict__ X, W* __restrict__ C,
     // in increasing b (independent loads in flight), then the groups are added in order
     if (tid < NV * kRedGroups) {
         const int c = tid % NV, g = tid / NV;
+        // at most ceil(148 / 6) = 25 blocks per group: every load is issued before the adds
+        constexpr int kMaxPer = (kNumSMs + kRedGroups - 1) / kRedGroups;
+        double v[kMaxPer];
+#pragma unroll
+        for (int q = 0; q < kMaxPer; ++q) {
+            const unsigned b = g + q * kRedGroups;
+            v[q] = b < gridDim.x ? __ldcg(part + (size_t)b * NV + c) : 0.0;
+        }
         double a = 0.0;
-#pragma unroll 4
-        for (unsigned b = g; b < gridDim.x; b += kRedGroups) a += __ldcg(part + (size_t)b * NV + c);
+#pragma unroll
+        for (int q = 0; q < kMaxPer; ++q) a += v[q];
         red[g][c] = a;
     }
     __syncthreads();

@@ -30,7 +30,8 @@ struct PairParams {
     int* cand_cnt;           // CAND: per row, number of candidates found
     int* cand;               // CAND: [n][cand_q] candidate columns
     int cand_q;
-    int dbg;                 // debug: bit0 skip epilogue folding, bit1 skip MMAs (timing only)
+    int dbg;                 // debug (timing only): bit0 skip the fold, bit1 skip MMAs, bit2 fold probe,
+                             // bit3 skip the X~ loads, bit4 skip the row-block end work
     unsigned long long* trace;   // debug (MPK_PAIR_TRACE): per-tile clock64 stamps of CTA 0
 };
 
