@@ -63,6 +63,50 @@ MPK_DEV float dot16_full(uint4 q, const float* __restrict__ cs, int t0, float ac
     return acc;
 }
 
+// One warp, 32 rows whose operand rows are G 16-byte chunks (G a power of two <= 16): load i of
+// lane l reads chunk l % G of row i (32 / G) + l / G, so every load instruction covers 32 / G
+// whole rows, 512 contiguous bytes; each lane multiplies its chunk with the same chunk of the
+// centre (held in registers) for its G rows, and a butterfly over the G lanes of a row group
+// (keep half, send half: G - 1 shuffles in all) leaves lane l with the full dot of row
+// (l % G) (32 / G) + l / G. The dot is summed in a fixed tree instead of sequentially: within
+// the same gamma_d bound the parity tests use.
+template <int G, typename LT, typename A>
+MPK_DEV A seed_batch_dot(const LT* __restrict__ Xl, int64_t row0, int d_pad, int rows_left,
+                         const A (&cr)[16 / sizeof(LT)], int lane) {
+    constexpr int m = 16 / (int)sizeof(LT);
+    constexpr int RPI = 32 / G;                    // rows per load instruction
+    const int q = lane & (G - 1), sgrp = lane / G;
+    uint4 buf[G];
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+        const int r = i * RPI + sgrp;
+        buf[i] = r < rows_left
+                     ? __ldg(reinterpret_cast<const uint4*>(Xl + (row0 + r) * d_pad) + q)
+                     : make_uint4(0, 0, 0, 0);
+    }
+    A part[G];
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+        LT e[m];
+        memcpy(e, &buf[i], 16);
+        A acc = (A)0;
+#pragma unroll
+        for (int u = 0; u < m; ++u) acc = fma((A)widen(e[u]), cr[u], acc);
+        part[i] = acc;
+    }
+#pragma unroll
+    for (int o = G / 2; o >= 1; o >>= 1) {
+        const bool upper = (lane & o) != 0;
+#pragma unroll
+        for (int u = 0; u < o; ++u) {
+            const A send = upper ? part[u] : part[u + o];
+            const A keep = upper ? part[u + o] : part[u];
+            part[u] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    return part[0];
+}
+
 template <typename LT, typename W>
 __global__ void __launch_bounds__(kSeedThreads, 2)
 seed_update_kernel(const LT* __restrict__ Xl, int64_t n, int d, int d_pad,
@@ -86,6 +130,40 @@ seed_update_kernel(const LT* __restrict__ Xl, int64_t n, int d, int d_pad,
     const int chunks = (d_pad * (int)sizeof(LT)) / 16;
     constexpr int m = 16 / (int)sizeof(LT);
     constexpr int QB = 16;                          // 16-byte chunks of a row in flight
+    const int G = vec ? chunks : 0;
+    if (G == 2 || G == 4 || G == 8 || G == 16) {
+        // the coalesced path: warps take 32-row batches, rows loaded "transposed"
+        const int q = lane & (G - 1);
+        A cr[m];
+#pragma unroll
+        for (int u = 0; u < m; ++u) cr[u] = cs[q * m + u];
+        const int warp = threadIdx.x >> 5, nw = kSeedThreads / 32;
+        for (int base = warp * 32; base < rows; base += nw * 32) {
+            const int rpi = 32 / G;
+            const int r = (lane & (G - 1)) * rpi + lane / G;      // this lane's row after the reduce
+            const bool mine = base + r < rows;
+            const int64_t i = b0 + base + r;
+            const double old = mine ? D2[i] : 0.0;
+            const W xni = mine ? xn[i] : (W)0;
+            const W si_w = (mine && guard) ? sx[i] : (W)1;
+            A dot;
+            switch (G) {
+                case 2: dot = seed_batch_dot<2, LT, A>(Xl, b0 + base, d_pad, rows - base, cr, lane); break;
+                case 4: dot = seed_batch_dot<4, LT, A>(Xl, b0 + base, d_pad, rows - base, cr, lane); break;
+                case 8: dot = seed_batch_dot<8, LT, A>(Xl, b0 + base, d_pad, rows - base, cr, lane); break;
+                default: dot = seed_batch_dot<16, LT, A>(Xl, b0 + base, d_pad, rows - base, cr, lane); break;
+            }
+            if (mine) {
+                const double si = (double)si_w;
+                double D = ((double)xni - 2.0 * (si * scc) * (double)dot) + xnc;
+                D = D > 0.0 ? D : 0.0;                  // NaN -> 0
+                if (i == c) D = 0.0;                    // the centre's own weight
+                const double nw2 = D < old ? D : old;
+                D2[i] = nw2;
+                d2s[base + r] = nw2;
+            }
+        }
+    } else
     // one row per thread: the whole row's 16-byte chunks are loaded before they are used (a
     // warp keeps 32 rows, 8 KB at d = 128 fp16, in flight); the dot is the sequential fp32 sum
     for (int r = threadIdx.x; r < rows; r += blockDim.x) {
