@@ -16,6 +16,7 @@
 #include "common.cuh"
 #include "internal.h"
 
+#include <stdlib.h>
 #include <string.h>
 
 #include <type_traits>
@@ -222,6 +223,138 @@ seed_update_kernel(const LT* __restrict__ Xl, int64_t n, int d, int d_pad,
     }
 }
 
+// The same round with the seeding block's rows streamed through shared memory by the TMA engine
+// (1-D bulk copies of 256-row stages into a ring; rows of G 16-byte chunks, G <= 16): the
+// copies of the next stages are in flight while the warps take 32-row batches of the current
+// one with the transposed, bank-conflict-free reads and the butterfly of seed_batch_dot.
+constexpr int kStageRows = 256;
+
+MPK_DEV void sbar_init(uint32_t b) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+}
+MPK_DEV void sbar_expect(uint32_t b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+                 : "memory");
+}
+MPK_DEV void sbar_wait(uint32_t b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "W_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra W_%=;\n\t}" ::"r"(b),
+        "r"(parity)
+        : "memory");
+}
+MPK_DEV void sbulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+template <int G, typename LT, typename W>
+__global__ void __launch_bounds__(kSeedThreads, 1)
+seed_update_tma_kernel(const LT* __restrict__ Xl, int64_t n, int d, int d_pad,
+                       const W* __restrict__ xn, const W* __restrict__ sx, int guard,
+                       const int64_t* __restrict__ idx, int j, double* __restrict__ D2,
+                       double* __restrict__ ps, int nstages) {
+    using A = typename seed_acc<LT>::T;
+    constexpr int m = 16 / (int)sizeof(LT);
+    constexpr int RPI = 32 / G;
+    constexpr int RB = G * 16;                        // row bytes
+    extern __shared__ __align__(128) unsigned char tsm[];
+    unsigned char* ring = tsm;                        // nstages x kStageRows x RB
+    A* cs = reinterpret_cast<A*>(tsm + (size_t)nstages * kStageRows * RB);
+    __shared__ double d2s[kSeedBlock];
+    __shared__ double wsum[kSeedThreads / 32];
+    __shared__ __align__(8) uint64_t full[4];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t c = idx[j];
+    const int64_t b0 = (int64_t)blockIdx.x * kSeedBlock;
+    const int rows = (int)((b0 + kSeedBlock < n) ? kSeedBlock : n - b0);
+    const int nst = (rows + kStageRows - 1) / kStageRows;
+    auto issue = [&](int st) {
+        const int r0 = st * kStageRows;
+        const int rr = rows - r0 < kStageRows ? rows - r0 : kStageRows;
+        const uint32_t fb = (uint32_t)__cvta_generic_to_shared(&full[st % nstages]);
+        sbar_expect(fb, (uint32_t)(rr * RB));
+        sbulk_g2s((uint32_t)__cvta_generic_to_shared(ring + (size_t)(st % nstages) * kStageRows * RB),
+                  Xl + (b0 + r0) * d_pad, (uint32_t)(rr * RB), fb);
+    };
+    if (tid == 0) {
+        for (int q = 0; q < nstages; ++q) sbar_init((uint32_t)__cvta_generic_to_shared(&full[q]));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int st = 0; st < nst && st < nstages; ++st) issue(st);
+    }
+    for (int t = tid; t < d_pad; t += blockDim.x) cs[t] = t < d ? (A)widen(Xl[c * d_pad + t]) : (A)0;
+    __syncthreads();
+    const double xnc = (double)xn[c];
+    const double scc = guard ? (double)sx[c] : 1.0;
+    const int q = lane & (G - 1), sgrp = lane / G;
+    A cr[m];
+#pragma unroll
+    for (int u = 0; u < m; ++u) cr[u] = cs[q * m + u];
+    for (int st = 0; st < nst; ++st) {
+        const int base = st * kStageRows + warp * 32;          // this warp's 32-row batch
+        const int r = q * RPI + sgrp;                          // the lane's row after the reduce
+        const bool mine = base + r < rows;
+        const int64_t i = b0 + base + r;
+        const double old = mine ? D2[i] : 0.0;
+        const W xni = mine ? xn[i] : (W)0;
+        const W si_w = (mine && guard) ? sx[i] : (W)1;
+        sbar_wait((uint32_t)__cvta_generic_to_shared(&full[st % nstages]), (uint32_t)((st / nstages) & 1));
+        const unsigned char* sb = ring + (size_t)(st % nstages) * kStageRows * RB + (size_t)warp * 32 * RB;
+        A part[G];
+#pragma unroll
+        for (int k2 = 0; k2 < G; ++k2) {
+            const int rr = k2 * RPI + sgrp;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (base + rr < rows) v = *reinterpret_cast<const uint4*>(sb + (size_t)rr * RB + q * 16);
+            LT e[m];
+            memcpy(e, &v, 16);
+            A acc = (A)0;
+#pragma unroll
+            for (int u = 0; u < m; ++u) acc = fma((A)widen(e[u]), cr[u], acc);
+            part[k2] = acc;
+        }
+#pragma unroll
+        for (int o = G / 2; o >= 1; o >>= 1) {
+            const bool upper = (lane & o) != 0;
+#pragma unroll
+            for (int u = 0; u < o; ++u) {
+                const A send = upper ? part[u] : part[u + o];
+                const A keep = upper ? part[u + o] : part[u];
+                part[u] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+        if (mine) {
+            const double si = (double)si_w;
+            double D = ((double)xni - 2.0 * (si * scc) * (double)part[0]) + xnc;
+            D = D > 0.0 ? D : 0.0;                      // NaN -> 0
+            if (i == c) D = 0.0;                        // the centre's own weight
+            const double nw2 = D < old ? D : old;
+            D2[i] = nw2;
+            d2s[base + r] = nw2;
+        }
+        __syncthreads();                                // the stage is consumed
+        if (tid == 0 && st + nstages < nst) issue(st + nstages);
+    }
+    // block sum in the fixed order of seed_update_kernel
+    double a = 0.0;
+    const int per = kSeedBlock / kSeedThreads;
+    for (int qq = 0; qq < per; ++qq) {
+        const int rr = tid * per + qq;
+        if (rr < rows) a += d2s[rr];
+    }
+    a = warp_sum(a);
+    if (lane == 0) wsum[warp] = a;
+    __syncthreads();
+    if (tid == 0) {
+        double t2 = 0.0;
+        for (int w = 0; w < kSeedThreads / 32; ++w) t2 += wsum[w];
+        ps[blockIdx.x] = t2;
+    }
+}
+
 // Exclusive scan of one double per thread over a kPickThreads CTA (fixed order: warp shuffles,
 // then the warp totals scanned by warp 0). Returns the exclusive prefix; *total = the sum.
 MPK_DEV double cta_exclusive_scan(double v, double* wtot, double* total) {
@@ -370,10 +503,42 @@ cudaError_t seed_rounds(const void* Xl, int64_t n, int d, int d_pad, const void*
     }
     const int row_bytes = d_pad * (int)sizeof(LT);
     const int vec = (row_bytes % 16 == 0) && ((reinterpret_cast<uintptr_t>(Xl) & 15) == 0);
+    const int G = vec ? row_bytes / 16 : 0;
+    // the TMA-ring kernel for rows of 2..16 chunks: as many 256-row stages as fit beside the
+    // block's D^2 staging (static 32 KB) in 227 KB
+    int nstages = 0;
+    size_t tsm = 0;
+    if ((G == 2 || G == 4 || G == 8 || G == 16) && !getenv("MPK_SEED_NO_TMA")) {
+        nstages = 3;
+        while (nstages > 1 && (size_t)nstages * kStageRows * row_bytes + sm + 34 * 1024 > 227 * 1024)
+            --nstages;
+        tsm = (size_t)nstages * kStageRows * row_bytes + sm;
+        // once per seeding call (per device: the attribute is per device)
+        cudaError_t ea;
+        switch (G) {
+            case 2: ea = cudaFuncSetAttribute(seed_update_tma_kernel<2, LT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm); break;
+            case 4: ea = cudaFuncSetAttribute(seed_update_tma_kernel<4, LT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm); break;
+            case 8: ea = cudaFuncSetAttribute(seed_update_tma_kernel<8, LT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm); break;
+            default: ea = cudaFuncSetAttribute(seed_update_tma_kernel<16, LT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm); break;
+        }
+        if (ea != cudaSuccess) { cudaGetLastError(); nstages = 0; }   // the one-row-per-thread kernel
+    }
     for (int j = 1; j < k; ++j) {
-        seed_update_kernel<LT, W><<<(unsigned)nb, kSeedThreads, sm, s>>>(
-            (const LT*)Xl, n, d, d_pad, (const W*)xn, (const W*)sx, guard, idx, j - 1, D2, ps,
-            vec);
+        if (nstages > 0) {
+#define SEED_TMA(GV) seed_update_tma_kernel<GV, LT, W><<<(unsigned)nb, kSeedThreads, tsm, s>>>( \
+            (const LT*)Xl, n, d, d_pad, (const W*)xn, (const W*)sx, guard, idx, j - 1, D2, ps, nstages)
+            switch (G) {
+                case 2: SEED_TMA(2); break;
+                case 4: SEED_TMA(4); break;
+                case 8: SEED_TMA(8); break;
+                default: SEED_TMA(16); break;
+            }
+#undef SEED_TMA
+        } else {
+            seed_update_kernel<LT, W><<<(unsigned)nb, kSeedThreads, sm, s>>>(
+                (const LT*)Xl, n, d, d_pad, (const W*)xn, (const W*)sx, guard, idx, j - 1, D2, ps,
+                vec);
+        }
         seed_pick_kernel<<<1, kPickThreads, 0, s>>>(D2, ps, n, nb, u, j, idx, warn);
     }
     launches_add(1 + 2 * (int64_t)(k - 1));
