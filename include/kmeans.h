@@ -195,11 +195,13 @@ int kmeans_set_stream(kmeans_handle h, void* cuda_stream);
  * Alg 3 step 1 in the low precision, on the handle's n rows of X (same
  * normalisation and operands as kmeans_fit; X host or device, work dtype, n x d). u: k uniforms
  * in [0, 1) (host), the method's random draws. indices (host, int64[k], out): the chosen rows,
- * distinct. The draw is the deterministic rule of DESIGN.md reading R6 (first index
- * floor(u_0 n); then the first index whose running sum of D^2 weights, in a fixed blocked order,
- * exceeds u_j * sum; D^2 from the stored low operands with the dot in fp64). Pass the rows
- * X[indices] as C0 to kmeans_fit for Alg 3 / Alg 5 end to end. Single-GPU handles only.
- * Returns 0, KMEANS_WARN_SEED_UNIFORM, or an error (u outside [0, 1): KMEANS_EINVAL).        */
+ * distinct. The draw is DESIGN.md reading R6: first index floor(u_0 n); then the inverse-CDF
+ * draw of Alg 1 line 2's law, the first index whose running sum of the weights D^2 exceeds
+ * u_j * sum (D^2: min over the chosen centres of O4's expanded formula from the stored low
+ * operands, fp32-accumulated dots, floored at 0; a chosen centre's own weight 0; the sums in a
+ * fixed parallel order). Pass the rows X[indices] as C0 to kmeans_fit for Alg 3 / Alg 5 end to
+ * end. Single-GPU handles only. Returns 0, KMEANS_WARN_SEED_UNIFORM (a round whose sum was 0 or
+ * non-finite drew floor(u_j n)), or an error (u outside [0, 1): KMEANS_EINVAL).              */
 int kmeans_seed_d2(kmeans_handle h, const void* X, const double* u, int64_t* indices);
 
 /* kmeans_set_delta — Alg 4 / Alg 5: per point-centroid pair, the
@@ -208,8 +210,11 @@ int kmeans_seed_d2(kmeans_handle h, const void* X, const double* u, int64_t* ind
  * fp64: max(xn, cn) >= delta^2 min(xn, cn)), with Alg 4's infinity-norm operand scaling, and the
  * working precision otherwise. delta = 1 makes every pair low precision (Alg 3 with scaling);
  * delta = 0 turns the switch off (the default: every pair low precision, scaling as created).
- * Runs on CUDA cores (both dot products per pair). The number of low-precision pairs is in
- * kmeans_stats.n_dist_low. Returns KMEANS_EINVAL unless delta == 0 or 1 <= delta < inf.      */
+ * With fp32 work and fp16/bf16 operands on the tcgen05 path it runs as a certified tensor-core
+ * filter plus exact per-pair evaluation of the candidate columns of uncertified rows (DESIGN.md
+ * R10: the labels of the per-pair evaluation); otherwise on CUDA cores (both dots per pair).
+ * The number of low-precision pairs is in kmeans_stats.n_dist_low (and eta). Returns
+ * KMEANS_EINVAL unless delta == 0 or 1 <= delta < inf.                                      */
 int kmeans_set_delta(kmeans_handle h, double delta);
 
 /* kmeans_set_timing — 1 = record CUDA events around every kernel of the loop (per-kernel times
