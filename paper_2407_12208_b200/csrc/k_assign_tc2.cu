@@ -70,6 +70,9 @@ constexpr int P_NON_EPI = 4;
 #ifndef MPK_PAIR_CNINIT_EARLY
 #define MPK_PAIR_CNINIT_EARLY 1
 #endif
+#ifndef MPK_PAIR_RBALT
+#define MPK_PAIR_RBALT 1                 // ASSIGN, one tile per row-block: warpgroups alternate row-blocks
+#endif
 #ifndef MPK_PAIR_HOT_WAIT
 #define MPK_PAIR_HOT_WAIT 1              // epilogue: test_wait before a bare try_wait loop
 #endif
@@ -171,8 +174,15 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
     // Measured: e5m2 2.15 -> 2.05 ms (the fold bounds it; decoupling the warpgroups helps), fp16
     // 2.42 -> 2.68 ms (twice the MMA instructions, commits and waits per tile where the MMA
     // pipeline already binds), so fp16 keeps one 256-column MMA per tile.
+    // Row-block alternation (ASSIGN, one centroid tile: C3 k = 256, C4 k = 64): warpgroup w folds
+    // ALL NB columns of the row-blocks w, w + 2, ... of its pair, so it holds each row's complete
+    // minimum and does the row-block end itself (label, changed count, SSE: no merge, no hand-off
+    // to warp 3), and one warpgroup's per-row-block overhead overlaps the other's fold. With the
+    // column split both warpgroups reach the row-block end together, once per tile.
+    const bool rbalt = MODE == PAIR_ASSIGN && MPK_PAIR_RBALT && p.NT == 1 && P_EWG == 2 &&
+                       !(p.dbg & (16 | 32));
     const bool hsplit = MODE == PAIR_ASSIGN && MPK_PAIR_HSPLIT && p.NB == 256 && P_EWG == 2 &&
-                        p.tmem_cols >= 512 && p.is_f8;
+                        p.tmem_cols >= 512 && p.is_f8 && !rbalt;
     // "cn init" (fp16/bf16 ASSIGN, 256-column tiles, no guard): each accumulator is pre-loaded
     // with ||c_j||^2 / 2 by the epilogue (tcgen05.st, after it has read the previous tile from
     // it) and the MMA adds x~ . (-c~) (B negated in the instruction descriptor), so the
@@ -182,10 +192,10 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
     // (tcgen05.st, as much TMEM write traffic as the MMA's) costs more: 2.59-2.64 vs 2.47-2.51 ms
     // with the release before or after the last chunk's fold. Off by default; correct either way
     // (the parity tests pass with it on).
-    const bool cninit = MPK_PAIR_CNINIT && !hsplit && MODE == PAIR_ASSIGN && p.NB == 256 &&
+    const bool cninit = MPK_PAIR_CNINIT && !hsplit && !rbalt && MODE == PAIR_ASSIGN && p.NB == 256 &&
                         p.nacc == 2 && P_EWG == 2 && !p.is_f8 && MPK_PAIR_ACC_DBUF && !p.guard &&
                         !(p.dbg & 7);
-    const bool fwd = !cninit && !hsplit && MODE == PAIR_ASSIGN && MPK_PAIR_FWD && p.NB == 256 && p.nacc == 2 && (P_EWG == 2 || P_EWG == 4) &&
+    const bool fwd = !cninit && !hsplit && !rbalt && MODE == PAIR_ASSIGN && MPK_PAIR_FWD && p.NB == 256 && p.nacc == 2 && (P_EWG == 2 || P_EWG == 4) &&
                      !p.is_f8 &&
                      MPK_PAIR_ACC_DBUF && !p.guard;
 
@@ -203,7 +213,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             mbar_init(smem_u32(&t_full[i]), 1);
             // one arrival per CTA (named barrier first), one per epilogue warp, or (half split)
             // one per warp of the owning warpgroup
-            mbar_init(smem_u32(&t_empty[i]), hsplit ? 8 : ((fwd || (!MPK_PAIR_WARP_ARRIVE && !cninit)) ? 2 : 2 * P_EPI));
+            mbar_init(smem_u32(&t_empty[i]), (hsplit || rbalt) ? 8 : ((fwd || (!MPK_PAIR_WARP_ARRIVE && !cninit)) ? 2 : 2 * P_EPI));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x)) : "memory");
@@ -374,8 +384,8 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 if (++slot == SA) { slot = 0; aph ^= 1; }
             }
         }
-    } else if (warp == 3 && CAND) {
-        // no row-block end in CAND mode
+    } else if (warp == 3 && (CAND || rbalt)) {
+        // no row-block end in CAND mode; the epilogue does its own with row-block alternation
     } else if (warp == 3) {
         // ------------------------------------------------ row-block end (both CTAs): merge the
         // two warpgroups' partials; labels, changed count and SSE (FINAL: certification)
@@ -543,7 +553,91 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&t_empty[b]), 0));
             }
         }
-        for (int64_t rb = pair; rb < num_rb; rb += npairs, ++rbi) {
+        if (rbalt) {
+            // one tile per row-block: this warpgroup's row-blocks rbi = wg, wg + 2, ... (accumulator
+            // rbi mod nacc, the MMA warp's order); all NB columns, reverse scan, then the row-block
+            // end in place. The point data is loaded one own row-block (two of the pair's) ahead.
+            double my_sse = 0.0, my_changed = 0.0;
+            const int nch = NB >> 5;                       // NB is a multiple of 64 when NT == 1
+            auto pt_xn = [&](int64_t rb) {
+                const int64_t r = rb * rows_per_rb + rank * P_BM + q;
+                return (rb < num_rb && r < n) ? p.xn[r] : 0.0f;
+            };
+            auto pt_old = [&](int64_t rb) {
+                const int64_t r = rb * rows_per_rb + rank * P_BM + q;
+                return (rb < num_rb && r < n) ? p.labels[r] : 0;
+            };
+            int64_t rb = pair + wg * npairs;
+            float m2_a = pt_m2(rb), xn_a = pt_xn(rb);
+            int old_a = pt_old(rb);
+            for (int64_t ri = wg; rb < num_rb; rb += 2 * npairs, ri += 2) {
+                const int64_t row = rb * rows_per_rb + rank * P_BM + q;
+                const float m2 = m2_a, xn = xn_a;
+                const int old = old_a;
+                m2_a = pt_m2(rb + 2 * npairs);
+                xn_a = pt_xn(rb + 2 * npairs);
+                old_a = pt_old(rb + 2 * npairs);
+                const int b = (int)(ri % nacc);
+                mbar_wait_hot(smem_u32(&t_full[b]), (uint32_t)(ri / nacc) & 1u);
+                tc_fence_after();
+                const uint32_t col0 = tmem_base + lane_addr + (uint32_t)b * NB;
+                float cv[NCH], c2[NCH], cs[NCH];
+                chains_init(cv, cs, c2);
+                uint64_t s2[NCH / 2];
+#pragma unroll
+                for (int m = 0; m < NCH / 2; ++m) s2[m] = pack2(-1.0f, -1.0f);
+                auto fold_all = [&](auto guard_tag) {
+                    constexpr bool GD = decltype(guard_tag)::value;
+                    // chunks nch-1 .. 0, two at a time; the next chunk's TMEM load is in flight
+                    // while this one folds
+                    uint32_t va[32], vb[32];
+                    ChunkCn<4, GD> cq;
+                    tmem_ld32(col0 + (nch - 1) * 32, va);
+                    for (int i = nch - 1; i >= 1; i -= 2) {
+                        tmem_wait_ld_dep(va);
+                        tmem_ld32(col0 + (i - 1) * 32, vb);
+                        load_chunk_cn<4, GD>(cn_s, sc_s, i * 32, cq);
+                        fold_rev_m3<4, GD>(va, cq, m2, cv, s2);
+                        tmem_wait_ld_dep(vb);
+                        if (i >= 3) tmem_ld32(col0 + (i - 2) * 32, va);
+                        load_chunk_cn<4, GD>(cn_s, sc_s, (i - 1) * 32, cq);
+                        fold_rev_m3<4, GD>(vb, cq, m2, cv, s2);
+                    }
+                };
+                if (!(dbg & 1)) {
+                    if (guard) fold_all(std::true_type{});
+                    else fold_all(std::false_type{});
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&t_empty[b]), 0));
+#pragma unroll
+                for (int m = 0; m < NCH / 2; ++m) unpack2(s2[m], cs[2 * m], cs[2 * m + 1]);
+                // chains -> column: key = 8 v + c with v the forward group ordinal = the column
+                float b1 = cv[0], k1 = fmaf(cs[0], -8.0f, -8.0f);
+#pragma unroll
+                for (int c = 1; c < NCH; ++c) {
+                    const float kc = fmaf(cs[c], -8.0f, (float)(c - 8));
+                    if (cv[c] < b1 || (cv[c] == b1 && kc < k1)) { b1 = cv[c]; k1 = kc; }
+                }
+                int j1 = (int)k1;
+                // no value below +inf, or ||x||^2 not finite: the forward scan's default column 0
+                if (!(b1 < INFINITY) || !(xn < INFINITY)) j1 = 0;
+                if (row < n) {
+                    p.labels[row] = j1;
+                    if (old != j1) my_changed += 1.0;
+                    const float md = xn + b1;
+                    my_sse += md > 0.0f ? (double)md : 0.0;
+                }
+            }
+            my_sse = warp_sum(my_sse);
+            my_changed = warp_sum(my_changed);
+            if (lane == 0) {
+                if (p.acc_sse) atomicAdd(p.acc_sse, my_sse);
+                if (p.acc_changed && my_changed != 0.0) atomicAdd(p.acc_changed, my_changed);
+            }
+        }
+        for (int64_t rb = pair; rb < num_rb && !rbalt; rb += npairs, ++rbi) {
             const int64_t row = rb * rows_per_rb + rank * P_BM + q;
             const float m2 = m2_n;
             const float T = T_n;                                             // CAND threshold

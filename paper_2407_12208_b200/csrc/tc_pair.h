@@ -31,7 +31,8 @@ struct PairParams {
     int* cand;               // CAND: [n][cand_q] candidate columns
     int cand_q;
     int dbg;                 // debug (timing only): bit0 skip the fold, bit1 skip MMAs, bit2 fold probe,
-                             // bit3 skip the X~ loads, bit4 skip the row-block end work
+                             // bit3 skip the X~ loads, bit4 skip the row-block end work;
+                             // bit5 (same results): no row-block alternation (column split)
     unsigned long long* trace;   // debug (MPK_PAIR_TRACE): per-tile clock64 stamps of CTA 0
 };
 

@@ -92,6 +92,41 @@ def test_tc_deep_row_blocks_c5_shape(dist, guard, monkeypatch):
     _assign_vs_oracle(200_003, 128, 1024, dist, guard, 77, want_variant=2)
 
 
+@pytest.mark.parametrize("dist", ["fp16", "bf16", "e5m2"])
+@pytest.mark.parametrize("guard", [False, True])
+@pytest.mark.parametrize("shape", [(200_003, 64, 256), (120_001, 32, 64), (90_007, 16, 40)])
+def test_tc_deep_row_blocks_one_tile(dist, guard, shape, monkeypatch):
+    """One centroid tile per row-block (the C3 / C4 shapes: k <= 256): the two epilogue
+    warpgroups alternate row-blocks and each does its own row-block end (k_assign_tc2.cu
+    "row-block alternation"); >= 4 row-blocks per CTA pair, so both warpgroups cycle through
+    every accumulator more than once — against the oracle label by label, ragged tail."""
+    _set_kind(monkeypatch, 2)
+    n, d, k = shape
+    _assign_vs_oracle(n, d, k, dist, guard, n + k, want_variant=2)
+
+
+@pytest.mark.parametrize("dist,shape", [("fp16", (200_003, 64, 256)), ("e5m2", (120_001, 32, 64))])
+def test_tc_one_tile_alternation_equals_column_split(dist, shape, monkeypatch):
+    """The row-block alternation and the column split (MPK_PAIR_DBG bit 5) fold the same values
+    in the same reverse order: identical labels, the SSE equal up to its summation order."""
+    n, d, k = shape
+    X, _ = synth.blobs(n, d, max(2, k // 3), sigma=1.5, seed=5, dtype=np.float32)
+    C = synth.init_rows(X, k, 3)
+    out = []
+    for dbg in ("0", "32"):
+        monkeypatch.setenv("MPK_PAIR_DBG", dbg)
+        km = mpk.KMeans(n, d, k, "fp32", dist, guard=True)
+        mpk.kmeans_set_centroids(km.h, dev(C))
+        lab = torch.empty(n, dtype=torch.int32, device="cuda")
+        sse = km.assign(dev(X), lab)
+        assert km.stats()["tc_variant"] == 2
+        km.close()
+        out.append((lab.cpu().numpy(), sse))
+    monkeypatch.delenv("MPK_PAIR_DBG")
+    assert np.array_equal(out[0][0], out[1][0])
+    assert abs(out[0][1] - out[1][1]) <= 1e-9 * abs(out[1][1])
+
+
 @pytest.mark.parametrize("dist,k,variant", [("fp16", 2048, 1), ("bf16", 2048, 1),
                                             ("e5m2", 2048, 2), ("e5m2", 4096, 1)])
 def test_tc_large_k_streaming(dist, k, variant, monkeypatch):
