@@ -73,13 +73,16 @@ constexpr int P_NON_EPI = 4;
 #ifndef MPK_PAIR_RBALT
 #define MPK_PAIR_RBALT 1                 // ASSIGN, one tile per row-block: warpgroups alternate row-blocks
 #endif
+#ifndef MPK_PAIR_TRACE_RB
+#define MPK_PAIR_TRACE_RB 0              // clock64 stamps in the row-block alternation (MPK_PAIR_TRACE)
+#endif
 #ifndef MPK_PAIR_HOT_WAIT
 #define MPK_PAIR_HOT_WAIT 1              // epilogue: test_wait before a bare try_wait loop
 #endif
 constexpr int P_EWG = MPK_PAIR_EWG;      // epilogue warpgroups (split the columns)
 constexpr int P_EPI = 4 * P_EWG;
 constexpr int P_THREADS = (P_NON_EPI + P_EPI) * 32;
-constexpr int P_MAX_ACC = 4;
+constexpr int P_MAX_ACC = 8;
 constexpr size_t P_BUDGET = 227 * 1024;
 constexpr uint32_t TRACE_T = 256;        // tiles traced under MPK_PAIR_TRACE
 // named barriers (0 is __syncthreads)
@@ -554,35 +557,48 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             }
         }
         if (rbalt) {
-            // one tile per row-block: this warpgroup's row-blocks rbi = wg, wg + 2, ... (accumulator
-            // rbi mod nacc, the MMA warp's order); all NB columns, reverse scan, then the row-block
+            // one tile per row-block: this warpgroup's row-blocks ri = wg, wg + 2, ... (accumulator
+            // ri mod nacc, the MMA warp's order); all NB columns, reverse scan, then the row-block
             // end in place. The point data is loaded one own row-block (two of the pair's) ahead.
-            double my_sse = 0.0, my_changed = 0.0;
+            double my_sse = 0.0;
+            int my_changed = 0;
             const int nch = NB >> 5;                       // NB is a multiple of 64 when NT == 1
-            auto pt_xn = [&](int64_t rb) {
-                const int64_t r = rb * rows_per_rb + rank * P_BM + q;
-                return (rb < num_rb && r < n) ? p.xn[r] : 0.0f;
+            const int64_t step = 2 * npairs * rows_per_rb;  // rows between own row-blocks
+            int64_t row = (pair + wg * npairs) * rows_per_rb + rank * P_BM + q;
+            const int64_t row_end = num_rb * rows_per_rb;  // first row of no row-block
+            float m2_a = -2.0f, xn_a = 0.0f;
+            int old_a = 0;
+            auto load_pt = [&](int64_t r) {
+                if (r < n) {
+                    xn_a = p.xn[r];
+                    old_a = p.labels[r];
+                    if (guard) m2_a = -2.0f * p.sx[r];
+                }
             };
-            auto pt_old = [&](int64_t rb) {
-                const int64_t r = rb * rows_per_rb + rank * P_BM + q;
-                return (rb < num_rb && r < n) ? p.labels[r] : 0;
-            };
-            int64_t rb = pair + wg * npairs;
-            float m2_a = pt_m2(rb), xn_a = pt_xn(rb);
-            int old_a = pt_old(rb);
-            for (int64_t ri = wg; rb < num_rb; rb += 2 * npairs, ri += 2) {
-                const int64_t row = rb * rows_per_rb + rank * P_BM + q;
+            load_pt(row);
+            int b = wg;                                    // accumulator of the current row-block
+            uint32_t ph = 0;                               // its phase
+#if MPK_PAIR_TRACE_RB
+            int64_t ri = wg;
+#endif
+            for (; row < row_end; row += step) {
                 const float m2 = m2_a, xn = xn_a;
                 const int old = old_a;
-                m2_a = pt_m2(rb + 2 * npairs);
-                xn_a = pt_xn(rb + 2 * npairs);
-                old_a = pt_old(rb + 2 * npairs);
-                const int b = (int)(ri % nacc);
-                mbar_wait_hot(smem_u32(&t_full[b]), (uint32_t)(ri / nacc) & 1u);
+                load_pt(row + step);
+#if MPK_PAIR_TRACE_RB
+                const bool tr = trace != nullptr && blockIdx.x == 0 && lane == 0 &&
+                                (warp & 3) == 0 && ri < TRACE_T;
+                if (tr) trace[ri * 8 + 5] = clock64();
+#endif
+                mbar_wait_hot(smem_u32(&t_full[b]), ph);
                 tc_fence_after();
+#if MPK_PAIR_TRACE_RB
+                if (tr) trace[ri * 8 + 2] = clock64();
+#endif
                 const uint32_t col0 = tmem_base + lane_addr + (uint32_t)b * NB;
-                float cv[NCH], c2[NCH], cs[NCH];
-                chains_init(cv, cs, c2);
+                float cv[NCH];
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) cv[c] = INFINITY;
                 uint64_t s2[NCH / 2];
 #pragma unroll
                 for (int m = 0; m < NCH / 2; ++m) s2[m] = pack2(-1.0f, -1.0f);
@@ -608,12 +624,21 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                     if (guard) fold_all(std::true_type{});
                     else fold_all(std::false_type{});
                 }
+#if MPK_PAIR_TRACE_RB
+                if (tr) trace[ri * 8 + 3] = clock64();
+#endif
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&t_empty[b]), 0));
+                b += 2;
+                if (b >= nacc) { b -= nacc; ph ^= 1u; }
+#if MPK_PAIR_TRACE_RB
+                if (tr) trace[ri * 8 + 4] = clock64();
+#endif
+                // chains -> column: key = 8 v + c with v the forward group ordinal, i.e. the column
+                float cs[NCH];
 #pragma unroll
                 for (int m = 0; m < NCH / 2; ++m) unpack2(s2[m], cs[2 * m], cs[2 * m + 1]);
-                // chains -> column: key = 8 v + c with v the forward group ordinal = the column
                 float b1 = cv[0], k1 = fmaf(cs[0], -8.0f, -8.0f);
 #pragma unroll
                 for (int c = 1; c < NCH; ++c) {
@@ -625,16 +650,20 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 if (!(b1 < INFINITY) || !(xn < INFINITY)) j1 = 0;
                 if (row < n) {
                     p.labels[row] = j1;
-                    if (old != j1) my_changed += 1.0;
+                    my_changed += old != j1;
                     const float md = xn + b1;
                     my_sse += md > 0.0f ? (double)md : 0.0;
                 }
+#if MPK_PAIR_TRACE_RB
+                if (tr) trace[ri * 8 + 6] = clock64();
+                ri += 2;
+#endif
             }
             my_sse = warp_sum(my_sse);
             my_changed = warp_sum(my_changed);
             if (lane == 0) {
                 if (p.acc_sse) atomicAdd(p.acc_sse, my_sse);
-                if (p.acc_changed && my_changed != 0.0) atomicAdd(p.acc_changed, my_changed);
+                if (p.acc_changed && my_changed != 0) atomicAdd(p.acc_changed, (double)my_changed);
             }
         }
         for (int64_t rb = pair; rb < num_rb && !rbalt; rb += npairs, ++rbi) {
@@ -1016,15 +1045,18 @@ bool pair_plan(int dist, int d, int d_pad, int k, PairParams* pp, size_t* smem_b
     // static shared (the warp-3 partial buffers) counts against the same 227 KB
     const size_t stat = 3 * 2 * P_EWG * P_BM * 4;
     const size_t fixed = 1024 + stat + (size_t)k_pad * 12 + 8 +
-                         (size_t)(2 * 8 + 1 + 2 * P_MAX_ACC) * 8 + 16;
+                         (size_t)(2 * 16 + 1 + 2 * P_MAX_ACC) * 8 + 16;
     const size_t bres = (size_t)NT * b_half;
     if (fixed + bres + 2 * a_tile > P_BUDGET) return false;
-    int SA = (int)std::min<size_t>(4, (P_BUDGET - fixed - bres) / a_tile);
+    int sa_cap = 4, acc_cap = 4;
+    if (const char* e = getenv("MPK_PAIR_SA")) sa_cap = std::max(2, std::min(16, atoi(e)));
+    if (const char* e = getenv("MPK_PAIR_NACC")) acc_cap = std::max(2, std::min(P_MAX_ACC, atoi(e)));
+    int SA = (int)std::min<size_t>(sa_cap, (P_BUDGET - fixed - bres) / a_tile);
     PairParams& p = *pp;
     p = PairParams{};
     p.k = k; p.k_pad = k_pad; p.d = d; p.d_pad = d_pad; p.NB = NB; p.NT = NT; p.KB = KB;
     p.SWZ = SWZ; p.SA = SA;
-    p.nacc = std::min(P_MAX_ACC, 512 / NB);
+    p.nacc = std::min(acc_cap, 512 / NB);
     int cols = p.nacc * NB, pw = 32;
     while (pw < cols) pw <<= 1;
     p.tmem_cols = pw;
