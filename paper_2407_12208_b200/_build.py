@@ -53,7 +53,8 @@ def _stale(srcs: list[str], target: str) -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    if not force and not _stale(srcs, LIB):
+    # experiment flags (MPK_NVCC_EXTRA) always rebuild: the library on disk may predate them
+    if not force and not os.environ.get("MPK_NVCC_EXTRA") and not _stale(srcs, LIB):
         return LIB
     os.makedirs(OBJ, exist_ok=True)
     nvcc = _nvcc()

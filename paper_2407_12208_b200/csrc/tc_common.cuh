@@ -52,6 +52,32 @@ MPK_DEV void mbar_wait_hot(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// Five phases at once (the grouped MMA issue: one accumulator and up to four X~ slots): all
+// test_waits are issued back to back so their latencies (~150 cycles each) overlap, then a
+// spinning try_wait on each one not yet complete. Repeating a barrier is allowed.
+MPK_DEV void mbar_wait5_hot(uint32_t b0, uint32_t p0, const uint32_t (&b)[4], const uint32_t (&p)[4]) {
+    asm volatile(
+        "{\n\t.reg .pred Q0, Q1, Q2, Q3, Q4;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 Q0, [%0], %1;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 Q1, [%2], %3;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 Q2, [%4], %5;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 Q3, [%6], %7;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 Q4, [%8], %9;\n\t"
+        "@Q0 bra C1_%=;\n\t"
+        "W0_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 Q0, [%0], %1;\n\t@!Q0 bra W0_%=;\n\t"
+        "C1_%=:\n\t@Q1 bra C2_%=;\n\t"
+        "W1_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 Q1, [%2], %3;\n\t@!Q1 bra W1_%=;\n\t"
+        "C2_%=:\n\t@Q2 bra C3_%=;\n\t"
+        "W2_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 Q2, [%4], %5;\n\t@!Q2 bra W2_%=;\n\t"
+        "C3_%=:\n\t@Q3 bra C4_%=;\n\t"
+        "W3_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 Q3, [%6], %7;\n\t@!Q3 bra W3_%=;\n\t"
+        "C4_%=:\n\t@Q4 bra DONE_%=;\n\t"
+        "W4_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 Q4, [%8], %9;\n\t@!Q4 bra W4_%=;\n\t"
+        "DONE_%=:\n\t}" ::"r"(b0),
+        "r"(p0), "r"(b[0]), "r"(p[0]), "r"(b[1]), "r"(p[1]), "r"(b[2]), "r"(p[2]), "r"(b[3]),
+        "r"(p[3])
+        : "memory");
+}
 MPK_DEV void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"

@@ -10,6 +10,7 @@ namespace tcdev {
 struct PairParams {
     int64_t n;
     int k, k_pad, d, d_pad, NB, NT, KB, SWZ, SA, nacc, tmem_cols;
+    int rbr;                 // one tile per row-block: row-blocks per accumulator (1..4)
     uint32_t a_tile_bytes;   // 128 rows x row bytes (this CTA's half of M = 256)
     uint32_t b_half_bytes;   // NB/2 rows x row bytes (this CTA's half of one centroid tile)
     uint32_t kb_a_bytes, kb_b_bytes;
