@@ -122,8 +122,10 @@ struct LoopState {
     int iter;          // iterations completed
     int stop;          // set when converged: later launches are no-ops
     int converged;
-    unsigned counter;  // block ticket of the current launch (reset by the last block)
+    unsigned counter;  // K5g: block ticket of the launch (reset by the last block); K5p: block
+                       // arrivals so far (the grid barrier of iteration t waits for grid (t + 1))
     double tol;        // < 0: never stop early
+    int fault;         // K5p: a block gave up waiting at the grid barrier
 };
 bool smalld_loop_supported(int d, int k);
 int smalld_loop_grid(int64_t n);
@@ -132,6 +134,14 @@ cudaError_t launch_smalld_iter(int work, int dist, const Problem& p, const void*
                                int32_t* labels, double* part, LoopState* st, IterRec* trace,
                                unsigned long long* census, cudaStream_t s);   // Xw == nullptr: only set the kernel's
                                                       // shared-memory attribute (per device)
+// K5p: the same iteration, all max_iter of them in ONE cooperative launch (every block resident,
+// its rows kept in shared memory across iterations; one grid barrier per iteration, after which
+// every block reduces the partials in the same fixed order and forms the same centres).
+// cudaErrorNotSupported when the rows do not fit in shared memory or the grid cannot be
+// co-resident (the caller then uses K5g).
+cudaError_t launch_smalld_persist(int work, int dist, const Problem& p, const void* Xw, void* Cw,
+                                  int32_t* labels, double* part, LoopState* st, IterRec* trace,
+                                  unsigned long long* census, int max_iter, cudaStream_t s);
 
 // K6m: Alg 4's per-pair precision switch with threshold delta (>= 1); n_low (device) gets the
 // number of triggered (low-precision) pairs added.

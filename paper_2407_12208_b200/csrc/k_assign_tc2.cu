@@ -76,6 +76,9 @@ constexpr int P_NON_EPI = 4;
 #ifndef MPK_PAIR_TRACE_RB
 #define MPK_PAIR_TRACE_RB 0              // clock64 stamps in the row-block alternation (MPK_PAIR_TRACE)
 #endif
+#ifndef MPK_PAIR_EARLY_REL
+#define MPK_PAIR_EARLY_REL 1             // row-block alternation: release before the last chunk's fold
+#endif
 #ifndef MPK_PAIR_HOT_WAIT
 #define MPK_PAIR_HOT_WAIT 1              // epilogue: test_wait before a bare try_wait loop
 #endif
@@ -715,6 +718,20 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                     uint64_t s2[NCH / 2];
 #pragma unroll
                     for (int m = 0; m < NCH / 2; ++m) s2[m] = pack2(-1.0f, -1.0f);
+                    // the group's last TMEM load has landed: release the accumulator (before the
+                    // last chunk's fold, so the MMA refill overlaps it)
+                    auto release = [&]() {
+#if MPK_PAIR_TRACE_RB
+                        if (tr) trace[g * 8 + 3] = clock64();
+#endif
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&t_empty[b]), 0));
+#if MPK_PAIR_TRACE_RB
+                        if (tr) trace[g * 8 + 4] = clock64();
+#endif
+                    };
+                    const bool last = r == nr - 1;
                     auto fold_all = [&](auto guard_tag) {
                         constexpr bool GD = decltype(guard_tag)::value;
                         // chunks nch-1 .. 0, two at a time; the next chunk's TMEM load is in
@@ -729,6 +746,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                             fold_rev_m3<4, GD>(va, cq, m2, cv, s2);
                             tmem_wait_ld_dep(vb);
                             if (i >= 3) tmem_ld32(col0 + (i - 2) * 32, va);
+                            else if (last && MPK_PAIR_EARLY_REL) release();
                             load_chunk_cn<4, GD>(cn_s, sc_s, (i - 1) * 32, cq);
                             fold_rev_m3<4, GD>(vb, cq, m2, cv, s2);
                         }
@@ -737,18 +755,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                         if (guard) fold_all(std::true_type{});
                         else fold_all(std::false_type{});
                     }
-                    if (r == nr - 1) {
-                        // the group's last TMEM load has landed: release the accumulator
-#if MPK_PAIR_TRACE_RB
-                        if (tr) trace[g * 8 + 3] = clock64();
-#endif
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&t_empty[b]), 0));
-#if MPK_PAIR_TRACE_RB
-                        if (tr) trace[g * 8 + 4] = clock64();
-#endif
-                    }
+                    if (last && ((dbg & 1) || !MPK_PAIR_EARLY_REL)) release();
                     // chains -> column: key = 8 v + c with v the forward group ordinal, i.e. the
                     // column
                     float cs[NCH];

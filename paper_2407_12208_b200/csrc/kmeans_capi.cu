@@ -781,6 +781,24 @@ int run_smalld_loop(kmeans_ctx* h, int max_iter, double tol, int* it_out, bool* 
         CK(cudaMallocHost(&h->loop_host, 2 * sizeof(LoopState)));
     }
     Problem p{h->n, h->d, h->k, h->d_pad, h->guard};
+    if (!getenv("MPK_NO_PERSIST")) {
+        // K5p: every iteration in one cooperative launch when the rows fit in shared memory
+        h->loop_host[0] = LoopState{0, 0, 0, 0u, tol, 0};
+        CK(cudaMemcpyAsync(h->loop, &h->loop_host[0], sizeof(LoopState), cudaMemcpyHostToDevice, s));
+        const cudaError_t e = launch_smalld_persist(h->work, h->dist, p, h->Xw, h->Cw, h->labels,
+                                                    h->loop_part, h->loop, h->trace,
+                                                    h->census + 2, max_iter, s);
+        if (e == cudaSuccess) {
+            CK(cudaMemcpyAsync(&h->loop_host[1], h->loop, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (h->loop_host[1].fault)
+                return fail(h, KMEANS_ECUDA, "K5p: a block timed out at the grid barrier");
+            *it_out = h->loop_host[1].iter;
+            *conv_out = h->loop_host[1].converged != 0;
+            return 0;
+        }
+        if (e != cudaErrorNotSupported) CK(e);
+    }
     auto one = [&](cudaStream_t st) {
         return launch_smalld_iter(h->work, h->dist, p, h->Xw, h->Cw, h->labels, h->loop_part,
                                   h->loop, h->trace, h->census + 2, st);
@@ -808,7 +826,7 @@ int run_smalld_loop(kmeans_ctx* h, int max_iter, double tol, int* it_out, bool* 
         launches_add(-kLoopChunk);   // captured, not launched
         h->loop_graph_guard = h->guard;
     }
-    h->loop_host[0] = LoopState{0, 0, 0, 0u, tol};
+    h->loop_host[0] = LoopState{0, 0, 0, 0u, tol, 0};
     CK(cudaMemcpyAsync(h->loop, &h->loop_host[0], sizeof(LoopState), cudaMemcpyHostToDevice, s));
     int done = 0;
     while (done < max_iter) {
