@@ -128,7 +128,6 @@ struct LoopState {
     int fault;         // K5p: a block gave up waiting at the grid barrier
 };
 bool smalld_loop_supported(int d, int k);
-int smalld_loop_grid(int64_t n);
 size_t smalld_loop_part_bytes(int64_t n);
 cudaError_t launch_smalld_iter(int work, int dist, const Problem& p, const void* Xw, void* Cw,
                                int32_t* labels, double* part, LoopState* st, IterRec* trace,

@@ -42,9 +42,9 @@ static_assert(LK * LD == 32, "the finalize maps (cluster, feature) onto the 32 l
 #ifndef MPK_SL_TILE
 #define MPK_SL_TILE 2048
 #endif
-#ifndef MPK_SL_MINB
-#define MPK_SL_MINB 1
-#endif
+// K5g blocks per SM (registers capped at 128 per thread): the streaming kernel is latency-bound
+// on its row loop, so a second block per SM hides it (4096^2 image: 186 -> 129 us per iteration)
+constexpr int kK5gBlocksPerSM = 2;
 constexpr int kTileRows = MPK_SL_TILE;   // rows per pipeline stage (8 per thread)
 constexpr int kStages = 3;           // tiles in flight per block (bulk copies)
 constexpr int kMaxResident = 8;
@@ -95,7 +95,7 @@ MPK_DEV void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t ba
 // in shared memory (stage m = tile m, loaded once), and the iterations are separated by a grid
 // barrier that the last block releases after its finalize (same arithmetic, same order as K5g).
 template <typename W, int DIST, int D, int KT, bool PERSIST>
-__global__ void __launch_bounds__(LT, MPK_SL_MINB)
+__global__ void __launch_bounds__(LT, PERSIST ? 1 : kK5gBlocksPerSM)
 smalld_iter_kernel(Problem p, const W* __restrict__ X, W* __restrict__ C,
                    int32_t* __restrict__ labels, double* __restrict__ part,
                    LoopState* __restrict__ st, IterRec* __restrict__ trace,
@@ -374,8 +374,8 @@ smalld_iter_kernel(Problem p, const W* __restrict__ X, W* __restrict__ C,
     // in increasing b (independent loads in flight), then the groups are added in order
     if (tid < NV * kRedGroups) {
         const int c = tid % NV, g = tid / NV;
-        // at most ceil(148 / 6) = 25 blocks per group: every load is issued before the adds
-        constexpr int kMaxPer = (kNumSMs + kRedGroups - 1) / kRedGroups;
+        // at most ceil(grid / 6) blocks per group: every load is issued before the adds
+        constexpr int kMaxPer = (kNumSMs * kK5gBlocksPerSM + kRedGroups - 1) / kRedGroups;
         double v[kMaxPer];
 #pragma unroll
         for (int q = 0; q < kMaxPer; ++q) {
@@ -464,6 +464,14 @@ smalld_iter_kernel(Problem p, const W* __restrict__ X, W* __restrict__ C,
     }   // iterations
 }
 
+// Grid: K5p runs one block per SM (cooperative, up to 227 KB of shared memory each); K5g the
+// same grid whenever K5p could run this n (so the two partition the rows identically and agree
+// bit for bit), else up to kK5gBlocksPerSM blocks per SM.
+static int loop_grid(int64_t n, bool one_per_sm) {
+    const int64_t tiles = (n + kTileRows - 1) / kTileRows;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, one_per_sm ? kNumSMs : kNumSMs * kK5gBlocksPerSM));
+}
+
 template <typename W>
 size_t smem_bytes_for(int d, int stages) {
     return (size_t)stages * kTileRows * ((size_t)d * sizeof(W) + sizeof(int32_t));
@@ -480,7 +488,15 @@ template <typename W, int DIST, int D, int KT>
 cudaError_t launch_dk(const Problem& p, const void* X, void* C, int32_t* labels, double* part,
                       int grid, LoopState* st, IterRec* trace, unsigned long long* census,
                       int persist, cudaStream_t s) {
+    using AT = typename std::conditional<DIST == KMEANS_FP64, double, float>::type;
+    // could K5p hold this n? (one block per SM, its tiles and cached operands in shared memory)
+    const int64_t ntiles = (p.n + kTileRows - 1) / kTileRows;
+    const int g1 = loop_grid(p.n, true);
+    const int per = (int)((ntiles + g1 - 1) / g1);              // tiles of the busiest block
+    const size_t smp = smem_bytes_persist<W, AT>(D, per);
+    const bool fits = per <= kMaxResident && smp <= 227 * 1024;
     if (persist < 0) {
+        grid = fits ? g1 : loop_grid(p.n, false);
         const size_t sm = smem_bytes_for<W>(D, kStages);
         if (!X) {   // attribute-only call (before a stream capture: not a stream operation)
             return cudaFuncSetAttribute(smalld_iter_kernel<W, DIST, D, KT, false>,
@@ -490,11 +506,9 @@ cudaError_t launch_dk(const Problem& p, const void* X, void* C, int32_t* labels,
             p, (const W*)X, (W*)C, labels, part, st, trace, census, 1);
         return cudaGetLastError();
     }
-    const int64_t ntiles = (p.n + kTileRows - 1) / kTileRows;
-    const int per = (int)((ntiles + grid - 1) / grid);          // tiles of the busiest block
-    using AT = typename std::conditional<DIST == KMEANS_FP64, double, float>::type;
-    const size_t sm = smem_bytes_persist<W, AT>(D, per);
-    if (per > kMaxResident || sm > 227 * 1024) return cudaErrorNotSupported;
+    if (!fits) return cudaErrorNotSupported;
+    grid = g1;
+    const size_t sm = smp;
     auto kern = smalld_iter_kernel<W, DIST, D, KT, true>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) { cudaGetLastError(); return cudaErrorNotSupported; }
@@ -534,19 +548,17 @@ cudaError_t launch_t(const Problem& p, const void* X, void* C, int32_t* labels, 
 
 bool smalld_loop_supported(int d, int k) { return d <= LD && k <= LK; }
 
-int smalld_loop_grid(int64_t n) {
-    const int64_t tiles = (n + kTileRows - 1) / kTileRows;
-    return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, kNumSMs));
-}
 
 // two buffers: K5p alternates them by iteration parity
-size_t smalld_loop_part_bytes(int64_t n) { return 2 * (size_t)smalld_loop_grid(n) * NV * sizeof(double); }
+size_t smalld_loop_part_bytes(int64_t n) {
+    return 2 * (size_t)loop_grid(n, false) * NV * sizeof(double);   // the larger grid
+}
 
 namespace {
 cudaError_t launch_any(int work, int dist, const Problem& p, const void* Xw, void* Cw,
                        int32_t* labels, double* part, LoopState* st, IterRec* trace,
                        unsigned long long* census, int persist, cudaStream_t s) {
-    const int g = smalld_loop_grid(p.n);
+    const int g = 0;                                   // launch_dk chooses the grid
 #define MPK_SL(W)                                                                                  \
     switch (dist) {                                                                                \
         case KMEANS_FP64: return launch_t<W, KMEANS_FP64>(p, Xw, Cw, labels, part, g, st, trace, census, persist, s); \
