@@ -97,6 +97,25 @@ def test_virtual_ranks_fp32_fx_bit_identical(g, dist):
 
 
 @pytest.mark.parametrize("g", [2, 3])
+@pytest.mark.parametrize("dist", ["fp16", "e5m2"])
+def test_virtual_ranks_one_tile_groups_bit_identical(g, dist):
+    """k = 64 (one 64-column tile per row-block: the warpgroups alternate groups of four
+    row-blocks, k_assign_tc2.cu) with >= 4 row-blocks per CTA pair on every shard: the g-rank
+    fit equals the 1-rank fit bit for bit."""
+    X, _, C0 = synth.make("c5_vq_10m", n=240_007, seed=6)
+    C0 = C0[:64].copy()
+    flags = mpk.KMEANS_NORM_NONE
+    lab1, cent1, sse1, st1 = _plain_fit(X, C0, "fp32", dist, flags, 4)
+    labg, cents, sses, iters, stats = _virtual_fit(X, C0, "fp32", dist, flags, 4, g)
+    assert st1["dist_kernel"] == "tcgen05" and st1["tc_variant"] == 2
+    np.testing.assert_array_equal(labg, lab1)
+    for c in cents:
+        np.testing.assert_array_equal(c.view(np.uint32), cent1.view(np.uint32))
+    for s in sses:
+        assert abs(s - sse1) <= 1e-12 * sse1
+
+
+@pytest.mark.parametrize("g", [2, 3])
 def test_virtual_ranks_zscore_matches_oracle(g):
     """z-score statistics allreduced across ranks (two passes, fp64 sums, eq:z-norm
     PAPER.md:119-126): the g-rank fit agrees with the oracle's single-process fit to the fp16
