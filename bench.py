@@ -416,7 +416,10 @@ def main():
         unit, alg = "TFLOP/s", f"2*n*k*d = {flops:.4e} flop"
     roof = {"kernel": f"assign_{kern}", "bound": bound, "achieved": achieved, "peak": peak,
             "unit": unit, "frac": (achieved / peak) if achieved else None,
-            "traffic": traffic_from_profiles(args.config, dist), "peak_source": peak_note,
+            "traffic": traffic_from_profiles(args.config, dist),
+            "traffic_source": "profiles/ncu_traffic.json (an earlier ncu --set full capture of this "
+                              "launch, not measured in this run)",
+            "peak_source": peak_note,
             "algorithmic_per_launch": alg,
             "avg_launch_ms": t_launch_ms,
             "share_of_step": (t_dist / ms) if ms > 0 else None}
