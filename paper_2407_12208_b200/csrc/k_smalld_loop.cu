@@ -43,7 +43,8 @@ static_assert(LK * LD == 32, "the finalize maps (cluster, feature) onto the 32 l
 #define MPK_SL_TILE 2048
 #endif
 // K5g blocks per SM (registers capped at 128 per thread): the streaming kernel is latency-bound
-// on its row loop, so a second block per SM hides it (4096^2 image: 186 -> 129 us per iteration)
+// on its row loop, so a second block per SM hides it (4096^2 image: 186 -> 129 us per iteration).
+// fp64 work keeps one (its 3-stage ring of fp64 rows fills the shared memory; no register cap).
 constexpr int kK5gBlocksPerSM = 2;
 constexpr int kTileRows = MPK_SL_TILE;   // rows per pipeline stage (8 per thread)
 constexpr int kStages = 3;           // tiles in flight per block (bulk copies)
@@ -95,7 +96,7 @@ MPK_DEV void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t ba
 // in shared memory (stage m = tile m, loaded once), and the iterations are separated by a grid
 // barrier that the last block releases after its finalize (same arithmetic, same order as K5g).
 template <typename W, int DIST, int D, int KT, bool PERSIST>
-__global__ void __launch_bounds__(LT, PERSIST ? 1 : kK5gBlocksPerSM)
+__global__ void __launch_bounds__(LT, (PERSIST || sizeof(W) == 8) ? 1 : kK5gBlocksPerSM)
 smalld_iter_kernel(Problem p, const W* __restrict__ X, W* __restrict__ C,
                    int32_t* __restrict__ labels, double* __restrict__ part,
                    LoopState* __restrict__ st, IterRec* __restrict__ trace,
