@@ -96,7 +96,7 @@ MPK_DEV void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t ba
 // in shared memory (stage m = tile m, loaded once), and the iterations are separated by a grid
 // barrier that the last block releases after its finalize (same arithmetic, same order as K5g).
 template <typename W, int DIST, int D, int KT, bool PERSIST>
-__global__ void __launch_bounds__(LT, (PERSIST || sizeof(W) == 8) ? 1 : kK5gBlocksPerSM)
+__global__ void __launch_bounds__(LT, (PERSIST || sizeof(W) == 8 || DIST == KMEANS_FP64) ? 1 : kK5gBlocksPerSM)
 smalld_iter_kernel(Problem p, const W* __restrict__ X, W* __restrict__ C,
                    int32_t* __restrict__ labels, double* __restrict__ part,
                    LoopState* __restrict__ st, IterRec* __restrict__ trace,
