@@ -79,6 +79,9 @@ constexpr int P_NON_EPI = 4;
 #ifndef MPK_PAIR_EARLY_REL
 #define MPK_PAIR_EARLY_REL 1             // row-block alternation: release before the last chunk's fold
 #endif
+#ifndef MPK_PAIR_RBH
+#define MPK_PAIR_RBH 1                   // ASSIGN, 256-column tiles: warpgroups alternate row-blocks, half-tiles
+#endif
 #ifndef MPK_PAIR_HOT_WAIT
 #define MPK_PAIR_HOT_WAIT 1              // epilogue: test_wait before a bare try_wait loop
 #endif
@@ -198,10 +201,24 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
     // minimum and does the row-block end itself (label, changed count, SSE: no merge, no hand-off
     // to warp 3), and one warpgroup's per-row-block overhead overlaps the other's fold. With the
     // column split both warpgroups reach the row-block end together, once per tile.
-    const bool rbalt = MODE == PAIR_ASSIGN && MPK_PAIR_RBALT && p.NT == 1 && P_EWG == 2 &&
+    // Row-block halves ("rbh"; ASSIGN, 256-column tiles): warpgroup w owns accumulators 2w, 2w+1
+    // (128 columns each) and folds ALL columns of the row-blocks w, w + 2, ... half-tile by
+    // half-tile (each tile issued as two N = 128 MMAs), so the warpgroups never wait for each
+    // other: no shared accumulator, no merge, no hand-off to warp 3; each warpgroup refills one
+    // accumulator while it folds the other. The resident C~ is laid out so that half h of tile t
+    // is centroids t*256 + h*128 + [0, 128) (CTA r holds rows h*128 + r*64 + [0, 64) of each half;
+    // 64-row TMA boxes), so the halves scan in decreasing column order. Two MMA issuers (warps
+    // 1 and 2), one per warpgroup's row-blocks.
+    // Measured (tools/ab_pair.sh, C5): fp16 2.64 -> 2.48 ms; E5M2 1.96 -> 2.05 ms and C3 (one
+    // tile) 74.5 -> 79 us are slower than the half split / row-block alternation, so fp16 / bf16
+    // with several tiles per row-block only.
+    const bool rbh = MODE == PAIR_ASSIGN && MPK_PAIR_RBH && p.NB == 256 && p.NT >= 2 && !p.is_f8 &&
+                     P_EWG == 2 && p.tmem_cols >= 512 && p.box_rows == 64 &&
+                     !(p.dbg & (16 | 32 | 64));
+    const bool rbalt = MODE == PAIR_ASSIGN && MPK_PAIR_RBALT && p.NT == 1 && P_EWG == 2 && !rbh &&
                        !(p.dbg & (16 | 32));
     const bool hsplit = MODE == PAIR_ASSIGN && MPK_PAIR_HSPLIT && p.NB == 256 && P_EWG == 2 &&
-                        p.tmem_cols >= 512 && p.is_f8 && !rbalt;
+                        p.tmem_cols >= 512 && p.is_f8 && !rbalt && !rbh;
     // "cn init" (fp16/bf16 ASSIGN, 256-column tiles, no guard): each accumulator is pre-loaded
     // with ||c_j||^2 / 2 by the epilogue (tcgen05.st, after it has read the previous tile from
     // it) and the MMA adds x~ . (-c~) (B negated in the instruction descriptor), so the
@@ -211,10 +228,10 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
     // (tcgen05.st, as much TMEM write traffic as the MMA's) costs more: 2.59-2.64 vs 2.47-2.51 ms
     // with the release before or after the last chunk's fold. Off by default; correct either way
     // (the parity tests pass with it on).
-    const bool cninit = MPK_PAIR_CNINIT && !hsplit && !rbalt && MODE == PAIR_ASSIGN && p.NB == 256 &&
+    const bool cninit = MPK_PAIR_CNINIT && !hsplit && !rbalt && !rbh && MODE == PAIR_ASSIGN && p.NB == 256 &&
                         p.nacc == 2 && P_EWG == 2 && !p.is_f8 && MPK_PAIR_ACC_DBUF && !p.guard &&
                         !(p.dbg & 7);
-    const bool fwd = !cninit && !hsplit && !rbalt && MODE == PAIR_ASSIGN && MPK_PAIR_FWD && p.NB == 256 && p.nacc == 2 && (P_EWG == 2 || P_EWG == 4) &&
+    const bool fwd = !cninit && !hsplit && !rbalt && !rbh && MODE == PAIR_ASSIGN && MPK_PAIR_FWD && p.NB == 256 && p.nacc == 2 && (P_EWG == 2 || P_EWG == 4) &&
                      !p.is_f8 &&
                      MPK_PAIR_ACC_DBUF && !p.guard;
 
@@ -228,11 +245,11 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
         mbar_init(smem_u32(b_full), 1);
         mbar_init(smem_u32(&part_free[0]), 1);
         mbar_init(smem_u32(&part_free[1]), 1);
-        for (int i = 0; i < (hsplit ? 4 : p.nacc); ++i) {
+        for (int i = 0; i < ((hsplit || rbh) ? 4 : p.nacc); ++i) {
             mbar_init(smem_u32(&t_full[i]), 1);
             // one arrival per CTA (named barrier first), one per epilogue warp, or (half split)
             // one per warp of the owning warpgroup
-            mbar_init(smem_u32(&t_empty[i]), (hsplit || rbalt) ? 8 : ((fwd || (!MPK_PAIR_WARP_ARRIVE && !cninit)) ? 2 : 2 * P_EPI));
+            mbar_init(smem_u32(&t_empty[i]), (hsplit || rbalt || rbh) ? 8 : ((fwd || (!MPK_PAIR_WARP_ARRIVE && !cninit)) ? 2 : 2 * P_EPI));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x)) : "memory");
@@ -259,19 +276,78 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
     const int half = p.NB / 2;
     const int dbg = p.dbg;
 
+    // rbh MMA issue for warpgroup w's row-blocks (leader CTA; the calling warp runs converged,
+    // one lane issues): per half-tile q (running count) accumulator 2w + (q & 1)
+    auto rbh_mma = [&](int w) {
+        const int SA = p.SA, KB = p.KB, NT = p.NT;
+        const int ksteps = p.SWZ / 32;
+        const bool f8 = p.is_f8 != 0;
+        const uint32_t dhi = umma_desc_hi(p.SWZ);
+        const uint32_t b_lo0 = umma_desc_lo(smem_u32(b_base));
+        const uint32_t a_lo0 = umma_desc_lo(smem_u32(a_base));
+        const uint32_t a_tile16 = p.a_tile_bytes >> 4, b_half16 = p.b_half_bytes >> 4;
+        const uint32_t kb_a16 = p.kb_a_bytes >> 4, kb_b16 = p.kb_b_bytes >> 4;
+        const uint32_t idesc128 = (p.idesc & ~(0x3Fu << 17)) | ((128u >> 3) << 17);
+        const uint32_t h16 = (64u * (uint32_t)p.SWZ) >> 4;   // 64 centroid rows
+        mbar_wait(smem_u32(b_full), 0);
+        tc_fence_after();
+        int slot = w % SA;
+        uint32_t aph = 0, qq = 0;
+        for (int64_t rb = pair + w * npairs; rb < num_rb; rb += 2 * npairs) {
+            mbar_wait_hot(smem_u32(&a_full[slot]), aph);
+            tc_fence_after();
+            const uint32_t a_lo = a_lo0 + slot * a_tile16;
+            for (int t = 0; t < NT; ++t) {
+                const int tb = NT - 1 - t;
+                for (int hh = 1; hh >= 0; --hh, ++qq) {
+                    const int acc = 2 * w + (int)(qq & 1u);
+                    mbar_wait_hot(smem_u32(&t_empty[acc]), ((qq >> 1) & 1u) ^ 1u);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t d_tmem = tmem_base + (uint32_t)acc * 128u;
+                        const uint32_t b_lo = b_lo0 + tb * b_half16 + (uint32_t)hh * h16;
+                        if (!(dbg & 2)) {
+                            for (int kb = 0; kb < KB; ++kb)
+                                for (int ks = 0; ks < ksteps; ++ks) {
+                                    const uint64_t ad = desc_join(dhi, a_lo + kb * kb_a16 + ks * 2);
+                                    const uint64_t bd = desc_join(dhi, b_lo + kb * kb_b16 + ks * 2);
+                                    const uint32_t accum = (kb | ks) ? 1u : 0u;
+                                    if (f8) mma2_f8(d_tmem, ad, bd, idesc128, accum);
+                                    else mma2_f16(d_tmem, ad, bd, idesc128, accum);
+                                }
+                        }
+                        tc_commit_pair(smem_u32(&t_full[acc]));
+                        if (t == NT - 1 && hh == 0) tc_commit_pair(smem_u32(&a_empty[slot]));
+                    }
+                    __syncwarp();
+                }
+            }
+            for (int u = 0; u < 2; ++u)
+                if (++slot == SA) { slot = 0; aph ^= 1; }
+        }
+    };
+
     if (warp == W_CRES) {
         // ------------------------------------------------ resident centroid halves (once)
         if (elect_one()) {
             const uint32_t fb = smem_u32(b_full);
             if (leader) mbar_expect_tx(fb, 2u * p.NT * p.b_half_bytes);
+            // boxes of p.box_rows rows: the standard layout (CTA r: rows t NB + r NB/2 + [0, NB/2))
+            // or, for rbh, rows t 256 + u 128 + r 64 + [0, 64) at row offset 64 u
+            const int nbox = half / p.box_rows;
             for (int t = 0; t < p.NT; ++t) {
                 const uint32_t dst = smem_u32(b_base + (size_t)t * p.b_half_bytes);
                 for (int kb = 0; kb < p.KB; ++kb)
-                    tma_load_2d_pair(dst + kb * p.kb_b_bytes, &tmap_c, kb * eps,
-                                     t * p.NB + (int)rank * half, fb);
+                    for (int u = 0; u < nbox; ++u) {
+                        const int row = rbh ? t * 256 + u * 128 + (int)rank * 64
+                                            : t * p.NB + (int)rank * half + u * p.box_rows;
+                        tma_load_2d_pair(dst + kb * p.kb_b_bytes + u * p.box_rows * p.SWZ, &tmap_c,
+                                         kb * eps, row, fb);
+                    }
             }
         }
         __syncwarp();
+        if (rbh && leader) rbh_mma(1);                 // the second warpgroup's MMA issuer
         if (fwd) {
             int b = 0;
             for (int64_t rb = pair; rb < num_rb; rb += npairs)
@@ -330,6 +406,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             // cn init: the first use of each accumulator waits for the epilogue's pre-load (its
             // first release), so the phase bit starts flipped
             uint32_t aph = 0, tph = cninit ? 1u : 0u, ai = 0;
+            if (rbh) rbh_mma(0);
             if (rbalt) {
                 // groups of R row-blocks (one MMA each, N = NB) into one accumulator of R NB-column
                 // blocks, one "accumulator full" commit per group; the row-blocks keep their own
@@ -419,7 +496,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                     if (++slot == SA) { slot = 0; aph ^= 1; }
                 }
             }
-            for (int64_t rb = pair; rb < num_rb && !hsplit && !rbalt; rb += npairs) {
+            for (int64_t rb = pair; rb < num_rb && !hsplit && !rbalt && !rbh; rb += npairs) {
 #if MPK_PAIR_TRACE_RB
                 // fine stamps of the MMA loop (rows TRACE_T/2 + ai): loop top, a_full ok, fenced,
                 // t_empty ok, elected, MMAs issued, t_full committed, a_empty committed
@@ -488,7 +565,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 if (++slot == SA) { slot = 0; aph ^= 1; }
             }
         }
-    } else if (warp == W_RBEND && (CAND || rbalt)) {
+    } else if (warp == W_RBEND && (CAND || rbalt || rbh)) {
         // no row-block end in CAND mode; the epilogue does its own with row-block alternation
     } else if (warp == W_RBEND) {
         // ------------------------------------------------ row-block end (both CTAs): merge the
@@ -791,12 +868,110 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 if (p.acc_changed && my_changed != 0) atomicAdd(p.acc_changed, (double)my_changed);
             }
         };
+        if (rbh) {
+            // this warpgroup's row-blocks; per row-block NT tiles x 2 halves in decreasing column
+            // order, half-tile q into accumulator 2 wg + (q & 1); the point data one own row-block
+            // ahead; the row-block end in place
+            double my_sse = 0.0;
+            int my_changed = 0;
+            const int64_t step = 2 * npairs * rows_per_rb;
+            int64_t row = (pair + wg * npairs) * rows_per_rb + rank * P_BM + q;
+            const int64_t row_end = num_rb * rows_per_rb;
+            float m2_a = -2.0f, xn_a = 0.0f;
+            int old_a = 0;
+            auto load_pt = [&](int64_t r) {
+                if (r < n) {
+                    xn_a = p.xn[r];
+                    old_a = p.labels[r];
+                    if (guard) m2_a = -2.0f * p.sx[r];
+                }
+            };
+            load_pt(row);
+            uint32_t qq = 0;
+            for (; row < row_end; row += step) {
+                const float m2 = m2_a, xn = xn_a;
+                const int old = old_a;
+                load_pt(row + step);
+                float cv[NCH];
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) cv[c] = INFINITY;
+                uint64_t s2[NCH / 2];
+#pragma unroll
+                for (int m = 0; m < NCH / 2; ++m) s2[m] = pack2(-1.0f, -1.0f);
+                for (int t = 0; t < NT; ++t) {
+                    const int tb = NT - 1 - t;
+                    for (int hh = 1; hh >= 0; --hh, ++qq) {
+                        const int acc = 2 * wg + (int)(qq & 1u);
+                        mbar_wait_hot(smem_u32(&t_full[acc]), (qq >> 1) & 1u);
+                        tc_fence_after();
+                        const uint32_t col0 = tmem_base + lane_addr + (uint32_t)acc * 128u;
+                        const int jb = tb * 256 + hh * 128;        // centroid of accumulator column 0
+                        auto release = [&]() {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&t_empty[acc]), 0));
+                        };
+                        auto fold_half = [&](auto guard_tag) {
+                            constexpr bool GD = decltype(guard_tag)::value;
+                            // chunks 3 .. 0; the next chunk's TMEM load in flight while this one
+                            // folds; released once the last load has landed
+                            uint32_t va[32], vb[32];
+                            ChunkCn<4, GD> cq;
+                            tmem_ld32(col0 + 96, va);
+                            tmem_wait_ld_dep(va);
+                            tmem_ld32(col0 + 64, vb);
+                            load_chunk_cn<4, GD>(cn_s, sc_s, jb + 96, cq);
+                            fold_rev_m3<4, GD>(va, cq, m2, cv, s2);
+                            tmem_wait_ld_dep(vb);
+                            tmem_ld32(col0 + 32, va);
+                            load_chunk_cn<4, GD>(cn_s, sc_s, jb + 64, cq);
+                            fold_rev_m3<4, GD>(vb, cq, m2, cv, s2);
+                            tmem_wait_ld_dep(va);
+                            tmem_ld32(col0, vb);
+                            load_chunk_cn<4, GD>(cn_s, sc_s, jb + 32, cq);
+                            fold_rev_m3<4, GD>(va, cq, m2, cv, s2);
+                            tmem_wait_ld_dep(vb);
+                            release();
+                            load_chunk_cn<4, GD>(cn_s, sc_s, jb, cq);
+                            fold_rev_m3<4, GD>(vb, cq, m2, cv, s2);
+                        };
+                        if (dbg & 1) release();
+                        else if (guard) fold_half(std::true_type{});
+                        else fold_half(std::false_type{});
+                    }
+                }
+                // chains -> column: key = 8 v + c with v the forward group ordinal = the column
+                float cs[NCH];
+#pragma unroll
+                for (int m = 0; m < NCH / 2; ++m) unpack2(s2[m], cs[2 * m], cs[2 * m + 1]);
+                float b1 = cv[0], k1 = fmaf(cs[0], -8.0f, -8.0f);
+#pragma unroll
+                for (int c = 1; c < NCH; ++c) {
+                    const float kc = fmaf(cs[c], -8.0f, (float)(c - 8));
+                    if (cv[c] < b1 || (cv[c] == b1 && kc < k1)) { b1 = cv[c]; k1 = kc; }
+                }
+                int j1 = (int)k1;
+                if (!(b1 < INFINITY) || !(xn < INFINITY)) j1 = 0;
+                if (row < n) {
+                    p.labels[row] = j1;
+                    my_changed += old != j1;
+                    const float md = xn + b1;
+                    my_sse += md > 0.0f ? (double)md : 0.0;
+                }
+            }
+            my_sse = warp_sum(my_sse);
+            my_changed = warp_sum(my_changed);
+            if (lane == 0) {
+                if (p.acc_sse) atomicAdd(p.acc_sse, my_sse);
+                if (p.acc_changed && my_changed != 0) atomicAdd(p.acc_changed, (double)my_changed);
+            }
+        }
         if (rbalt) {
             if (p.rbr == 4) rbalt_loop(std::integral_constant<int, 4>{});
             else if (p.rbr == 2) rbalt_loop(std::integral_constant<int, 2>{});
             else rbalt_loop(std::integral_constant<int, 1>{});
         }
-        for (int64_t rb = pair; rb < num_rb && !rbalt; rb += npairs, ++rbi) {
+        for (int64_t rb = pair; rb < num_rb && !rbalt && !rbh; rb += npairs, ++rbi) {
             const int64_t row = rb * rows_per_rb + rank * P_BM + q;
             const float m2 = m2_n;
             const float T = T_n;                                             // CAND threshold
@@ -1206,6 +1381,9 @@ bool pair_plan(int dist, int d, int d_pad, int k, PairParams* pp, size_t* smem_b
     p.kb_b_bytes = (uint32_t)(NB / 2) * SWZ;
     p.is_f8 = dist == KMEANS_E5M2;
     if (const char* e = getenv("MPK_PAIR_DBG")) p.dbg = atoi(e);
+    // 64-row boxes for 256-column tiles (the rbh layout loads each CTA's half-tile as two
+    // boxes from different centroid ranges; the standard layout as two consecutive ones)
+    p.box_rows = NB == 256 ? 64 : NB / 2;
 
     p.u_low = dist == KMEANS_FP16 ? 0x1p-11 : (dist == KMEANS_BF16 ? 0x1p-8 : 0x1p-3);
     p.eta_low = dist == KMEANS_FP16 ? 0x1p-25 : (dist == KMEANS_BF16 ? 0x1p-134 : 0x1p-17);
@@ -1216,7 +1394,7 @@ bool pair_plan(int dist, int d, int d_pad, int k, PairParams* pp, size_t* smem_b
     return true;
 }
 
-int pair_box_rows(const PairParams& p) { return p.NB / 2; }
+int pair_box_rows(const PairParams& p) { return p.box_rows; }
 
 cudaError_t pair_set_smem(size_t bytes) {
     cudaError_t e = cudaFuncSetAttribute(assign_pair_kernel<PAIR_ASSIGN>,

@@ -11,6 +11,7 @@ struct PairParams {
     int64_t n;
     int k, k_pad, d, d_pad, NB, NT, KB, SWZ, SA, nacc, tmem_cols;
     int rbr;                 // one tile per row-block: row-blocks per accumulator (1..4)
+    int box_rows;            // TMA box rows of the centroid map (64 for 256-column tiles)
     uint32_t a_tile_bytes;   // 128 rows x row bytes (this CTA's half of M = 256)
     uint32_t b_half_bytes;   // NB/2 rows x row bytes (this CTA's half of one centroid tile)
     uint32_t kb_a_bytes, kb_b_bytes;
@@ -33,7 +34,8 @@ struct PairParams {
     int cand_q;
     int dbg;                 // debug (timing only): bit0 skip the fold, bit1 skip MMAs, bit2 fold probe,
                              // bit3 skip the X~ loads, bit4 skip the row-block end work;
-                             // bit5 (same results): no row-block alternation (column split)
+                             // bit5 (same results): no row-block alternation (column split);
+                             // bit6 (same results): no row-block halves (rbh)
     unsigned long long* trace;   // debug (MPK_PAIR_TRACE): per-tile clock64 stamps of CTA 0
 };
 
