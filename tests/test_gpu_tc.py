@@ -127,6 +127,29 @@ def test_tc_one_tile_alternation_equals_column_split(dist, shape, monkeypatch):
     assert abs(out[0][1] - out[1][1]) <= 1e-9 * abs(out[1][1])
 
 
+@pytest.mark.parametrize("dist,guard", [("fp16", False), ("bf16", True)])
+def test_tc_row_block_halves_equal_column_split(dist, guard, monkeypatch):
+    """C5 shape (four 256-column tiles per row-block): the warpgroups' own half-tile
+    accumulators ("rbh") and the column split (MPK_PAIR_DBG bit 6) visit the same values in the
+    same decreasing column order: identical labels, the SSE equal up to its summation order."""
+    n, d, k = 120_011, 128, 1024
+    X, _ = synth.blobs(n, d, 300, sigma=1.5, seed=9, dtype=np.float32)
+    C = synth.init_rows(X, k, 2)
+    out = []
+    for dbg in ("0", "64"):
+        monkeypatch.setenv("MPK_PAIR_DBG", dbg)
+        km = mpk.KMeans(n, d, k, "fp32", dist, guard=guard)
+        mpk.kmeans_set_centroids(km.h, dev(C))
+        lab = torch.empty(n, dtype=torch.int32, device="cuda")
+        sse = km.assign(dev(X), lab)
+        assert km.stats()["tc_variant"] == 2
+        km.close()
+        out.append((lab.cpu().numpy(), sse))
+    monkeypatch.delenv("MPK_PAIR_DBG")
+    assert np.array_equal(out[0][0], out[1][0])
+    assert abs(out[0][1] - out[1][1]) <= 1e-9 * abs(out[1][1])
+
+
 @pytest.mark.parametrize("dist,k,variant", [("fp16", 2048, 1), ("bf16", 2048, 1),
                                             ("e5m2", 2048, 2), ("e5m2", 4096, 1)])
 def test_tc_large_k_streaming(dist, k, variant, monkeypatch):

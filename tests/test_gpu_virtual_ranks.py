@@ -97,6 +97,24 @@ def test_virtual_ranks_fp32_fx_bit_identical(g, dist):
 
 
 @pytest.mark.parametrize("g", [2, 3])
+@pytest.mark.parametrize("dist", ["fp16", "bf16"])
+def test_virtual_ranks_row_block_halves_bit_identical(g, dist):
+    """The C5 shape (d = 128, k = 1024: four 256-column tiles per row-block, the warpgroups'
+    own half-tile accumulators, k_assign_tc2.cu "rbh") on every shard: the g-rank fit equals the
+    1-rank fit bit for bit."""
+    X, _, C0 = synth.make("c5_vq_10m", n=60_013, seed=8)
+    flags = mpk.KMEANS_NORM_NONE
+    lab1, cent1, sse1, st1 = _plain_fit(X, C0, "fp32", dist, flags, 3)
+    labg, cents, sses, iters, stats = _virtual_fit(X, C0, "fp32", dist, flags, 3, g)
+    assert st1["dist_kernel"] == "tcgen05" and st1["tc_variant"] == 2
+    np.testing.assert_array_equal(labg, lab1)
+    for c in cents:
+        np.testing.assert_array_equal(c.view(np.uint32), cent1.view(np.uint32))
+    for s in sses:
+        assert abs(s - sse1) <= 1e-12 * sse1
+
+
+@pytest.mark.parametrize("g", [2, 3])
 @pytest.mark.parametrize("dist", ["fp16", "e5m2"])
 def test_virtual_ranks_one_tile_groups_bit_identical(g, dist):
     """k = 64 (one 64-column tile per row-block: the warpgroups alternate groups of four
