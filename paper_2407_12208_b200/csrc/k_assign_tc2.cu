@@ -303,7 +303,13 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                     const int acc = 2 * w + (int)(qq & 1u);
                     mbar_wait_hot(smem_u32(&t_empty[acc]), ((qq >> 1) & 1u) ^ 1u);
                     tc_fence_after();
+#if MPK_PAIR_TRACE_RB
+                    const bool trq = p.trace && blockIdx.x == 0 && w == 0 && qq < TRACE_T;
+#endif
                     if (elect_one()) {
+#if MPK_PAIR_TRACE_RB
+                        if (trq) p.trace[qq * 8 + 0] = clock64();
+#endif
                         const uint32_t d_tmem = tmem_base + (uint32_t)acc * 128u;
                         const uint32_t b_lo = b_lo0 + tb * b_half16 + (uint32_t)hh * h16;
                         if (!(dbg & 2)) {
@@ -318,6 +324,9 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                         }
                         tc_commit_pair(smem_u32(&t_full[acc]));
                         if (t == NT - 1 && hh == 0) tc_commit_pair(smem_u32(&a_empty[slot]));
+#if MPK_PAIR_TRACE_RB
+                        if (trq) p.trace[qq * 8 + 1] = clock64();
+#endif
                     }
                     __syncwarp();
                 }
@@ -902,14 +911,25 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                     const int tb = NT - 1 - t;
                     for (int hh = 1; hh >= 0; --hh, ++qq) {
                         const int acc = 2 * wg + (int)(qq & 1u);
+#if MPK_PAIR_TRACE_RB
+                        const bool trq = trace && blockIdx.x == 0 && wg == 0 && (warp & 3) == 0 &&
+                                         lane == 0 && qq < TRACE_T;
+                        if (trq) trace[qq * 8 + 5] = clock64();
+#endif
                         mbar_wait_hot(smem_u32(&t_full[acc]), (qq >> 1) & 1u);
                         tc_fence_after();
+#if MPK_PAIR_TRACE_RB
+                        if (trq) trace[qq * 8 + 2] = clock64();
+#endif
                         const uint32_t col0 = tmem_base + lane_addr + (uint32_t)acc * 128u;
                         const int jb = tb * 256 + hh * 128;        // centroid of accumulator column 0
                         auto release = [&]() {
                             tc_fence_before();
                             __syncwarp();
                             if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&t_empty[acc]), 0));
+#if MPK_PAIR_TRACE_RB
+                            if (trq) trace[qq * 8 + 3] = clock64();
+#endif
                         };
                         auto fold_half = [&](auto guard_tag) {
                             constexpr bool GD = decltype(guard_tag)::value;
@@ -938,6 +958,9 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                         if (dbg & 1) release();
                         else if (guard) fold_half(std::true_type{});
                         else fold_half(std::false_type{});
+#if MPK_PAIR_TRACE_RB
+                        if (trq) trace[qq * 8 + 4] = clock64();
+#endif
                     }
                 }
                 // chains -> column: key = 8 v + c with v the forward group ordinal = the column
