@@ -165,9 +165,14 @@ struct TcPlan;                  // opaque (TMA descriptors etc.)
 TcPlan* tc_plan_create(int dist, int64_t n, int d, int d_pad, int k, const void* Xl,
                        const void* Cl, std::string* err);
 void tc_plan_destroy(TcPlan*);
+// fx (optional; the Lloyd loop with the fixed-point update): the CTA-pair kernel lists the
+// changed rows itself (FxState::list / seg_cnt, gate[0]) so the update skips fx_diff_kernel;
+// *fx_listed tells whether it did
+struct FxState;
 cudaError_t launch_assign_tc(TcPlan* plan, const Problem& p, const float* xn, const float* sx,
                              const float* cn, const float* sc, int32_t* labels, double* acc_sse,
-                             double* acc_changed, cudaStream_t s);
+                             double* acc_changed, cudaStream_t s, FxState* fx = nullptr,
+                             bool* fx_listed = nullptr);
 // Final pass (Alg 3 step 7) as a certified tensor-core filter: rows whose top-2 gap exceeds the
 // error bound get the filter's argmin (= the working-precision argmin); the others are appended
 // to fb_rows (count in *fb_count) for launch_assign_simt(row_list = fb_rows).
@@ -240,8 +245,11 @@ struct FxState {
     long long* Shi = nullptr;   // k*d: sum of i1 (coarse parts)
     long long* Slo = nullptr;   // k*d: sum of i2 (fine parts)
     long long* part = nullptr;  // piece totals of multi-piece clusters (hi d, lo d per slot)
-    int32_t* prev = nullptr;    // n: labels of the previous iteration
-    int3* list = nullptr;       // changed rows (row, old, new), capacity gate[1]
+    int32_t* prev = nullptr;    // n: labels of the previous iteration (fx_diff_kernel)
+    // changed rows (row, old, new), by 32-row segment: segment s (rows 32 s ..) lists its
+    // seg_cnt[s] changed rows at list[32 s ..]; gate[0] counts them all
+    int3* list = nullptr;
+    int* seg_cnt = nullptr;
     long long* gShi = nullptr;  // several ranks: the allreduced totals and counts
     long long* gSlo = nullptr;
     int* gcnt = nullptr;
@@ -251,9 +259,11 @@ struct FxState {
 cudaError_t launch_fx_colmax(const float* Xw, int64_t n, int d, FxState& fx, bool have_amax,
                              cudaStream_t s);
 cudaError_t launch_fx_scale(int d, FxState& fx, cudaStream_t s);
+// listed: the distance kernel has produced the changed-row list and gate[0] (see
+// launch_assign_tc); else fx_diff_kernel finds them from prev
 cudaError_t launch_update_fx(const float* Xw, int64_t n, int d, int k, const int32_t* labels,
                              int* cnt, int* offs, int* cursor, int* perm, const UpdateScratch& us,
-                             FxState& fx, cudaStream_t s);
+                             FxState& fx, cudaStream_t s, bool listed = false);
 cudaError_t launch_finalize_fx(int64_t k, int d, const FxState& fx, const long long* Shi,
                                const long long* Slo, const int* cnt, const double* acc,
                                AccLayout L, float* Cw, IterRec* rec, cudaStream_t s);

@@ -560,7 +560,8 @@ static cudaError_t launch_impl(TcPlan* pl, const tcdev::Params& p, bool final_mo
 
 cudaError_t launch_assign_tc(TcPlan* pl, const Problem& pb, const float* xn, const float* sx,
                              const float* cn, const float* sc, int32_t* labels, double* acc_sse,
-                             double* acc_changed, cudaStream_t s) {
+                             double* acc_changed, cudaStream_t s, FxState* fx, bool* fx_listed) {
+    if (fx_listed) *fx_listed = false;
     tcdev::Params p = pl->prm;
     p.n = pb.n;
     p.guard = pb.guard;
@@ -572,6 +573,12 @@ cudaError_t launch_assign_tc(TcPlan* pl, const Problem& pb, const float* xn, con
         tcdev::PairParams q = pl->pp;
         q.n = pb.n; q.guard = pb.guard; q.xn = xn; q.sx = sx; q.cn = cn; q.sc = sc;
         q.labels = labels; q.acc_sse = acc_sse; q.acc_changed = acc_changed;
+        if (fx && !getenv("MPK_NO_FX_LIST")) {
+            cudaError_t e = cudaMemsetAsync(fx->gate, 0, sizeof(int), s);   // gate[0]: count
+            if (e != cudaSuccess) return e;
+            q.fx_list = fx->list; q.fx_seg_cnt = fx->seg_cnt; q.fx_gate = fx->gate;
+            if (fx_listed) *fx_listed = true;
+        }
         return tcdev::pair_launch(pl->tmap_x, pl->tmap_c, q, tcdev::PAIR_ASSIGN, pl->smem_bytes, s);
     }
     return launch_impl(pl, p, false, s);

@@ -117,6 +117,16 @@ MPK_DEV void named_bar_sync(int id, int nthreads) {
 MPK_DEV void named_bar_arrive(int id, int nthreads) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+// The changed rows of a warp's 32-row segment (lane l = row 32 s + l) for the fixed-point
+// update (PairParams::fx_list), called by all 32 lanes: a ballot, no atomics (the count goes to
+// fx_gate[0] once per warp at the end of the kernel).
+MPK_DEV void fx_list_rows(const PairParams& p, bool ch, bool in_range, int64_t row, int old, int nw) {
+    const unsigned m = __ballot_sync(0xffffffffu, ch);
+    const int lane = threadIdx.x & 31;
+    const int64_t seg = row >> 5;
+    if (lane == 0 && in_range) p.fx_seg_cnt[seg] = __popc(m);
+    if (ch) p.fx_list[seg * 32 + __popc(m & ((1u << lane) - 1u))] = make_int3((int)row, old, nw);
+}
 
 // CAND: one 32-column chunk -> candidate columns (value computed exactly as in fold32)
 template <bool GUARD>
@@ -635,10 +645,12 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                     }
                 }
                 const int64_t row = rb * rows_per_rb + rank * P_BM + q;
-                if (row >= n) continue;
                 // ||x||^2 not finite (a NaN / inf coordinate): every distance xn + v is NaN or
                 // +inf, and the scan's default is column 0 (the kernel's v omits xn)
                 if (!FINAL && !(xn_r[u] < INFINITY)) j1 = 0;
+                if (!FINAL && p.fx_list)
+                    fx_list_rows(p, row < n && old_r[u] != j1, row - lane < n, row, old_r[u], j1);
+                if (row >= n) continue;
                 p.labels[row] = j1;
                 if (!FINAL) {
                     if (old_r[u] != j1) my_changed += 1.0;
@@ -682,6 +694,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             if (lane == 0) {
                 if (p.acc_sse) atomicAdd(p.acc_sse, my_sse);
                 if (p.acc_changed && my_changed != 0.0) atomicAdd(p.acc_changed, my_changed);
+                if (p.fx_list && my_changed != 0.0) atomicAdd(p.fx_gate, (int)my_changed);
             }
         }
     } else {
@@ -857,6 +870,8 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                     // no value below +inf, or ||x||^2 not finite: the forward scan's default
                     // column 0
                     if (!(b1 < INFINITY) || !(xn < INFINITY)) j1 = 0;
+                    if (p.fx_list)
+                        fx_list_rows(p, row < n && old_c[r] != j1, row - lane < n, row, old_c[r], j1);
                     if (row < n) {
                         p.labels[row] = j1;
                         my_changed += old_c[r] != j1;
@@ -875,6 +890,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             if (lane == 0) {
                 if (p.acc_sse) atomicAdd(p.acc_sse, my_sse);
                 if (p.acc_changed && my_changed != 0) atomicAdd(p.acc_changed, (double)my_changed);
+                if (p.fx_list && my_changed != 0) atomicAdd(p.fx_gate, my_changed);
             }
         };
         if (rbh) {
@@ -975,6 +991,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 }
                 int j1 = (int)k1;
                 if (!(b1 < INFINITY) || !(xn < INFINITY)) j1 = 0;
+                if (p.fx_list) fx_list_rows(p, row < n && old != j1, row - lane < n, row, old, j1);
                 if (row < n) {
                     p.labels[row] = j1;
                     my_changed += old != j1;
@@ -987,6 +1004,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             if (lane == 0) {
                 if (p.acc_sse) atomicAdd(p.acc_sse, my_sse);
                 if (p.acc_changed && my_changed != 0) atomicAdd(p.acc_changed, (double)my_changed);
+                if (p.fx_list && my_changed != 0) atomicAdd(p.fx_gate, my_changed);
             }
         }
         if (rbalt) {

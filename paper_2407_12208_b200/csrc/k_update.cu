@@ -626,17 +626,16 @@ MPK_DEV void fx_q(float x, float2 c, int& i1, int& i2) {
 // re-summation runs instead.
 __global__ void __launch_bounds__(256)
 fx_diff_kernel(const int32_t* __restrict__ labels, int32_t* __restrict__ prev, int64_t n,
-               int3* __restrict__ list, int* __restrict__ gate) {
-    // one list-counter atomic per block and sweep (a single hot counter serialised the warps'
-    // atomics when many rows change); any order of the list is fine (integer updates)
+               int3* __restrict__ list, int* __restrict__ seg_cnt, int* __restrict__ gate) {
+    // each warp lists the changed rows of its 32-row segments (one ballot: no slot atomics);
+    // one count atomic per block and sweep (a single hot counter serialised the warps when many
+    // rows change); any order of the list is fine (integer updates)
     constexpr int R = 4;                                  // rows per thread in flight
-    __shared__ int wcount[8], wbase[8], bbase;
+    __shared__ int wcount[8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int cap = gate[1];
     const int64_t span = (int64_t)blockDim.x * R;
     for (int64_t base = (int64_t)blockIdx.x * span; base < n; base += (int64_t)gridDim.x * span) {
         int l[R], o[R];
-        unsigned m[R];
         int tot = 0;
 #pragma unroll
         for (int u = 0; u < R; ++u) {
@@ -646,60 +645,59 @@ fx_diff_kernel(const int32_t* __restrict__ labels, int32_t* __restrict__ prev, i
         }
 #pragma unroll
         for (int u = 0; u < R; ++u) {
-            const int64_t i = base + u * blockDim.x + threadIdx.x;
+            const int64_t i = base + u * blockDim.x + threadIdx.x;   // 32-aligned per warp
             const bool ch = i < n && l[u] != o[u];
-            m[u] = __ballot_sync(0xffffffffu, ch);
-            tot += __popc(m[u]);
-            if (ch) prev[i] = l[u];
+            const unsigned m = __ballot_sync(0xffffffffu, ch);
+            const int64_t seg = i >> 5;
+            if (lane == 0 && i < n) seg_cnt[seg] = __popc(m);
+            if (ch) {
+                list[seg * 32 + __popc(m & ((1u << lane) - 1u))] = make_int3((int)i, o[u], l[u]);
+                prev[i] = l[u];
+            }
+            tot += __popc(m);
         }
         if (lane == 0) wcount[warp] = tot;
         __syncthreads();
         if (threadIdx.x == 0) {
             int run = 0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { wbase[w] = run; run += wcount[w]; }
-            bbase = run ? atomicAdd(&gate[0], run) : 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) run += wcount[w];
+            if (run) atomicAdd(&gate[0], run);
         }
-        __syncthreads();
-        int slot = bbase + wbase[warp];
-#pragma unroll
-        for (int u = 0; u < R; ++u) {
-            if (m[u] & (1u << lane)) {
-                const int sl = slot + __popc(m[u] & ((1u << lane) - 1u));
-                if (sl < cap)
-                    list[sl] = make_int3((int)(base + u * blockDim.x + threadIdx.x), o[u], l[u]);
-            }
-            slot += __popc(m[u]);
-        }
-        __syncthreads();                                  // wcount / wbase reused next sweep
+        __syncthreads();                                  // wcount reused next sweep
     }
 }
-// Incremental update from the changed-row list: a warp per row, lanes over columns.
+// Incremental update from the changed-row list: a warp per 32-row segment, its changed rows in
+// turn, lanes over columns.
 __global__ void __launch_bounds__(256)
-fx_incr_kernel(const float* __restrict__ X, int d, const int3* __restrict__ list,
-               const int* __restrict__ gate, const float2* __restrict__ sc,
-               long long* __restrict__ Shi, long long* __restrict__ Slo, int* __restrict__ cnt) {
-    const int m = gate[0];
-    if (m > gate[1]) return;                              // the full path ran
+fx_incr_kernel(const float* __restrict__ X, int64_t n, int d, const int3* __restrict__ list,
+               const int* __restrict__ seg_cnt, const int* __restrict__ gate,
+               const float2* __restrict__ sc, long long* __restrict__ Shi,
+               long long* __restrict__ Slo, int* __restrict__ cnt) {
+    if (gate[0] > gate[1]) return;                        // the full path ran
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t w = warp; w < m; w += nwarps) {
-        const int3 e = list[w];
-        const float* xr = X + (int64_t)e.x * d;
-        for (int t = lane; t < d; t += 32) {
-            int i1, i2;
-            fx_q(__ldg(xr + t), sc[t], i1, i2);
-            const long long hi = i1, lo = i2;
-            atomicAdd(reinterpret_cast<unsigned long long*>(Shi + (int64_t)e.z * d + t), (unsigned long long)hi);
-            atomicAdd(reinterpret_cast<unsigned long long*>(Slo + (int64_t)e.z * d + t), (unsigned long long)lo);
-            if (e.y >= 0) {
-                atomicAdd(reinterpret_cast<unsigned long long*>(Shi + (int64_t)e.y * d + t), (unsigned long long)(-hi));
-                atomicAdd(reinterpret_cast<unsigned long long*>(Slo + (int64_t)e.y * d + t), (unsigned long long)(-lo));
+    const int64_t nseg = (n + 31) >> 5;
+    for (int64_t sg = warp; sg < nseg; sg += nwarps) {
+        const int c = seg_cnt[sg];
+        for (int q = 0; q < c; ++q) {
+            const int3 e = list[sg * 32 + q];
+            const float* xr = X + (int64_t)e.x * d;
+            for (int t = lane; t < d; t += 32) {
+                int i1, i2;
+                fx_q(__ldg(xr + t), sc[t], i1, i2);
+                const long long hi = i1, lo = i2;
+                atomicAdd(reinterpret_cast<unsigned long long*>(Shi + (int64_t)e.z * d + t), (unsigned long long)hi);
+                atomicAdd(reinterpret_cast<unsigned long long*>(Slo + (int64_t)e.z * d + t), (unsigned long long)lo);
+                if (e.y >= 0) {
+                    atomicAdd(reinterpret_cast<unsigned long long*>(Shi + (int64_t)e.y * d + t), (unsigned long long)(-hi));
+                    atomicAdd(reinterpret_cast<unsigned long long*>(Slo + (int64_t)e.y * d + t), (unsigned long long)(-lo));
+                }
             }
-        }
-        if (lane == 0) {
-            atomicAdd(&cnt[e.z], 1);
-            if (e.y >= 0) atomicSub(&cnt[e.y], 1);
+            if (lane == 0) {
+                atomicAdd(&cnt[e.z], 1);
+                if (e.y >= 0) atomicSub(&cnt[e.y], 1);
+            }
         }
     }
 }
@@ -964,14 +962,16 @@ cudaError_t launch_fx_scale(int d, FxState& fx, cudaStream_t s) {
 
 cudaError_t launch_update_fx(const float* Xw, int64_t n, int d, int k, const int32_t* labels,
                              int* cnt, int* offs, int* cursor, int* perm, const UpdateScratch& us,
-                             FxState& fx, cudaStream_t s) {
-    launches_add(8);     // diff, 6 gated full-path kernels, incremental
-    // gate[0] = changed rows (reset), gate[1] = capacity (kept)
-    cudaError_t e = cudaMemsetAsync(fx.gate, 0, sizeof(int), s);
-    if (e != cudaSuccess) return e;
-    int g = (int)std::min<int64_t>((n + 1023) / 1024, kNumSMs * 8);
-    if (g < 1) g = 1;
-    fx_diff_kernel<<<g, 256, 0, s>>>(labels, fx.prev, n, fx.list, fx.gate);
+                             FxState& fx, cudaStream_t s, bool listed) {
+    launches_add(listed ? 7 : 8);     // [diff,] 6 gated full-path kernels, incremental
+    if (!listed) {
+        // gate[0] = changed rows (reset), gate[1] = capacity (kept)
+        cudaError_t e = cudaMemsetAsync(fx.gate, 0, sizeof(int), s);
+        if (e != cudaSuccess) return e;
+        int g = (int)std::min<int64_t>((n + 1023) / 1024, kNumSMs * 8);
+        if (g < 1) g = 1;
+        fx_diff_kernel<<<g, 256, 0, s>>>(labels, fx.prev, n, fx.list, fx.seg_cnt, fx.gate);
+    }
     const int* gate = fx.gate;
     // full re-summation, gated: runs only when the list overflowed
     const int64_t nb = (n + kDetRows - 1) / kDetRows;
@@ -999,7 +999,8 @@ cudaError_t launch_update_fx(const float* Xw, int64_t n, int d, int k, const int
     segsum_fix_fx_kernel<<<dim3((unsigned)k, (unsigned)((d + 31) / 32)), 256, 0, s>>>(
         d, offs, us.mpo, fx.part, fx.Shi, fx.Slo, gate);
     // incremental update, gated the other way
-    fx_incr_kernel<<<kNumSMs * 4, 256, 0, s>>>(Xw, d, fx.list, gate, fx.sc, fx.Shi, fx.Slo, cnt);
+    fx_incr_kernel<<<kNumSMs * 4, 256, 0, s>>>(Xw, n, d, fx.list, fx.seg_cnt, gate, fx.sc, fx.Shi,
+                                               fx.Slo, cnt);
     return cudaGetLastError();
 }
 

@@ -199,7 +199,7 @@ void free_all(kmeans_ctx* h) {
                     h->sc, h->labels, h->acc, h->cnt, h->offs, h->cursor, h->perm, h->trace,
                     h->shift, h->scale, h->partials, h->census, h->sse_dev, h->us.cb,
                     h->us.part, h->us.mpo, h->fx.amax, h->fx.sc, h->fx.isc, h->fx.Shi,
-                    h->fx.Slo, h->fx.part, h->fx.prev, h->fx.list, h->fx.gate, h->fx.gShi,
+                    h->fx.Slo, h->fx.part, h->fx.prev, h->fx.list, h->fx.seg_cnt, h->fx.gate, h->fx.gShi,
                     h->fx.gSlo, h->fx.gcnt};
     for (void* b : bufs)
         if (b) cudaFree(b);
@@ -338,7 +338,10 @@ int create_impl(int64_t n, int32_t d, int32_t k, int work, int dist, int flags,
         CA(dalloc(&h->fx.Slo, (size_t)k * d * sizeof(long long)));
         CA(dalloc(&h->fx.part, fx_part_bytes(n, d)));
         CA(dalloc(&h->fx.prev, (size_t)n * sizeof(int32_t)));
-        CA(dalloc(&h->fx.list, (size_t)h->fx.cap * sizeof(int3)));
+        // the list by 32-row segment: room for every row (the distance kernel writes each
+        // segment's changed rows at its own offset, no slot counter)
+        CA(dalloc(&h->fx.list, (size_t)((n + 31) / 32) * 32 * sizeof(int3)));
+        CA(dalloc(&h->fx.seg_cnt, (size_t)((n + 31) / 32) * sizeof(int)));
         CA(dalloc(&h->fx.gate, 4 * sizeof(int)));
         if (sharded) {          // sharded: each rank keeps its shard's totals; A6 sums them
             CA(dalloc(&h->fx.gShi, (size_t)k * d * sizeof(long long)));
@@ -570,7 +573,9 @@ int assign_mixed_tc(kmeans_ctx* h, int64_t rows, double* acc_sse, double* acc_ch
 }
 
 // Distance + argmin for the current centroids on h->n rows (loop iteration or assign).
-int run_assign(kmeans_ctx* h, int64_t rows, double* acc_sse, double* acc_changed) {
+int run_assign(kmeans_ctx* h, int64_t rows, double* acc_sse, double* acc_changed,
+               bool* fx_listed = nullptr) {
+    if (fx_listed) *fx_listed = false;
     Problem p{rows, h->d, h->k, h->d_pad, h->guard};
     if (h->delta > 0.0 && mixed_tc_ok(h)) {
         if (int rc = assign_mixed_tc(h, rows, acc_sse, acc_changed)) return rc;
@@ -581,7 +586,8 @@ int run_assign(kmeans_ctx* h, int64_t rows, double* acc_sse, double* acc_changed
     } else if (h->dist_kernel == DK_TCGEN05) {
         CK(launch_assign_tc(h->tc, p, (const float*)h->xn, h->guard ? (const float*)h->sx : nullptr,
                             (const float*)h->cn, h->guard ? (const float*)h->sc : nullptr,
-                            h->labels, acc_sse, acc_changed, h->stream));
+                            h->labels, acc_sse, acc_changed, h->stream,
+                            fx_listed ? &h->fx : nullptr, fx_listed));
     } else {
         CK(launch_assign_simt(h->work, h->dist, p, h->Xl, h->xn, h->guard ? h->sx : nullptr,
                               h->Cl, h->cn, h->guard ? h->sc : nullptr, h->labels, acc_sse,
@@ -927,12 +933,14 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
                                    h->guard ? h->sc : nullptr, h->labels, h->acc, h->L, s));
             if (timing) { CK(cudaEventRecord(t1, s)); CK(cudaEventRecord(t2, s)); }
         } else {
-            if (int rc = run_assign(h, n, h->acc + h->L.sse(), h->acc + h->L.changed()))
+            bool listed = false;     // the distance kernel listed the changed rows (FX)
+            if (int rc = run_assign(h, n, h->acc + h->L.sse(), h->acc + h->L.changed(),
+                                    fx_on ? &listed : nullptr))
                 return rc;                                                   // A4
             if (timing) CK(cudaEventRecord(t1, s));
             if (fx_on)
                 CK(launch_update_fx((const float*)h->Xw, n, d, k, h->labels, h->cnt, h->offs,
-                                    h->cursor, h->perm, h->us, h->fx, s));   // A5 (R9)
+                                    h->cursor, h->perm, h->us, h->fx, s, listed));   // A5 (R9)
             else
                 CK(launch_update(h->work, h->Xw, n, d, k, h->labels, h->cnt, h->offs, h->cursor,
                                  h->perm, h->acc, h->L, h->us, s));          // A5

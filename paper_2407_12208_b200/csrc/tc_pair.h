@@ -11,6 +11,13 @@ struct PairParams {
     int64_t n;
     int k, k_pad, d, d_pad, NB, NT, KB, SWZ, SA, nacc, tmem_cols;
     int rbr;                 // one tile per row-block: row-blocks per accumulator (1..4)
+    // ASSIGN in the Lloyd loop with the fixed-point update (k_update.cu FX): each warp writes
+    // the changed rows (row, old, new) of its 32-row segment s to fx_list[32 s ..] and their
+    // number to fx_seg_cnt[s]; each warp adds its total to fx_gate[0] once, at the end — what
+    // fx_diff_kernel would produce; nullptr: off
+    int3* fx_list;
+    int* fx_seg_cnt;
+    int* fx_gate;
     int box_rows;            // TMA box rows of the centroid map (64 for 256-column tiles)
     uint32_t a_tile_bytes;   // 128 rows x row bytes (this CTA's half of M = 256)
     uint32_t b_half_bytes;   // NB/2 rows x row bytes (this CTA's half of one centroid tile)

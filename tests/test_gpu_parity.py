@@ -390,6 +390,28 @@ def test_fx_incremental_equals_full_resummation(dist, norm):
     assert sum(1 for c in a["stats"]["changed_t"][2:] if c > 0) >= 2
 
 
+@pytest.mark.parametrize("dist,k", [("fp16", 1024), ("fp16", 256), ("e5m2", 64), ("bf16", 1024),
+                                    ("e5m2", 1024)])
+def test_fx_changed_rows_listed_by_the_distance_kernel(dist, k):
+    """The CTA-pair kernel lists the changed rows itself (PairParams::fx_list, by 32-row segment,
+    from every ASSIGN row end — column split / half split through warp 3, row-block alternation
+    and groups, row-block halves) instead of the update's fx_diff pass (MPK_NO_FX_LIST=1): the
+    same integer updates, so bit-identical labels, centres and traces over a fit whose labels
+    keep changing (incremental and full paths)."""
+    X, _, C0 = synth.make("c5_vq_10m", n=70_001, seed=11)
+    C0 = C0[:k].copy()
+    a = _fit_env({}, X, C0, "fp32", dist, norm="zscore", max_iter=10)
+    b = _fit_env({"MPK_NO_FX_LIST": "1"}, X, C0, "fp32", dist, norm="zscore", max_iter=10)
+    assert a["stats"]["dist_kernel"] == "tcgen05" and a["stats"]["tc_variant"] == 2
+    assert np.array_equal(a["labels"], b["labels"])
+    assert np.array_equal(a["centroids"].view(np.uint32), b["centroids"].view(np.uint32))
+    assert a["stats"]["sse_t"] == b["stats"]["sse_t"]
+    assert a["stats"]["changed_t"] == b["stats"]["changed_t"]
+    assert sum(1 for c in a["stats"]["changed_t"][2:] if c > 0) >= 2
+    # one launch (fx_diff) fewer per iteration
+    assert a["stats"]["n_kernel_launches"] == b["stats"]["n_kernel_launches"] - 10
+
+
 def test_fx_matches_fp64_summation_path():
     """The fixed-point totals (default) and the fp64 summation of R7 (MPK_NO_FX) agree: the means
     differ at most by the fp64 path's own rounding (a few fp32 ulps), labels essentially equal."""
