@@ -159,7 +159,11 @@ MPK_DEV void cand32(const uint32_t (&v)[32], const float* cn_s, const float* sc_
     }
 }
 
-template <int MODE>
+// RBHK: the ASSIGN instantiation for several 256-column tiles per row-block (C5), which carries
+// the row-block halves (fp16 / bf16) next to the half split (E5M2); the other instantiation
+// serves one tile per row-block (C3 / C4), where the rbh code compiled into the same kernel
+// cost ~10 % at C4 (and, the other way round, dropping it cost the half split ~3 %)
+template <int MODE, bool RBHK = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                    const __grid_constant__ CUtensorMap tmap_c, PairParams p) {
@@ -222,7 +226,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
     // Measured (tools/ab_pair.sh, C5): fp16 2.64 -> 2.48 ms; E5M2 1.96 -> 2.05 ms and C3 (one
     // tile) 74.5 -> 79 us are slower than the half split / row-block alternation, so fp16 / bf16
     // with several tiles per row-block only.
-    const bool rbh = MODE == PAIR_ASSIGN && MPK_PAIR_RBH && p.NB == 256 && p.NT >= 2 && !p.is_f8 &&
+    const bool rbh = RBHK && MODE == PAIR_ASSIGN && MPK_PAIR_RBH && p.NB == 256 && p.NT >= 2 && !p.is_f8 &&
                      P_EWG == 2 && p.tmem_cols >= 512 && p.box_rows == 64 &&
                      !(p.dbg & (16 | 32 | 64));
     const bool rbalt = MODE == PAIR_ASSIGN && MPK_PAIR_RBALT && p.NT == 1 && P_EWG == 2 && !rbh &&
@@ -1373,6 +1377,9 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
     }
 }
 
+// the launch picks the instantiation: RBHK for several 256-column tiles per row-block
+static bool pair_uses_rbh(const PairParams& p) { return p.NB == 256 && p.NT >= 2; }
+
 bool pair_plan(int dist, int d, int d_pad, int k, PairParams* pp, size_t* smem_bytes) {
     const int es = dist == KMEANS_E5M2 ? 1 : 2;
     const int RB = d_pad * es;
@@ -1441,6 +1448,9 @@ cudaError_t pair_set_smem(size_t bytes) {
     cudaError_t e = cudaFuncSetAttribute(assign_pair_kernel<PAIR_ASSIGN>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(assign_pair_kernel<PAIR_ASSIGN, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess)
         e = cudaFuncSetAttribute(assign_pair_kernel<PAIR_FINAL>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e == cudaSuccess)
@@ -1464,7 +1474,10 @@ cudaError_t pair_launch(const CUtensorMap& tmap_x, const CUtensorMap& tmap_c, co
         if (!buf) cudaMalloc(&buf, bytes);
         cudaMemsetAsync(buf, 0, bytes, s);
         q.trace = buf;
-        assign_pair_kernel<PAIR_ASSIGN><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, q);
+        if (pair_uses_rbh(q))
+            assign_pair_kernel<PAIR_ASSIGN, true><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, q);
+        else
+            assign_pair_kernel<PAIR_ASSIGN><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, q);
         cudaStreamSynchronize(s);
         static unsigned long long h[TRACE_T * 8];
         cudaMemcpy(h, buf, bytes, cudaMemcpyDeviceToHost);
@@ -1481,6 +1494,8 @@ cudaError_t pair_launch(const CUtensorMap& tmap_x, const CUtensorMap& tmap_c, co
         assign_pair_kernel<PAIR_FINAL><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, p);
     else if (mode == PAIR_CAND)
         assign_pair_kernel<PAIR_CAND><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, p);
+    else if (pair_uses_rbh(p))
+        assign_pair_kernel<PAIR_ASSIGN, true><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, p);
     else
         assign_pair_kernel<PAIR_ASSIGN><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, p);
     return cudaGetLastError();
