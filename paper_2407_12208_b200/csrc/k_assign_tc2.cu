@@ -82,6 +82,9 @@ constexpr int P_NON_EPI = 4;
 #ifndef MPK_PAIR_RBH
 #define MPK_PAIR_RBH 1                   // ASSIGN, 256-column tiles: warpgroups alternate row-blocks, half-tiles
 #endif
+#ifndef MPK_PAIR_RBH_PARTS
+#define MPK_PAIR_RBH_PARTS 2             // rbh: accumulators (parts of a 256-column tile) per warpgroup
+#endif
 #ifndef MPK_PAIR_HOT_WAIT
 #define MPK_PAIR_HOT_WAIT 1              // epilogue: test_wait before a bare try_wait loop
 #endif
@@ -102,6 +105,8 @@ constexpr int W_CRES = MPK_PAIR_ROLES_HIGH ? P_EPI + 2 : 2;   // resident C~, ac
 constexpr int W_MMA = MPK_PAIR_ROLES_HIGH ? P_EPI + 3 : 1;    // MMA issuer, TMEM allocation
 constexpr int P_MAX_ACC = 8;
 constexpr int P_MAX_RBR = 4;             // row-blocks per accumulator (one-tile row-block groups)
+constexpr int kRbhParts = MPK_PAIR_RBH_PARTS;   // rbh: parts (accumulators) per tile and warpgroup
+static_assert(kRbhParts == 2 || kRbhParts == 4, "rbh parts");
 constexpr size_t P_BUDGET = 227 * 1024;
 constexpr uint32_t TRACE_T = 256;        // tiles traced under MPK_PAIR_TRACE
 // named barriers (0 is __syncthreads)
@@ -227,7 +232,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
     // tile) 74.5 -> 79 us are slower than the half split / row-block alternation, so fp16 / bf16
     // with several tiles per row-block only.
     const bool rbh = RBHK && MODE == PAIR_ASSIGN && MPK_PAIR_RBH && p.NB == 256 && p.NT >= 2 && !p.is_f8 &&
-                     P_EWG == 2 && p.tmem_cols >= 512 && p.box_rows == 64 &&
+                     P_EWG == 2 && p.tmem_cols >= 512 && p.box_rows == 128 / kRbhParts &&
                      !(p.dbg & (16 | 32 | 64));
     const bool rbalt = MODE == PAIR_ASSIGN && MPK_PAIR_RBALT && p.NT == 1 && P_EWG == 2 && !rbh &&
                        !(p.dbg & (16 | 32));
@@ -259,7 +264,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
         mbar_init(smem_u32(b_full), 1);
         mbar_init(smem_u32(&part_free[0]), 1);
         mbar_init(smem_u32(&part_free[1]), 1);
-        for (int i = 0; i < ((hsplit || rbh) ? 4 : p.nacc); ++i) {
+        for (int i = 0; i < (hsplit ? 4 : rbh ? 2 * kRbhParts : p.nacc); ++i) {
             mbar_init(smem_u32(&t_full[i]), 1);
             // one arrival per CTA (named barrier first), one per epilogue warp, or (half split)
             // one per warp of the owning warpgroup
@@ -301,8 +306,9 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
         const uint32_t a_lo0 = umma_desc_lo(smem_u32(a_base));
         const uint32_t a_tile16 = p.a_tile_bytes >> 4, b_half16 = p.b_half_bytes >> 4;
         const uint32_t kb_a16 = p.kb_a_bytes >> 4, kb_b16 = p.kb_b_bytes >> 4;
-        const uint32_t idesc128 = (p.idesc & ~(0x3Fu << 17)) | ((128u >> 3) << 17);
-        const uint32_t h16 = (64u * (uint32_t)p.SWZ) >> 4;   // 64 centroid rows
+        constexpr int PW = 256 / kRbhParts;                // columns per part
+        const uint32_t idescP = (p.idesc & ~(0x3Fu << 17)) | (((uint32_t)PW >> 3) << 17);
+        const uint32_t h16 = ((uint32_t)(PW / 2) * (uint32_t)p.SWZ) >> 4;   // a part's rows per CTA
         mbar_wait(smem_u32(b_full), 0);
         tc_fence_after();
         int slot = w % SA;
@@ -313,9 +319,9 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
             const uint32_t a_lo = a_lo0 + slot * a_tile16;
             for (int t = 0; t < NT; ++t) {
                 const int tb = NT - 1 - t;
-                for (int hh = 1; hh >= 0; --hh, ++qq) {
-                    const int acc = 2 * w + (int)(qq & 1u);
-                    mbar_wait_hot(smem_u32(&t_empty[acc]), ((qq >> 1) & 1u) ^ 1u);
+                for (int hh = kRbhParts - 1; hh >= 0; --hh, ++qq) {
+                    const int acc = kRbhParts * w + (int)(qq % kRbhParts);
+                    mbar_wait_hot(smem_u32(&t_empty[acc]), ((qq / kRbhParts) & 1u) ^ 1u);
                     tc_fence_after();
 #if MPK_PAIR_TRACE_RB
                     const bool trq = p.trace && blockIdx.x == 0 && w == 0 && qq < TRACE_T;
@@ -324,7 +330,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
 #if MPK_PAIR_TRACE_RB
                         if (trq) p.trace[qq * 8 + 0] = clock64();
 #endif
-                        const uint32_t d_tmem = tmem_base + (uint32_t)acc * 128u;
+                        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * PW);
                         const uint32_t b_lo = b_lo0 + tb * b_half16 + (uint32_t)hh * h16;
                         if (!(dbg & 2)) {
                             for (int kb = 0; kb < KB; ++kb)
@@ -332,8 +338,8 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                                     const uint64_t ad = desc_join(dhi, a_lo + kb * kb_a16 + ks * 2);
                                     const uint64_t bd = desc_join(dhi, b_lo + kb * kb_b16 + ks * 2);
                                     const uint32_t accum = (kb | ks) ? 1u : 0u;
-                                    if (f8) mma2_f8(d_tmem, ad, bd, idesc128, accum);
-                                    else mma2_f16(d_tmem, ad, bd, idesc128, accum);
+                                    if (f8) mma2_f8(d_tmem, ad, bd, idescP, accum);
+                                    else mma2_f16(d_tmem, ad, bd, idescP, accum);
                                 }
                         }
                         tc_commit_pair(smem_u32(&t_full[acc]));
@@ -362,7 +368,7 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 const uint32_t dst = smem_u32(b_base + (size_t)t * p.b_half_bytes);
                 for (int kb = 0; kb < p.KB; ++kb)
                     for (int u = 0; u < nbox; ++u) {
-                        const int row = rbh ? t * 256 + u * 128 + (int)rank * 64
+                        const int row = rbh ? t * 256 + u * (256 / kRbhParts) + (int)rank * (128 / kRbhParts)
                                             : t * p.NB + (int)rank * half + u * p.box_rows;
                         tma_load_2d_pair(dst + kb * p.kb_b_bytes + u * p.box_rows * p.SWZ, &tmap_c,
                                          kb * eps, row, fb);
@@ -929,20 +935,21 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 for (int m = 0; m < NCH / 2; ++m) s2[m] = pack2(-1.0f, -1.0f);
                 for (int t = 0; t < NT; ++t) {
                     const int tb = NT - 1 - t;
-                    for (int hh = 1; hh >= 0; --hh, ++qq) {
-                        const int acc = 2 * wg + (int)(qq & 1u);
+                    for (int hh = kRbhParts - 1; hh >= 0; --hh, ++qq) {
+                        const int acc = kRbhParts * wg + (int)(qq % kRbhParts);
 #if MPK_PAIR_TRACE_RB
                         const bool trq = trace && blockIdx.x == 0 && wg == 0 && (warp & 3) == 0 &&
                                          lane == 0 && qq < TRACE_T;
                         if (trq) trace[qq * 8 + 5] = clock64();
 #endif
-                        mbar_wait_hot(smem_u32(&t_full[acc]), (qq >> 1) & 1u);
+                        mbar_wait_hot(smem_u32(&t_full[acc]), (qq / kRbhParts) & 1u);
                         tc_fence_after();
 #if MPK_PAIR_TRACE_RB
                         if (trq) trace[qq * 8 + 2] = clock64();
 #endif
-                        const uint32_t col0 = tmem_base + lane_addr + (uint32_t)acc * 128u;
-                        const int jb = tb * 256 + hh * 128;        // centroid of accumulator column 0
+                        constexpr int PW = 256 / kRbhParts;
+                        const uint32_t col0 = tmem_base + lane_addr + (uint32_t)(acc * PW);
+                        const int jb = tb * 256 + hh * PW;         // centroid of accumulator column 0
                         auto release = [&]() {
                             tc_fence_before();
                             __syncwarp();
@@ -953,10 +960,23 @@ assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                         };
                         auto fold_half = [&](auto guard_tag) {
                             constexpr bool GD = decltype(guard_tag)::value;
-                            // chunks 3 .. 0; the next chunk's TMEM load in flight while this one
-                            // folds; released once the last load has landed
                             uint32_t va[32], vb[32];
                             ChunkCn<4, GD> cq;
+                            if (kRbhParts == 4) {
+                                // chunks 1, 0; released once the second load has landed
+                                tmem_ld32(col0 + 32, va);
+                                tmem_wait_ld_dep(va);
+                                tmem_ld32(col0, vb);
+                                load_chunk_cn<4, GD>(cn_s, sc_s, jb + 32, cq);
+                                fold_rev_m3<4, GD>(va, cq, m2, cv, s2);
+                                tmem_wait_ld_dep(vb);
+                                release();
+                                load_chunk_cn<4, GD>(cn_s, sc_s, jb, cq);
+                                fold_rev_m3<4, GD>(vb, cq, m2, cv, s2);
+                                return;
+                            }
+                            // chunks 3 .. 0; the next chunk's TMEM load in flight while this one
+                            // folds; released once the last load has landed
                             tmem_ld32(col0 + 96, va);
                             tmem_wait_ld_dep(va);
                             tmem_ld32(col0 + 64, vb);
@@ -1431,7 +1451,7 @@ bool pair_plan(int dist, int d, int d_pad, int k, PairParams* pp, size_t* smem_b
     if (const char* e = getenv("MPK_PAIR_DBG")) p.dbg = atoi(e);
     // 64-row boxes for 256-column tiles (the rbh layout loads each CTA's half-tile as two
     // boxes from different centroid ranges; the standard layout as two consecutive ones)
-    p.box_rows = NB == 256 ? 64 : NB / 2;
+    p.box_rows = NB == 256 ? 128 / kRbhParts : NB / 2;
 
     p.u_low = dist == KMEANS_FP16 ? 0x1p-11 : (dist == KMEANS_BF16 ? 0x1p-8 : 0x1p-3);
     p.eta_low = dist == KMEANS_FP16 ? 0x1p-25 : (dist == KMEANS_BF16 ? 0x1p-134 : 0x1p-17);
