@@ -127,6 +127,11 @@ MPK_DEV double guard_scale(double amax, int guard) {
 // ------------------------------------------------------------------------------------------
 // Reductions.
 // ------------------------------------------------------------------------------------------
+// Programmatic dependent launch: a kernel launched with launch_pdl may start while its
+// predecessor in the stream drains; it waits here (first statement) for that predecessor's
+// completion and memory. A no-op for an ordinary launch.
+MPK_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 template <typename T> MPK_DEV T warp_sum(T v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -1,5 +1,7 @@
 // internal.h — handle state and kernel launchers (C++; never crosses the C ABI).
 #pragma once
+#include <cstdlib>
+#include <utility>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -12,6 +14,25 @@ namespace mpk {
 // Number of kernels this library launched (process-wide); reported per fit in kmeans_stats.
 long long launches_read();
 void launches_add(int n);
+// Launch with programmatic stream serialization (PDL): the kernel's launch overlaps the tail of
+// the previous kernel in the stream; the kernel must call griddep_wait() before touching data the
+// previous kernels wrote (every kernel launched this way does so first). MPK_NO_PDL: plain launch.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+    static const bool off = getenv("MPK_NO_PDL") != nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    a[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = a;
+    cfg.numAttrs = off ? 0 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // Packed per-iteration accumulator (fp64): [sums k*d][counts k][sse][changed][nonfinite][pad]
 // One ncclAllReduce over this buffer is the only per-iteration cross-GPU exchange.

@@ -62,6 +62,7 @@ __global__ void count_kernel(const int32_t* __restrict__ labels, int64_t n, int 
 __global__ void scan_kernel(const int* __restrict__ cnt, int k, int64_t P, int* __restrict__ offs,
                             int* __restrict__ cursor, int* __restrict__ mpo,
                             double* __restrict__ acc_counts, const int* gate = nullptr) {
+    griddep_wait();
     if (gated_off(gate)) return;
     __shared__ int sh[1024], sh2[1024];
     __shared__ int carry, carry2;
@@ -108,6 +109,7 @@ constexpr int kDetRows = 8192;                    // rows per counting / scatter
 __global__ void __launch_bounds__(kDetThreads)
 block_count_kernel(const int32_t* __restrict__ labels, int64_t n, int k, int* __restrict__ CB,
                    const int* gate = nullptr) {
+    griddep_wait();
     if (gated_off(gate)) return;
     extern __shared__ int hist[];
     for (int j = threadIdx.x; j < k; j += blockDim.x) hist[j] = 0;
@@ -129,6 +131,7 @@ block_count_kernel(const int32_t* __restrict__ labels, int64_t n, int k, int* __
 __global__ void __launch_bounds__(1024)
 block_scan_kernel(int* __restrict__ CB, int64_t nb, int k, int* __restrict__ cnt,
                   const int* gate = nullptr) {
+    griddep_wait();
     if (gated_off(gate)) return;
     __shared__ int tot[32][33];
     const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
@@ -194,6 +197,7 @@ __global__ void __launch_bounds__(kDetThreads)
 scatter_det_kernel(const int32_t* __restrict__ labels, int64_t n, int k,
                    const int* __restrict__ offs, const int* __restrict__ CB,
                    int* __restrict__ perm, const int* gate = nullptr) {
+    griddep_wait();
     if (gated_off(gate)) return;
     const int kbits = 32 - __clz(k);              // keys l + 1 in [0, k]
     extern __shared__ int smem_i[];
@@ -673,6 +677,7 @@ fx_incr_kernel(const float* __restrict__ X, int64_t n, int d, const int3* __rest
                const int* __restrict__ seg_cnt, const int* __restrict__ gate,
                const float2* __restrict__ sc, long long* __restrict__ Shi,
                long long* __restrict__ Slo, int* __restrict__ cnt) {
+    griddep_wait();
     if (gate[0] > gate[1]) return;                        // the full path ran
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -708,6 +713,7 @@ segsum_fx_kernel(const float* __restrict__ X, int64_t n, int d, int k, const int
                  const int* __restrict__ offs, const int* __restrict__ mpo, int64_t P, int64_t C,
                  const float2* __restrict__ sc, long long* __restrict__ Shi,
                  long long* __restrict__ Slo, long long* __restrict__ part, const int* gate) {
+    griddep_wait();
     if (gated_off(gate)) return;
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -791,6 +797,7 @@ __global__ void __launch_bounds__(256)
 segsum_fix_fx_kernel(int d, const int* __restrict__ offs, const int* __restrict__ mpo,
                      const long long* __restrict__ part, long long* __restrict__ Shi,
                      long long* __restrict__ Slo, const int* gate) {
+    griddep_wait();
     if (gated_off(gate)) return;
     const int j = blockIdx.x;
     const int np = mpo[j + 1] - mpo[j];
@@ -858,6 +865,7 @@ __global__ void finalize_fx_kernel(int64_t k, int d, const long long* __restrict
                                    const long long* __restrict__ Slo, const int* __restrict__ cnt,
                                    const double* __restrict__ isc, const double* __restrict__ acc,
                                    AccLayout L, float* __restrict__ C, IterRec* __restrict__ rec) {
+    griddep_wait();
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -975,32 +983,38 @@ cudaError_t launch_update_fx(const float* Xw, int64_t n, int d, int k, const int
     const int* gate = fx.gate;
     // full re-summation, gated: runs only when the list overflowed
     const int64_t nb = (n + kDetRows - 1) / kDetRows;
-    block_count_kernel<<<(unsigned)nb, kDetThreads, sizeof(int) * k, s>>>(labels, n, k, us.cb, gate);
-    block_scan_kernel<<<(unsigned)((k + 31) / 32), 1024, 0, s>>>(us.cb, nb, k, cnt, gate);
+    // the chain below is launched with programmatic dependent launch (each kernel waits for its
+    // predecessor first): the launch latency of the gated-off kernels overlaps
+    launch_pdl(block_count_kernel, dim3((unsigned)nb), dim3(kDetThreads), sizeof(int) * k, s,
+               labels, n, k, us.cb, gate);
+    launch_pdl(block_scan_kernel, dim3((unsigned)((k + 31) / 32)), dim3(1024), 0, s, us.cb, nb, k,
+               cnt, gate);
     const int64_t P = kPiece;
-    scan_kernel<<<1, 1024, 0, s>>>(cnt, k, P, offs, cursor, us.mpo, nullptr, gate);
+    launch_pdl(scan_kernel, dim3(1), dim3(1024), 0, s, (const int*)cnt, k, P, offs, cursor, us.mpo,
+               (double*)nullptr, gate);
     static PerDeviceOnce attr;
     if (attr.need()) {
         cudaFuncSetAttribute(scatter_det_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kDetHistBytes + kDetRows * (int)sizeof(int));
         attr.done();
     }
-    scatter_det_kernel<<<(unsigned)nb, 32 * scatter_warps(k), scatter_smem(k), s>>>(
-        labels, n, k, offs, us.cb, perm, gate);
+    launch_pdl(scatter_det_kernel, dim3((unsigned)nb), dim3(32 * scatter_warps(k)), scatter_smem(k),
+               s, labels, n, k, (const int*)offs, (const int*)us.cb, perm, gate);
     const int VEC = d <= 32 ? 1 : (d <= 64 ? 2 : 4);
     const int colblk = 32 * VEC;
     const int64_t C = segsum_chunk(n);
     const int64_t nw = (n + C - 1) / C;
     dim3 grid((unsigned)((nw + 7) / 8), (unsigned)((d + colblk - 1) / colblk), 1);
-#define SEGSUMFX(V) segsum_fx_kernel<V, 8><<<grid, 256, 0, s>>>(Xw, n, d, k, perm, offs, us.mpo, P, C, \
-                                                                fx.sc, fx.Shi, fx.Slo, fx.part, gate)
+#define SEGSUMFX(V) launch_pdl(segsum_fx_kernel<V, 8>, grid, dim3(256), 0, s, Xw, n, d, k, (const int*)perm, \
+                                (const int*)offs, (const int*)us.mpo, P, C, (const float2*)fx.sc, fx.Shi, \
+                                fx.Slo, fx.part, gate)
     if (VEC == 1) SEGSUMFX(1); else if (VEC == 2) SEGSUMFX(2); else SEGSUMFX(4);
 #undef SEGSUMFX
-    segsum_fix_fx_kernel<<<dim3((unsigned)k, (unsigned)((d + 31) / 32)), 256, 0, s>>>(
-        d, offs, us.mpo, fx.part, fx.Shi, fx.Slo, gate);
+    launch_pdl(segsum_fix_fx_kernel, dim3((unsigned)k, (unsigned)((d + 31) / 32)), dim3(256), 0, s,
+               d, (const int*)offs, (const int*)us.mpo, (const long long*)fx.part, fx.Shi, fx.Slo, gate);
     // incremental update, gated the other way
-    fx_incr_kernel<<<kNumSMs * 4, 256, 0, s>>>(Xw, n, d, fx.list, fx.seg_cnt, gate, fx.sc, fx.Shi,
-                                               fx.Slo, cnt);
+    launch_pdl(fx_incr_kernel, dim3(kNumSMs * 4), dim3(256), 0, s, Xw, n, d, (const int3*)fx.list,
+               (const int*)fx.seg_cnt, gate, (const float2*)fx.sc, fx.Shi, fx.Slo, cnt);
     return cudaGetLastError();
 }
 
@@ -1010,7 +1024,8 @@ cudaError_t launch_finalize_fx(int64_t k, int d, const FxState& fx, const long l
     launches_add(1);
     int g = (int)std::min<int64_t>((k + 7) / 8, kNumSMs * 2);
     if (g < 1) g = 1;
-    finalize_fx_kernel<<<g, 256, 0, s>>>(k, d, Shi, Slo, cnt, fx.isc, acc, L, Cw, rec);
+    launch_pdl(finalize_fx_kernel, dim3(g), dim3(256), 0, s, k, d, Shi, Slo, cnt,
+               (const double*)fx.isc, acc, L, Cw, rec);
     return cudaGetLastError();
 }
 
