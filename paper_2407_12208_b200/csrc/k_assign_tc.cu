@@ -574,8 +574,8 @@ cudaError_t launch_assign_tc(TcPlan* pl, const Problem& pb, const float* xn, con
         q.n = pb.n; q.guard = pb.guard; q.xn = xn; q.sx = sx; q.cn = cn; q.sc = sc;
         q.labels = labels; q.acc_sse = acc_sse; q.acc_changed = acc_changed;
         if (fx && !getenv("MPK_NO_FX_LIST")) {
-            cudaError_t e = cudaMemsetAsync(fx->gate, 0, sizeof(int), s);   // gate[0]: count
-            if (e != cudaSuccess) return e;
+            // gate[0] (the count) is zero here: zeroed before the first iteration, then by
+            // finalize_fx after each update
             q.fx_list = fx->list; q.fx_seg_cnt = fx->seg_cnt; q.fx_gate = fx->gate;
             if (fx_listed) *fx_listed = true;
         }

@@ -172,6 +172,7 @@ template <int MODE, bool RBHK = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 assign_pair_kernel(const __grid_constant__ CUtensorMap tmap_x,
                    const __grid_constant__ CUtensorMap tmap_c, PairParams p) {
+    griddep_wait();                                   // launched with programmatic dependent launch
     constexpr bool FINAL = MODE == PAIR_FINAL;
     constexpr bool CAND = MODE == PAIR_CAND;
     // ASSIGN and FINAL: reverse column scan with 3-input minima (tc_common.cuh fold_rev_*)
@@ -1510,15 +1511,13 @@ cudaError_t pair_launch(const CUtensorMap& tmap_x, const CUtensorMap& tmap_c, co
         }
         return cudaGetLastError();
     }
-    if (mode == PAIR_FINAL)
-        assign_pair_kernel<PAIR_FINAL><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, p);
-    else if (mode == PAIR_CAND)
-        assign_pair_kernel<PAIR_CAND><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, p);
-    else if (pair_uses_rbh(p))
-        assign_pair_kernel<PAIR_ASSIGN, true><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, p);
-    else
-        assign_pair_kernel<PAIR_ASSIGN><<<(unsigned)grid, P_THREADS, smem_bytes, s>>>(tmap_x, tmap_c, p);
-    return cudaGetLastError();
+    // programmatic dependent launch (the kernel waits for its predecessor first): the launch of
+    // this cluster kernel overlaps the previous kernel's tail
+    auto kern = mode == PAIR_FINAL ? assign_pair_kernel<PAIR_FINAL>
+              : mode == PAIR_CAND ? assign_pair_kernel<PAIR_CAND>
+              : pair_uses_rbh(p) ? assign_pair_kernel<PAIR_ASSIGN, true>
+                                 : assign_pair_kernel<PAIR_ASSIGN>;
+    return launch_pdl(kern, dim3((unsigned)grid), dim3(P_THREADS), smem_bytes, s, tmap_x, tmap_c, p);
 }
 
 }  // namespace tcdev

@@ -446,6 +446,7 @@ __global__ void prep_kernel(const W* __restrict__ X, int64_t rows, int d, int d_
                             W* __restrict__ norms, W* __restrict__ scales,
                             typename low_type<DIST>::T* __restrict__ Xl,
                             unsigned long long* __restrict__ census) {
+    griddep_wait();                                   // launched with launch_pdl
     using L = typename low_type<DIST>::T;
     constexpr int WORK = sizeof(W) == 8 ? KMEANS_FP64 : KMEANS_FP32;
     constexpr bool same = (DIST == WORK);
@@ -954,23 +955,23 @@ static cudaError_t prep_dispatch(int dist, const W* X, int64_t rows, int d, int 
     int g = grid_for(rows * 32, 256, 16);
     switch (dist) {
         case KMEANS_FP64:
-            prep_kernel<W, KMEANS_FP64><<<g, 256, 0, s>>>(X, rows, d, d_pad, guard, norms, scales,
+            launch_pdl(prep_kernel<W, KMEANS_FP64>, dim3(g), dim3(256), 0, s, X, rows, d, d_pad, guard, norms, scales,
                                                          (double*)Xl, census);
             break;
         case KMEANS_FP32:
-            prep_kernel<W, KMEANS_FP32><<<g, 256, 0, s>>>(X, rows, d, d_pad, guard, norms, scales,
+            launch_pdl(prep_kernel<W, KMEANS_FP32>, dim3(g), dim3(256), 0, s, X, rows, d, d_pad, guard, norms, scales,
                                                          (float*)Xl, census);
             break;
         case KMEANS_FP16:
-            prep_kernel<W, KMEANS_FP16><<<g, 256, 0, s>>>(X, rows, d, d_pad, guard, norms, scales,
+            launch_pdl(prep_kernel<W, KMEANS_FP16>, dim3(g), dim3(256), 0, s, X, rows, d, d_pad, guard, norms, scales,
                                                          (__half*)Xl, census);
             break;
         case KMEANS_BF16:
-            prep_kernel<W, KMEANS_BF16><<<g, 256, 0, s>>>(X, rows, d, d_pad, guard, norms, scales,
+            launch_pdl(prep_kernel<W, KMEANS_BF16>, dim3(g), dim3(256), 0, s, X, rows, d, d_pad, guard, norms, scales,
                                                          (__nv_bfloat16*)Xl, census);
             break;
         case KMEANS_E5M2:
-            prep_kernel<W, KMEANS_E5M2><<<g, 256, 0, s>>>(X, rows, d, d_pad, guard, norms, scales,
+            launch_pdl(prep_kernel<W, KMEANS_E5M2>, dim3(g), dim3(256), 0, s, X, rows, d, d_pad, guard, norms, scales,
                                                          (e5m2_t*)Xl, census);
             break;
         default:

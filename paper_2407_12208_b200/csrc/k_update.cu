@@ -863,8 +863,9 @@ MPK_DEV float fx_quot_rn(long long H, long long L, int x, int m) {
 // Thm 5.3 terms, trace record).
 __global__ void finalize_fx_kernel(int64_t k, int d, const long long* __restrict__ Shi,
                                    const long long* __restrict__ Slo, const int* __restrict__ cnt,
-                                   const double* __restrict__ isc, const double* __restrict__ acc,
-                                   AccLayout L, float* __restrict__ C, IterRec* __restrict__ rec) {
+                                   const double* __restrict__ isc, double* __restrict__ acc,
+                                   AccLayout L, float* __restrict__ C, IterRec* __restrict__ rec,
+                                   int* __restrict__ gate0) {
     griddep_wait();
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -905,6 +906,11 @@ __global__ void finalize_fx_kernel(int64_t k, int d, const long long* __restrict
         if (blockIdx.x == 0) {
             rec->sse = acc[L.sse()];
             rec->changed = acc[L.changed()];
+            // zeroed here for the next iteration's distance kernel (instead of memsets between
+            // the iteration's kernels, which would break their programmatic dependent launches)
+            acc[L.sse()] = 0.0;
+            acc[L.changed()] = 0.0;
+            if (gate0) *gate0 = 0;
         }
     }
 }
@@ -1025,7 +1031,7 @@ cudaError_t launch_finalize_fx(int64_t k, int d, const FxState& fx, const long l
     int g = (int)std::min<int64_t>((k + 7) / 8, kNumSMs * 2);
     if (g < 1) g = 1;
     launch_pdl(finalize_fx_kernel, dim3(g), dim3(256), 0, s, k, d, Shi, Slo, cnt,
-               (const double*)fx.isc, acc, L, Cw, rec);
+               (const double*)fx.isc, const_cast<double*>(acc), L, Cw, rec, fx.gate);
     return cudaGetLastError();
 }
 

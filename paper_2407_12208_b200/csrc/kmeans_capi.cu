@@ -924,7 +924,12 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
         if (rec == rec_scratch) CK(cudaMemsetAsync(rec_scratch, 0, sizeof(IterRec), s));
         cudaEvent_t t0 = nullptr, t1 = nullptr, t2 = nullptr, t3 = nullptr, t4 = nullptr;
         if (timing) { t0 = evp.get(); t1 = evp.get(); t2 = evp.get(); t3 = evp.get(); t4 = evp.get(); }
-        CK(cudaMemsetAsync(h->acc, 0, sizeof(double) * h->L.total(), s));
+        // with the fixed-point update finalize_fx zeroes SSE_t, the changed count and the
+        // list counter for the next iteration (zeroed here before the first)
+        if (!fx_on || it == 1) {
+            CK(cudaMemsetAsync(h->acc, 0, sizeof(double) * h->L.total(), s));
+            if (fx_on) CK(cudaMemsetAsync(h->fx.gate, 0, sizeof(int), s));
+        }
         if (int rc = prep_centroids(h)) return rc;                         // A3
         if (timing) CK(cudaEventRecord(t0, s));
         if (h->dist_kernel == DK_SMALLD && h->delta <= 0.0) {              // A4 + A5 fused
