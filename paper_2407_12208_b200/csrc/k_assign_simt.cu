@@ -449,6 +449,72 @@ assign_simt_big_kernel(Problem p, const LT* __restrict__ Xl, const W* __restrict
 }
 
 // ------------------------------------------------------------------------------------------
+// K6b for d <= 4 (the image rows; the final pass of the small-d loop): one
+// row per thread, the centres in shared memory. K6b's 128 x 128 tile left almost every lane
+// idle at d = 3, k = 6. Same arithmetic per value as K6b: dot = fma over t = 0..d-1 from 0
+// (K6b's zero-padded columns add exact zeros), v = fma(-2 (s_i s_j), dot, ||c_j||^2), and the
+// ascending-j scan with strict < gives K6b's (value, index) minimum, lowest index on ties.
+// ------------------------------------------------------------------------------------------
+constexpr int kSmallK = 256;
+
+template <typename LT, typename W, int D>
+__global__ void __launch_bounds__(256)
+assign_simt_small_kernel(Problem p, const LT* __restrict__ Xl, const W* __restrict__ xn,
+                         const W* __restrict__ sx, const LT* __restrict__ Cl,
+                         const W* __restrict__ cn, const W* __restrict__ sc,
+                         int32_t* __restrict__ labels, double* acc_sse, double* acc_changed,
+                         const int* __restrict__ rows) {
+    __shared__ float Cs[kSmallK][D];
+    __shared__ W cns[kSmallK], scs[kSmallK];
+    for (int j = threadIdx.x; j < p.k; j += blockDim.x) {
+#pragma unroll
+        for (int t = 0; t < D; ++t) Cs[j][t] = (float)widen(Cl[(int64_t)j * p.d_pad + t]);
+        cns[j] = cn[j];
+        scs[j] = (p.guard && sc) ? sc[j] : (W)1;
+    }
+    __syncthreads();
+    double my_sse = 0.0, my_changed = 0.0;
+    for (int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; li < p.n;
+         li += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = rows ? (int64_t)rows[li] : li;
+        float x[D];
+#pragma unroll
+        for (int t = 0; t < D; ++t) x[t] = (float)widen(Xl[row * p.d_pad + t]);
+        const W srow = (p.guard && sx) ? sx[row] : (W)1;
+        float bestv = INFINITY;
+        int bestj = 0;
+        for (int j = 0; j < p.k; ++j) {
+            float dot = 0.0f;
+#pragma unroll
+            for (int t = 0; t < D; ++t) dot = fmaf(x[t], Cs[j][t], dot);
+            const W m2 = (W)-2 * (srow * scs[j]);
+            const float v = (float)fma(m2, (W)dot, cns[j]);
+            if (v < bestv) { bestv = v; bestj = j; }
+        }
+        if (acc_changed && labels[row] != bestj) my_changed += 1.0;
+        labels[row] = bestj;
+        if (acc_sse) {
+            const double md = (double)xn[row] + (double)bestv;
+            my_sse += md > 0.0 ? md : 0.0;
+        }
+    }
+    if (acc_sse || acc_changed) {
+        my_sse = warp_sum(my_sse);
+        my_changed = warp_sum(my_changed);
+        __shared__ double red[2][8];
+        const int tid = threadIdx.x;
+        if ((tid & 31) == 0) { red[0][tid >> 5] = my_sse; red[1][tid >> 5] = my_changed; }
+        __syncthreads();
+        if (tid == 0) {
+            double a = 0, b = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += red[0][w]; b += red[1][w]; }
+            if (acc_sse) atomicAdd(acc_sse, a);
+            if (acc_changed && b != 0.0) atomicAdd(acc_changed, b);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
 // K6m-b: Alg 4's per-pair precision switch for fp32 work on K6b's 128 x 128 tiles (8 x 8 per
 // thread). Per centroid tile, the rows' and columns' norm ranges classify the tile in fp64
 // (monotone, so the classification agrees with every per-pair decision):
@@ -916,6 +982,42 @@ __global__ void final_sse_fast_kernel(const float* __restrict__ X, int64_t n, in
     }
 }
 
+// fp32, d <= 4: a row per thread. Per row the exact products (df^2 = p2 + e2) are summed over
+// the D columns with the same compensated fp32 TwoSum as final_sse_fast_kernel (which runs it
+// over 4 rows of one column), then added in fp64: the same accuracy class, without 29 of 32
+// lanes idle at d = 3.
+template <int D>
+__global__ void __launch_bounds__(256)
+final_sse_small_kernel(const float* __restrict__ X, int64_t n, const float* __restrict__ C,
+                       const int32_t* __restrict__ labels, double* __restrict__ out) {
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int lab = labels[i];
+        float s = 0.0f, comp = 0.0f;
+#pragma unroll
+        for (int t = 0; t < D; ++t) {
+            const float df = X[i * D + t] - C[(int64_t)lab * D + t];
+            const float p2 = df * df;
+            const float e2 = fmaf(df, df, -p2);
+            const float u = s + p2;
+            const float z = u - s;
+            comp += (s - (u - z)) + (p2 - z) + e2;
+            s = u;
+        }
+        acc += (double)s + (double)comp;
+    }
+    acc = warp_sum(acc);
+    __shared__ double red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += red[w];
+        atomicAdd(out, a);
+    }
+}
+
 // fp32 rows of 128 / 256 columns (V float4 groups per lane): one 16-byte load of x and of its
 // centre per row and group, RW rows in flight per warp; per column the same exact-product TwoSum
 // over the RW rows as final_sse_fast_kernel, then fp64.
@@ -988,6 +1090,23 @@ cudaError_t simt_dispatch_acc(int dist, const Problem& p, const void* Xl, const 
                               cudaStream_t s, const int* rows) {
     if (p.n <= 0) return cudaSuccess;
     if constexpr (!std::is_same<LT, double>::value && std::is_same<W, float>::value) {
+        if (p.d <= 4 && p.k <= kSmallK && !getenv("MPK_SIMT_NO_SMALL")) {
+            // d <= 4: a row per thread (MPK_SIMT_NO_SMALL=1: K6b, for A/B and tests)
+            int64_t want = (p.n + 255) / 256;
+            const int g = (int)(want < 1 ? 1 : (want > kNumSMs * 8 ? kNumSMs * 8 : want));
+#define SIMT_SMALL(DV)                                                                             \
+            assign_simt_small_kernel<LT, W, DV><<<g, 256, 0, s>>>(                                 \
+                p, (const LT*)Xl, (const W*)xn, (const W*)sx, (const LT*)Cl, (const W*)cn,         \
+                (const W*)sc, labels, acc_sse, acc_changed, rows);
+            switch (p.d) {
+                case 1: SIMT_SMALL(1) break;
+                case 2: SIMT_SMALL(2) break;
+                case 3: SIMT_SMALL(3) break;
+                default: SIMT_SMALL(4) break;
+            }
+#undef SIMT_SMALL
+            return cudaGetLastError();
+        }
         // fp32 accumulation with fp32 working precision: the 8 x 8 register-tiled kernel
         const int64_t b2 = (p.n + B2M - 1) / B2M;
         assign_simt_big_kernel<LT, W><<<(unsigned)b2, B2T, 0, s>>>(
@@ -1091,7 +1210,16 @@ cudaError_t launch_final_sse(int work, const void* Xw, int64_t n, int d, const v
     if (work == KMEANS_FP64)
         final_sse_kernel<double><<<grid, 256, 0, s>>>((const double*)Xw, n, d, (const double*)Cw,
                                                      labels, sse_out);
-    else if (vec_ok && d == 128)
+    else if (d <= 4 && !getenv("MPK_SIMT_NO_SMALL")) {
+        const int64_t wr = (n + 255) / 256;
+        const int gs = (int)(wr < 1 ? 1 : (wr > kNumSMs * 8 ? kNumSMs * 8 : wr));
+        switch (d) {
+            case 1: final_sse_small_kernel<1><<<gs, 256, 0, s>>>((const float*)Xw, n, (const float*)Cw, labels, sse_out); break;
+            case 2: final_sse_small_kernel<2><<<gs, 256, 0, s>>>((const float*)Xw, n, (const float*)Cw, labels, sse_out); break;
+            case 3: final_sse_small_kernel<3><<<gs, 256, 0, s>>>((const float*)Xw, n, (const float*)Cw, labels, sse_out); break;
+            default: final_sse_small_kernel<4><<<gs, 256, 0, s>>>((const float*)Xw, n, (const float*)Cw, labels, sse_out); break;
+        }
+    } else if (vec_ok && d == 128)
         final_sse_vec_kernel<1><<<grid, 256, 0, s>>>((const float*)Xw, n, d, (const float*)Cw, labels, sse_out);
     else if (vec_ok)
         final_sse_vec_kernel<2><<<grid, 256, 0, s>>>((const float*)Xw, n, d, (const float*)Cw, labels, sse_out);

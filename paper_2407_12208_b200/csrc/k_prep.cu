@@ -743,6 +743,86 @@ prep_fast_kernel(const float* __restrict__ Xin, int64_t rows, int d, int d_pad, 
     }
 }
 
+// prep_fast_kernel for d <= 4 (the small-d path: images): one row per thread instead of one per
+// warp (a warp per row left 29 of 32 lanes idle at d = 3). The same arithmetic per element as
+// prep_row_fast, and ||x||^2 combined in the order prep_row_fast's warp sum gives when column c
+// sits in lane c: ((x0^2 + x2^2) + (x1^2 + x3^2)), each square exact in fp64.
+template <int DIST, bool NORM, int D>
+__global__ void __launch_bounds__(256)
+prep_small_kernel(const float* __restrict__ Xin, int64_t rows, int d_pad, int guard,
+                  float* __restrict__ norms, float* __restrict__ scales,
+                  typename low_type<DIST>::T* __restrict__ Xl,
+                  unsigned long long* __restrict__ census, float* __restrict__ Xout,
+                  const double* __restrict__ shift, const double* __restrict__ scale) {
+    using L = typename low_type<DIST>::T;
+    constexpr bool same = DIST == KMEANS_FP32;
+    double sh[D], sc[D], rc[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+        sh[c] = NORM ? shift[c] : 0.0;
+        sc[c] = NORM ? scale[c] : 1.0;
+        rc[c] = 1.0 / sc[c];
+    }
+    unsigned n_nonfinite = 0, n_under = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += stride) {
+        float v[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) v[c] = Xin[i * D + c];
+        if (NORM) {
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                v[c] = __double2float_rn(div_rn((double)v[c] - sh[c], sc[c], rc[c]));
+                Xout[i * D + c] = v[c];
+            }
+        }
+        double sq[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            // prep_row_fast's per-lane TwoSum over one column: (double)p + (double)e = v^2 exactly
+            const float p = v[c] * v[c];
+            const float e = fmaf(v[c], v[c], -p);
+            const float t = 0.0f + p;
+            const float z = t - 0.0f;
+            const float cs = 0.0f + ((0.0f - (t - z)) + (p - z) + e);
+            sq[c] = (double)t + (double)cs;
+        }
+        const double acc = (sq[0] + sq[2]) + (sq[1] + sq[3]);
+        float s = 1.0f;
+        if (guard && !same) {
+            float amax = 0.0f;
+#pragma unroll
+            for (int c = 0; c < D; ++c) amax = fmaxf(amax, fabsf(v[c]));
+            s = guard_scale(amax, guard);
+        }
+        norms[i] = __double2float_rn(acc);
+        if (scales) scales[i] = s;
+        for (int c = 0; c < d_pad; ++c) {
+            L o;
+            if (c < D) {
+                const float vc = c == 0 ? v[0] : c == 1 ? v[D > 1 ? 1 : 0] : c == 2 ? v[D > 2 ? 2 : 0] : v[D > 3 ? 3 : 0];
+                const float qv = (s == 1.0f) ? vc : vc / s;     // precision-u division (IEEE, RN)
+                o = rounder<DIST>::from(qv);
+                if (!same) {
+                    if (is_nonfinite_low(o)) n_nonfinite++;
+                    else if (qv != 0.0f && is_zero_or_subnormal_low(o)) n_under++;
+                }
+            } else {
+                o = rounder<DIST>::from(0.0f);
+            }
+            Xl[i * d_pad + c] = o;
+        }
+    }
+    if (census) {
+        const unsigned long long a = warp_sum((unsigned long long)n_nonfinite);
+        const unsigned long long b = warp_sum((unsigned long long)n_under);
+        if ((threadIdx.x & 31) == 0 && (a | b)) {
+            atomicAdd(&census[0], a);
+            atomicAdd(&census[1], b);
+        }
+    }
+}
+
 // Vectorised form of prep_fast_kernel for rows whose width is a multiple of 128 (d = d_pad,
 // d <= 256): a lane owns V float4 column groups (columns 128 w + 4 lane + e), so each row costs
 // one 16-byte load, one 16-byte store of the normalised row and one 4-element store of the
@@ -908,6 +988,23 @@ static void prep_fast_launch(const float* Xin, int64_t rows, int d, int d_pad, i
                              float* Xout, const double* shift, const double* scale,
                              cudaStream_t s, unsigned* amax, int* flags, bool* amax_done) {
     using L = typename low_type<DIST>::T;
+    if (d <= 4 && d_pad <= 8 && !getenv("MPK_PREP_NO_SMALL")) {
+        // one row per thread (small d); MPK_PREP_NO_SMALL=1: prep_fast_kernel (A/B, tests)
+        const int gs = grid_for(rows, 256, 8);
+#define PREP_SMALL(DV)                                                                              \
+        if (shift) prep_small_kernel<DIST, true, DV><<<gs, 256, 0, s>>>(Xin, rows, d_pad, guard, norms, \
+                                     scales, (L*)Xl, census, Xout, shift, scale);                   \
+        else prep_small_kernel<DIST, false, DV><<<gs, 256, 0, s>>>(Xin, rows, d_pad, guard, norms,     \
+                                     scales, (L*)Xl, census, Xout, shift, scale);
+        switch (d) {
+            case 1: PREP_SMALL(1) break;
+            case 2: PREP_SMALL(2) break;
+            case 3: PREP_SMALL(3) break;
+            default: PREP_SMALL(4) break;
+        }
+#undef PREP_SMALL
+        return;
+    }
     const int g = grid_for(rows * 8, 256, 8);
     const bool aligned = (((uintptr_t)Xin | (uintptr_t)Xout | (uintptr_t)Xl) & 15) == 0;
     if (d == d_pad && (d == 128 || d == 256) && aligned && !MPK_PREP_NO_VEC) {
