@@ -779,7 +779,11 @@ int prepare_points(kmeans_ctx* h, const void* X) {
 // chunk (launches after convergence return at once), with tol < 0 never.
 constexpr int kLoopChunk = 8;
 
-int run_smalld_loop(kmeans_ctx* h, int max_iter, double tol, int* it_out, bool* conv_out) {
+// *deferred (K5p): the loop state's device-to-host copy is enqueued but not waited for; the
+// caller reads h->loop_host[1] after its next stream synchronisation (the fit's outputs), so the
+// final pass is queued behind the loop without an idle GPU in between.
+int run_smalld_loop(kmeans_ctx* h, int max_iter, double tol, int* it_out, bool* conv_out,
+                    bool* deferred) {
     cudaStream_t s = h->stream;
     if (!h->loop) {
         CK(cudaMalloc(&h->loop, sizeof(LoopState)));
@@ -796,6 +800,11 @@ int run_smalld_loop(kmeans_ctx* h, int max_iter, double tol, int* it_out, bool* 
                                                     h->census + 2, max_iter, s);
         if (e == cudaSuccess) {
             CK(cudaMemcpyAsync(&h->loop_host[1], h->loop, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
+            if (deferred) {
+                *deferred = true;
+                *it_out = max_iter;           // upper bound until the copy has landed
+                return 0;
+            }
             CK(cudaStreamSynchronize(s));
             if (h->loop_host[1].fault)
                 return fail(h, KMEANS_ECUDA, "K5p: a block timed out at the grid barrier");
@@ -910,12 +919,13 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
     bool converged = false;
     IterRec rec_h{};
     IterRec* rec_scratch = h->trace + (KMEANS_MAX_TRACE - 1);
+    bool loop_deferred = false;
     const bool fused_loop = h->dist_kernel == DK_SMALLD && h->delta <= 0.0 && !h->comm &&
                             smalld_loop_supported(d, k) && !getenv("MPK_NO_FUSED_LOOP");
     if (fused_loop) {
         cudaEvent_t t0 = nullptr, t1 = nullptr;
         if (timing) { t0 = evp.get(); t1 = evp.get(); CK(cudaEventRecord(t0, s)); }
-        if (int rc = run_smalld_loop(h, max_iter, tol, &it, &converged)) return rc;
+        if (int rc = run_smalld_loop(h, max_iter, tol, &it, &converged, &loop_deferred)) return rc;
         // one fused kernel per iteration: its time is reported as the distance step's
         if (timing) { CK(cudaEventRecord(t1, s)); kev.insert(kev.end(), {t0, t1, t1, t1, t1}); }
     }
@@ -1018,6 +1028,14 @@ int fit_impl(kmeans_ctx* h, const void* X, const void* C0, int32_t max_iter, dou
                                    cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
+    if (loop_deferred) {
+        if (h->loop_host[1].fault)
+            return fail(h, KMEANS_ECUDA, "K5p: a block timed out at the grid barrier");
+        it = h->loop_host[1].iter;
+        converged = h->loop_host[1].converged != 0;
+        tl = std::min(it, KMEANS_MAX_TRACE - 1);
+        tr.resize(tl);
+    }
 
     kmeans_stats& st = h->stats;
     memset(&st, 0, sizeof(st));
