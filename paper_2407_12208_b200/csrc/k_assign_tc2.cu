@@ -1438,6 +1438,10 @@ bool pair_plan(int dist, int d, int d_pad, int k, PairParams* pp, size_t* smem_b
         p.rbr = 256 / NB;
         if (const char* e = getenv("MPK_PAIR_RBR")) p.rbr = atoi(e);
         p.rbr = std::max(1, std::min(std::min(P_MAX_RBR, 256 / NB), p.rbr));
+        // a group's R row-blocks hold R X~ slots until its accumulator is committed: with
+        // fewer slots (rows of 512 bytes leave room for 3) the issuer waited for a slot no one
+        // could free
+        while (p.rbr > SA) p.rbr >>= 1;
     }
     const int AW = p.rbr * NB;
     p.nacc = std::min(acc_cap, 512 / AW);

@@ -550,6 +550,9 @@ fx_colmax_vec_kernel(const float* __restrict__ X, int64_t n, int d, unsigned* __
                      int* __restrict__ flags) {
     const int cg = d >> 2, lanes = 256 / cg;
     const int g = threadIdx.x % cg, lane = threadIdx.x / cg;
+    __shared__ unsigned smax[1024];                   // d <= 1024
+    for (int j = threadIdx.x; j < d; j += blockDim.x) smax[j] = 0u;
+    __syncthreads();
     unsigned mx[4] = {0u, 0u, 0u, 0u};
     unsigned bad = 0;
     if (lane < lanes) {
@@ -572,10 +575,15 @@ fx_colmax_vec_kernel(const float* __restrict__ X, int64_t n, int d, unsigned* __
                 }
             }
         }
+        // the block's maxima first: one global atomic per column and block (per thread, the
+        // 64 columns of C3 took ~19k same-address atomics each)
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-            if (mx[e]) atomicMax(&amax[4 * g + e], mx[e]);
+            if (mx[e]) atomicMax(&smax[4 * g + e], mx[e]);
     }
+    __syncthreads();
+    for (int j = threadIdx.x; j < d; j += blockDim.x)
+        if (smax[j]) atomicMax(&amax[j], smax[j]);
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&flags[2], 1);
 }
 __global__ void fx_colmax_kernel(const float* __restrict__ X, int64_t n, int d,

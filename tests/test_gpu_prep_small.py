@@ -101,3 +101,17 @@ def test_small_d_assign_equals_register_tiled(d, dist, k, monkeypatch):
     C0 = X[rng.choice(n, k, replace=False)].copy()
     a, b = _both(monkeypatch, X, C0, dist, "minmax", False, 5, env="MPK_SIMT_NO_SMALL")
     _same(a, b)
+
+
+@pytest.mark.parametrize("d,norm,dist", [(64, "zscore", "fp16"), (3, "minmax", "fp16"),
+                                         (32, "minmax", "e5m2"), (200, "zscore", "bf16")])
+def test_warp_combine_equals_thread_combine(d, norm, dist, monkeypatch):
+    """The normalisation statistics' cross-block combine (O1): one warp per column staging the
+    partials in shared memory vs one thread per column (MPK_COMBINE_THREAD=1). Same additions
+    in the same block order: the transform, and so the whole fit, bit-identical."""
+    rng = np.random.default_rng(30 + d)
+    n = 300_000 if d <= 64 else 60_000
+    X = (rng.standard_normal((n, d)) * 5.0 + 100.0).astype(np.float32)
+    C0 = X[rng.choice(n, 16, replace=False)].copy()
+    a, b = _both(monkeypatch, X, C0, dist, norm, False, 3, env="MPK_COMBINE_THREAD")
+    _same(a, b)

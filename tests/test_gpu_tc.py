@@ -105,6 +105,18 @@ def test_tc_deep_row_blocks_one_tile(dist, guard, shape, monkeypatch):
     _assign_vs_oracle(n, d, k, dist, guard, n + k, want_variant=2)
 
 
+@pytest.mark.parametrize("dist", ["fp16", "bf16"])
+@pytest.mark.parametrize("shape", [(150_001, 200, 16), (150_001, 256, 40)])
+def test_tc_row_block_groups_with_few_row_slots(dist, shape, monkeypatch):
+    """512-byte operand rows leave room for only 3 X~ row-block slots, fewer than a group of
+    4 row-blocks per accumulator (k <= 64): the plan halves the group (k_assign_tc2.cu
+    pair_plan) — before, the MMA issuer waited for a slot that no one could free. Padded columns
+    (d = 200 -> d_pad = 256), many row-blocks per CTA pair, against the oracle."""
+    _set_kind(monkeypatch, 2)
+    n, d, k = shape
+    _assign_vs_oracle(n, d, k, dist, False, n + d, want_variant=2)
+
+
 @pytest.mark.parametrize("dist,shape", [("fp16", (200_003, 64, 256)), ("e5m2", (120_001, 32, 64))])
 def test_tc_one_tile_alternation_equals_column_split(dist, shape, monkeypatch):
     """The row-block alternation and the column split (MPK_PAIR_DBG bit 5) fold the same values
