@@ -1037,6 +1037,155 @@ prep_vec_kernel(const float* __restrict__ Xin, int64_t rows, int d, int guard,
     }
 }
 
+// prep_vec_kernel for d = 4G (G = 8, 16: d = 32, 64): a group of G lanes per row, 32/G rows per
+// warp side by side (a warp per row left the per-row work — shuffles, the fp64 division setup,
+// the stores — amortised over one or two columns per lane: issue-bound, ~150 us per million rows).
+// Same per-element arithmetic; ||x||^2 and the guard max reduced over the G lanes of the row.
+template <int DIST, bool NORM, int RPS, int G>
+__global__ void __launch_bounds__(256)
+prep_vecg_kernel(const float* __restrict__ Xin, int64_t rows, int d, int guard,
+                float* __restrict__ norms, float* __restrict__ scales,
+                typename low_type<DIST>::T* __restrict__ Xl,
+                unsigned long long* __restrict__ census, float* __restrict__ Xout,
+                const double* __restrict__ shift, const double* __restrict__ scale,
+                unsigned* __restrict__ amax, int* __restrict__ flags) {
+    using L = typename low_type<DIST>::T;
+    constexpr bool same = DIST == KMEANS_FP32;
+    constexpr int V = 1, PW = 32 / G;
+    const int wl = threadIdx.x & 31;
+    const int lane = wl % G, sub = wl / G;
+    // amax != nullptr: also the per-column max |x| of the (normalised) rows and flags[2] |= 1 on
+    // a non-finite value, for the fixed-point update (k_update.cu FX) — saves it a pass over X
+    unsigned mx[V][4] = {};
+    unsigned bad = 0;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double sh[V][4], sc[V][4], rc[V][4];
+#pragma unroll
+    for (int w = 0; w < V; ++w)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int c = 128 * w + 4 * lane + e;
+            sh[w][e] = NORM ? shift[c] : 0.0;
+            sc[w][e] = NORM ? scale[c] : 1.0;
+            rc[w][e] = 1.0 / sc[w][e];
+        }
+    unsigned n_nonfinite = 0, n_under = 0;
+    const int64_t nrb = (rows + PW - 1) / PW;         // row-blocks of PW rows, one per warp step
+    for (int64_t i = warp; i < nrb; i += RPS * nwarps) {
+        float4 xv[RPS][V];
+#pragma unroll
+        for (int r = 0; r < RPS; ++r) {
+            const int64_t ir = (i + r * nwarps) * PW + sub;
+#pragma unroll
+            for (int w = 0; w < V; ++w)
+                xv[r][w] = ir < rows ? __ldg(reinterpret_cast<const float4*>(Xin + ir * d + 128 * w) + lane)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int r = 0; r < RPS; ++r) {
+            if (i + r * nwarps >= nrb) break;         // warp-uniform
+            const int64_t ir = (i + r * nwarps) * PW + sub;
+            const bool ok = ir < rows;
+            float v[V][4];
+#pragma unroll
+            for (int w = 0; w < V; ++w) {
+                v[w][0] = xv[r][w].x; v[w][1] = xv[r][w].y; v[w][2] = xv[r][w].z; v[w][3] = xv[r][w].w;
+                if (NORM) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        v[w][e] = __double2float_rn(div_rn((double)v[w][e] - sh[w][e], sc[w][e], rc[w][e]));
+                    if (ok) reinterpret_cast<float4*>(Xout + ir * d + 128 * w)[lane] =
+                        make_float4(v[w][0], v[w][1], v[w][2], v[w][3]);
+                }
+            }
+            if (amax && ok) {
+#pragma unroll
+                for (int w = 0; w < V; ++w)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float a = fabsf(v[w][e]);
+                        if (!(a <= 3.402823466e38f)) bad = 1;
+                        else mx[w][e] = max(mx[w][e], __float_as_uint(a));
+                    }
+            }
+            float ss = 0.0f, cs = 0.0f;
+#pragma unroll
+            for (int w = 0; w < V; ++w)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float x = v[w][e];
+                    const float p = x * x;
+                    const float ep = fmaf(x, x, -p);
+                    const float t = ss + p;
+                    const float z = t - ss;
+                    cs += (ss - (t - z)) + (p - z) + ep;
+                    ss = t;
+                }
+            double acc = (double)ss + (double)cs;
+#pragma unroll
+            for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            float s = 1.0f;
+            if (guard && !same) {
+                float amax = 0.0f;
+#pragma unroll
+                for (int w = 0; w < V; ++w)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) amax = fmaxf(amax, fabsf(v[w][e]));
+#pragma unroll
+                for (int o = G / 2; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+                s = guard_scale(amax, guard);
+                if (s != 1.0f) {          // group-uniform: s is the row's
+#pragma unroll
+                    for (int w = 0; w < V; ++w)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) v[w][e] = v[w][e] / s;   // precision-u division
+                }
+            }
+            if (!ok) continue;
+            if (lane == 0) {
+                norms[ir] = __double2float_rn(acc);
+                if (scales) scales[ir] = s;
+            }
+#pragma unroll
+            for (int w = 0; w < V; ++w) {
+                L o[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    o[e] = rounder<DIST>::from(v[w][e]);
+                    if (!same) {
+                        if (is_nonfinite_low(o[e])) n_nonfinite++;
+                        else if (v[w][e] != 0.0f && is_zero_or_subnormal_low(o[e])) n_under++;
+                    }
+                }
+                store_low4<L>(Xl + ir * d + 128 * w + 4 * lane, o);
+            }
+        }
+    }
+    if (amax) {
+        __shared__ unsigned smx[256];
+        for (int t = threadIdx.x; t < d; t += blockDim.x) smx[t] = 0u;
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < V; ++w)
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (mx[w][e]) atomicMax(&smx[128 * w + 4 * lane + e], mx[w][e]);
+        __syncthreads();
+        for (int t = threadIdx.x; t < d; t += blockDim.x)
+            if (smx[t]) atomicMax(&amax[t], smx[t]);
+        if (__any_sync(0xffffffffu, bad) && wl == 0) atomicOr(&flags[2], 1);
+    }
+    if (census) {
+        const unsigned long long a = warp_sum((unsigned long long)n_nonfinite);
+        const unsigned long long b = warp_sum((unsigned long long)n_under);
+        if (wl == 0 && (a | b)) {
+            atomicAdd(&census[0], a);
+            atomicAdd(&census[1], b);
+        }
+    }
+}
+
 template <int DIST>
 static void prep_fast_launch(const float* Xin, int64_t rows, int d, int d_pad, int guard,
                              float* norms, float* scales, void* Xl, unsigned long long* census,
@@ -1077,6 +1226,18 @@ static void prep_fast_launch(const float* Xin, int64_t rows, int d, int d_pad, i
             else
                 prep_vec_kernel<DIST, false, 2, 2><<<g, 256, 0, s>>>(Xin, rows, d, guard, norms, scales,
                                                                      (L*)Xl, census, Xout, shift, scale, amax, flags);
+        }
+        if (amax_done) *amax_done = amax != nullptr;
+        return;
+    }
+    if (d == d_pad && (d == 32 || d == 64) && aligned && !getenv("MPK_PREP_NO_VECG")) {
+        // MPK_PREP_NO_VECG=1: prep_fast_kernel (A/B)
+        if (d == 32) {
+            if (shift) prep_vecg_kernel<DIST, true, 4, 8><<<g, 256, 0, s>>>(Xin, rows, d, guard, norms, scales, (L*)Xl, census, Xout, shift, scale, amax, flags);
+            else prep_vecg_kernel<DIST, false, 4, 8><<<g, 256, 0, s>>>(Xin, rows, d, guard, norms, scales, (L*)Xl, census, Xout, shift, scale, amax, flags);
+        } else {
+            if (shift) prep_vecg_kernel<DIST, true, 4, 16><<<g, 256, 0, s>>>(Xin, rows, d, guard, norms, scales, (L*)Xl, census, Xout, shift, scale, amax, flags);
+            else prep_vecg_kernel<DIST, false, 4, 16><<<g, 256, 0, s>>>(Xin, rows, d, guard, norms, scales, (L*)Xl, census, Xout, shift, scale, amax, flags);
         }
         if (amax_done) *amax_done = amax != nullptr;
         return;

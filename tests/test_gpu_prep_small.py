@@ -115,3 +115,23 @@ def test_warp_combine_equals_thread_combine(d, norm, dist, monkeypatch):
     C0 = X[rng.choice(n, 16, replace=False)].copy()
     a, b = _both(monkeypatch, X, C0, dist, norm, False, 3, env="MPK_COMBINE_THREAD")
     _same(a, b)
+
+
+@pytest.mark.parametrize("d,norm,dist,guard", [(64, "zscore", "fp16", False), (32, "none", "e5m2", True),
+                                               (64, "minmax", "bf16", "pow2"), (32, "zscore", "fp16", False)])
+def test_grouped_prep_matches_warp_per_row(d, norm, dist, guard, monkeypatch):
+    """prep_vecg_kernel (d = 32 / 64: G = d/4 lanes per row) against prep_fast_kernel
+    (MPK_PREP_NO_VECG=1). The normalised rows, the low operands and the guard scales are the
+    same per element; ||x||^2 is summed over the lanes in another grouping (both exact-product
+    compensated sums, rounded once to fp32), so a norm may differ by one ulp in rare rows:
+    labels equal up to near-ties, the fit's SSE to 1e-9."""
+    rng = np.random.default_rng(40 + d)
+    n = 200_003
+    X = (rng.standard_normal((n, d)) * 3.0 + 1.0).astype(np.float32)
+    C0 = X[rng.choice(n, 48, replace=False)].copy()
+    a, b = _both(monkeypatch, X, C0, dist, norm, guard, 4, env="MPK_PREP_NO_VECG")
+    assert a["iters"] == b["iters"] and a["rc"] == b["rc"]
+    assert (a["labels"] != b["labels"]).mean() <= 1e-4
+    assert abs(a["sse"] - b["sse"]) <= 1e-9 * abs(b["sse"])
+    for key in ("n_nonfinite", "n_underflow"):
+        assert a["stats"][key] == b["stats"][key], key
