@@ -1325,6 +1325,24 @@ cudaError_t launch_prep(int work, int dist, const void* Xw, int64_t rows, int d,
     if (work == KMEANS_FP64)
         return prep_dispatch<double>(dist, (const double*)Xw, rows, d, d_pad, guard,
                                      (double*)norms, (double*)scales, Xl, census, s);
+    // point rows of fp32 work with d = 32 / 64 / 128 / 256 (the final pass's fp16 operands, the
+    // rows of kmeans_assign): the lane-group / float4 kernels instead of a warp per row (E5M2 at
+    // C5 prepares its final-pass operands here). Centroid rows (k of them, every iteration)
+    // stay on prep_kernel. MPK_PREP_GENERIC=1: prep_kernel for all (A/B).
+    if (rows >= 65536 && d == d_pad && (d == 32 || d == 64 || d == 128 || d == 256) &&
+        (((uintptr_t)Xw | (uintptr_t)Xl) & 15) == 0 && !getenv("MPK_PREP_GENERIC")) {
+        const float* xi = (const float*)Xw;
+        float* nr = (float*)norms;
+        float* sc = (float*)scales;
+        switch (dist) {
+            case KMEANS_FP32: prep_fast_launch<KMEANS_FP32>(xi, rows, d, d_pad, guard, nr, sc, Xl, census, nullptr, nullptr, nullptr, s, nullptr, nullptr, nullptr); break;
+            case KMEANS_FP16: prep_fast_launch<KMEANS_FP16>(xi, rows, d, d_pad, guard, nr, sc, Xl, census, nullptr, nullptr, nullptr, s, nullptr, nullptr, nullptr); break;
+            case KMEANS_BF16: prep_fast_launch<KMEANS_BF16>(xi, rows, d, d_pad, guard, nr, sc, Xl, census, nullptr, nullptr, nullptr, s, nullptr, nullptr, nullptr); break;
+            case KMEANS_E5M2: prep_fast_launch<KMEANS_E5M2>(xi, rows, d, d_pad, guard, nr, sc, Xl, census, nullptr, nullptr, nullptr, s, nullptr, nullptr, nullptr); break;
+            default: return cudaErrorInvalidValue;
+        }
+        return cudaGetLastError();
+    }
     return prep_dispatch<float>(dist, (const float*)Xw, rows, d, d_pad, guard, (float*)norms,
                                 (float*)scales, Xl, census, s);
 }
